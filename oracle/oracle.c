@@ -1,0 +1,382 @@
+/*
+ * oracle.c — CPU ORACLE FOR THE FRONTIER BFS / BELLMAN-FORD HOT PATH.
+ *
+ * THIS IS TEST INFRASTRUCTURE, NOT PRODUCT CODE.  Only tests/, the smoke()
+ * entry point in __graft_entry__.py and bench.py's cpu_baseline / reference
+ * leg may load or execute it.  It shares no source, header, helper, table or
+ * constant with paper_1805_05208_b200/csrc (the CUDA path); neither side
+ * includes or links the other.
+ *
+ * Everything here is plain, sequential, single-threaded C written to be
+ * checked against the paper by eye.  It implements the *definitions* of the
+ * outputs, not the paper's parallel algorithm, because both frontier methods
+ * reach exactly (bit for bit) the unique shortest-path distances:
+ *
+ *   BFS  (sec:benchmark "Breadth-First Search"):
+ *        D[v] = shortest-path (hop) distance from src to v, infinity if
+ *        unreachable.
+ *   Bellman-Ford (sec:benchmark "General-Weight SSSP"):
+ *        D[v] = shortest-path distance from src to v, infinity if
+ *        unreachable.  (The -infinity clause for reachable negative cycles
+ *        cannot arise: weights are unsigned; reading A13.)
+ *
+ * Graph representation (sec:prelims): CSR with
+ * offsets[n+1] (int64) and targets[m] (uint32), optional weights[m]
+ * (uint32; NULL = unit weights, reading A17).  Edges are followed
+ * u -> targets[e] for e in [offsets[u], offsets[u+1]) (reading A4).
+ *
+ * Sentinels (reading A2): unreachable = 0xFFFFFFFF in uint32 outputs,
+ * UINT64_MAX in the uint64 outputs of the weighted routines.
+ * Parent of src = src (reading A3).
+ *
+ * Functions:
+ *   oracle_bfs              — textbook FIFO-queue BFS.
+ *   oracle_dijkstra         — textbook Dijkstra with an indexed binary heap
+ *                             (decrease-key), uint64 accumulation.
+ *   oracle_bellman_ford     — textbook Bellman-Ford: repeated passes that
+ *                             relax every edge until a pass changes nothing
+ *                             (at most n-1 useful passes).
+ *   oracle_frontier_bellman_ford — the paper's frontier formulation
+ *                             (sec:algs "BFS, wBFS,
+ *                             Bellman-Ford"): each round relaxes only the
+ *                             out-edges of vertices whose distance dropped in
+ *                             the previous round; run sequentially.
+ *   oracle_check_bfs        — O(n+m) certificate for a BFS output.
+ *   oracle_check_sssp       — O(n+m) certificate for an SSSP output (w >= 1).
+ *   oracle_reached_edges    — sum of out-degrees of reached vertices (the
+ *                             TEPS numerator, reading A20).
+ *
+ * Error convention: 0 = OK, negative = error (see ORACLE_E* below).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORACLE_OK 0
+#define ORACLE_EINVAL -1
+#define ORACLE_ENOMEM -2
+#define ORACLE_ERANGE -3   /* a finite distance does not fit in uint32 */
+#define ORACLE_EFAIL -4    /* certificate violated; *bad holds a witness */
+#define ORACLE_ENA -5      /* certificate not applicable (a zero weight) */
+
+#define INF32 0xFFFFFFFFu
+#define INF64 UINT64_MAX
+
+static int check_args(int64_t n, const int64_t *off, const uint32_t *tgt,
+                      uint32_t src) {
+  if (n < 1 || off == NULL || (off[n] > 0 && tgt == NULL)) return ORACLE_EINVAL;
+  if ((int64_t)src >= n) return ORACLE_EINVAL;
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* BFS: FIFO queue.  dist/parent are caller-owned arrays of length n;       */
+/* parent may be NULL.                                                       */
+/* ------------------------------------------------------------------------ */
+int oracle_bfs(int64_t n, const int64_t *off, const uint32_t *tgt,
+               uint32_t src, uint32_t *dist, uint32_t *parent) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (dist == NULL) return ORACLE_EINVAL;
+  uint32_t *queue = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+  if (!queue) return ORACLE_ENOMEM;
+  for (int64_t v = 0; v < n; v++) {
+    dist[v] = INF32;
+    if (parent) parent[v] = INF32;
+  }
+  int64_t head = 0, tail = 0;
+  dist[src] = 0;
+  if (parent) parent[src] = src;
+  queue[tail++] = src;
+  while (head < tail) {
+    uint32_t u = queue[head++];
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      uint32_t v = tgt[e];
+      if (dist[v] == INF32) {
+        dist[v] = dist[u] + 1;
+        if (parent) parent[v] = u;
+        queue[tail++] = v;
+      }
+    }
+  }
+  free(queue);
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Dijkstra with an indexed binary min-heap keyed by dist (uint64).         */
+/* weights NULL = unit weights.  dist is uint64[n] (INF64 = unreachable),    */
+/* parent uint32[n] or NULL.                                                 */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  uint32_t *heap;    /* heap[i] = vertex */
+  int64_t *pos;      /* pos[v] = index in heap, -1 if absent */
+  const uint64_t *key;
+  int64_t size;
+} heap_t;
+
+static void heap_swap(heap_t *h, int64_t i, int64_t j) {
+  uint32_t a = h->heap[i], b = h->heap[j];
+  h->heap[i] = b;
+  h->heap[j] = a;
+  h->pos[b] = i;
+  h->pos[a] = j;
+}
+
+static void heap_up(heap_t *h, int64_t i) {
+  while (i > 0) {
+    int64_t p = (i - 1) / 2;
+    if (h->key[h->heap[p]] <= h->key[h->heap[i]]) break;
+    heap_swap(h, i, p);
+    i = p;
+  }
+}
+
+static void heap_down(heap_t *h, int64_t i) {
+  for (;;) {
+    int64_t l = 2 * i + 1, r = l + 1, s = i;
+    if (l < h->size && h->key[h->heap[l]] < h->key[h->heap[s]]) s = l;
+    if (r < h->size && h->key[h->heap[r]] < h->key[h->heap[s]]) s = r;
+    if (s == i) break;
+    heap_swap(h, i, s);
+    i = s;
+  }
+}
+
+int oracle_dijkstra(int64_t n, const int64_t *off, const uint32_t *tgt,
+                    const uint32_t *w, uint32_t src, uint64_t *dist,
+                    uint32_t *parent) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (dist == NULL) return ORACLE_EINVAL;
+  heap_t h;
+  h.heap = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+  h.pos = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+  char *done = (char *)calloc((size_t)n, 1);
+  if (!h.heap || !h.pos || !done) {
+    free(h.heap); free(h.pos); free(done);
+    return ORACLE_ENOMEM;
+  }
+  h.key = dist;
+  h.size = 0;
+  for (int64_t v = 0; v < n; v++) {
+    dist[v] = INF64;
+    h.pos[v] = -1;
+    if (parent) parent[v] = INF32;
+  }
+  dist[src] = 0;
+  if (parent) parent[src] = src;
+  h.heap[0] = src;
+  h.pos[src] = 0;
+  h.size = 1;
+  while (h.size > 0) {
+    uint32_t u = h.heap[0];
+    heap_swap(&h, 0, h.size - 1);
+    h.size--;
+    h.pos[u] = -1;
+    if (h.size > 0) heap_down(&h, 0);
+    done[u] = 1;
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      uint32_t v = tgt[e];
+      if (done[v]) continue;
+      uint64_t nd = dist[u] + (w ? (uint64_t)w[e] : 1u);
+      if (nd < dist[v]) {
+        dist[v] = nd;
+        if (parent) parent[v] = u;
+        if (h.pos[v] < 0) {
+          h.heap[h.size] = v;
+          h.pos[v] = h.size;
+          h.size++;
+        }
+        heap_up(&h, h.pos[v]);
+      }
+    }
+  }
+  free(h.heap); free(h.pos); free(done);
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Textbook Bellman-Ford: relax all edges, pass after pass, until no change.*/
+/* With non-negative weights at most n-1 passes change anything; a change in*/
+/* pass n would mean a negative cycle, impossible here (returns EINVAL).    */
+/* ------------------------------------------------------------------------ */
+int oracle_bellman_ford(int64_t n, const int64_t *off, const uint32_t *tgt,
+                        const uint32_t *w, uint32_t src, uint64_t *dist,
+                        int64_t *passes) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (dist == NULL) return ORACLE_EINVAL;
+  for (int64_t v = 0; v < n; v++) dist[v] = INF64;
+  dist[src] = 0;
+  int64_t pass = 0;
+  for (;;) {
+    int changed = 0;
+    for (int64_t u = 0; u < n; u++) {
+      if (dist[u] == INF64) continue;
+      for (int64_t e = off[u]; e < off[u + 1]; e++) {
+        uint64_t nd = dist[u] + (w ? (uint64_t)w[e] : 1u);
+        if (nd < dist[tgt[e]]) {
+          dist[tgt[e]] = nd;
+          changed = 1;
+        }
+      }
+    }
+    pass++;
+    if (!changed) break;
+    if (pass > n) return ORACLE_EINVAL;
+  }
+  if (passes) *passes = pass;
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* The paper's frontier Bellman-Ford, run sequentially:    */
+/* frontier F = {src}; each round, for u in F and each edge (u,v,w), write  */
+/* D[v] = min(D[v], D[u]+w) (the priority-write); v joins the next frontier */
+/* iff the write lowered D[v].  Stop when the frontier is empty.  The next  */
+/* frontier is a set (a vertex is added once per round).                    */
+/* ------------------------------------------------------------------------ */
+int oracle_frontier_bellman_ford(int64_t n, const int64_t *off,
+                                 const uint32_t *tgt, const uint32_t *w,
+                                 uint32_t src, uint64_t *dist,
+                                 int64_t *rounds) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (dist == NULL) return ORACLE_EINVAL;
+  uint32_t *cur = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+  uint32_t *nxt = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+  char *in_next = (char *)calloc((size_t)n, 1);
+  if (!cur || !nxt || !in_next) {
+    free(cur); free(nxt); free(in_next);
+    return ORACLE_ENOMEM;
+  }
+  for (int64_t v = 0; v < n; v++) dist[v] = INF64;
+  dist[src] = 0;
+  int64_t fc = 1, r = 0;
+  cur[0] = src;
+  while (fc > 0) {
+    if (r >= n) { /* more than n rounds: impossible for w >= 0 */
+      free(cur); free(nxt); free(in_next);
+      return ORACLE_EINVAL;
+    }
+    int64_t nc = 0;
+    for (int64_t i = 0; i < fc; i++) {
+      uint32_t u = cur[i];
+      for (int64_t e = off[u]; e < off[u + 1]; e++) {
+        uint32_t v = tgt[e];
+        uint64_t nd = dist[u] + (w ? (uint64_t)w[e] : 1u);
+        if (nd < dist[v]) {
+          dist[v] = nd;
+          if (!in_next[v]) {
+            in_next[v] = 1;
+            nxt[nc++] = v;
+          }
+        }
+      }
+    }
+    for (int64_t i = 0; i < nc; i++) in_next[nxt[i]] = 0;
+    uint32_t *t = cur; cur = nxt; nxt = t;
+    fc = nc;
+    r++;
+  }
+  if (rounds) *rounds = r;
+  free(cur); free(nxt); free(in_next);
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Certificates (independent of every routine above).                       */
+/*                                                                          */
+/* BFS: (1) dist[src]=0; (2) for every edge u->v with dist[u] finite,       */
+/* dist[v] <= dist[u]+1; (3) every reached v != src has a tight in-edge     */
+/* u->v with dist[u]+1 == dist[v] — and, if parent is given, that edge is    */
+/* parent[v]->v; (4) parent[src]=src and parent[v]=INF iff dist[v]=INF.     */
+/* (1)+(2) give dist <= true distance; (3) gives a path of length dist[v],  */
+/* so dist >= true distance.  Hence dist is exact and parents are valid.    */
+/* On failure *bad = a witness vertex.                                      */
+/* ------------------------------------------------------------------------ */
+int oracle_check_bfs(int64_t n, const int64_t *off, const uint32_t *tgt,
+                     uint32_t src, const uint32_t *dist,
+                     const uint32_t *parent, int64_t *bad) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (dist == NULL) return ORACLE_EINVAL;
+  int64_t dummy;
+  if (!bad) bad = &dummy;
+  *bad = -1;
+  if (dist[src] != 0) { *bad = src; return ORACLE_EFAIL; }
+  if (parent && parent[src] != src) { *bad = src; return ORACLE_EFAIL; }
+  char *ok = (char *)calloc((size_t)n, 1);
+  if (!ok) return ORACLE_ENOMEM;
+  for (int64_t u = 0; u < n; u++) {
+    if (dist[u] == INF32) continue;
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      uint32_t v = tgt[e];
+      if ((uint64_t)dist[v] > (uint64_t)dist[u] + 1) {
+        *bad = v; free(ok); return ORACLE_EFAIL;
+      }
+      if ((uint64_t)dist[u] + 1 == (uint64_t)dist[v] &&
+          (parent == NULL || parent[v] == (uint32_t)u))
+        ok[v] = 1;
+    }
+  }
+  for (int64_t v = 0; v < n; v++) {
+    if (v == (int64_t)src) continue;
+    if (dist[v] == INF32) {
+      if (parent && parent[v] != INF32) { *bad = v; free(ok); return ORACLE_EFAIL; }
+    } else if (!ok[v]) {
+      *bad = v; free(ok); return ORACLE_EFAIL;
+    }
+  }
+  free(ok);
+  return ORACLE_OK;
+}
+
+/* SSSP with all weights >= 1 (weights NULL = unit): (1) dist[src]=0;       */
+/* (2) every edge with dist[u] finite has dist[v] <= dist[u]+w; (3) every   */
+/* reached v != src has a tight in-edge dist[u]+w == dist[v].  With w >= 1  */
+/* tight edges strictly decrease dist, so following them backwards ends at  */
+/* src: dist[v] is a real path length.  Returns ORACLE_ENA if some weight   */
+/* is 0 (the certificate then proves nothing).                              */
+int oracle_check_sssp(int64_t n, const int64_t *off, const uint32_t *tgt,
+                      const uint32_t *w, uint32_t src, const uint32_t *dist,
+                      int64_t *bad) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (dist == NULL) return ORACLE_EINVAL;
+  int64_t dummy;
+  if (!bad) bad = &dummy;
+  *bad = -1;
+  int64_t m = off[n];
+  if (w)
+    for (int64_t e = 0; e < m; e++)
+      if (w[e] == 0) return ORACLE_ENA;
+  if (dist[src] != 0) { *bad = src; return ORACLE_EFAIL; }
+  char *ok = (char *)calloc((size_t)n, 1);
+  if (!ok) return ORACLE_ENOMEM;
+  for (int64_t u = 0; u < n; u++) {
+    if (dist[u] == INF32) continue;
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      uint32_t v = tgt[e];
+      uint64_t nd = (uint64_t)dist[u] + (w ? (uint64_t)w[e] : 1u);
+      if ((uint64_t)dist[v] > nd) { *bad = v; free(ok); return ORACLE_EFAIL; }
+      if ((uint64_t)dist[v] == nd) ok[v] = 1;
+    }
+  }
+  for (int64_t v = 0; v < n; v++) {
+    if (v == (int64_t)src || dist[v] == INF32) continue;
+    if (!ok[v]) { *bad = v; free(ok); return ORACLE_EFAIL; }
+  }
+  free(ok);
+  return ORACLE_OK;
+}
+
+/* TEPS numerator: sum of out-degrees over vertices with finite dist.       */
+int64_t oracle_reached_edges(int64_t n, const int64_t *off,
+                             const uint32_t *dist) {
+  int64_t s = 0;
+  for (int64_t v = 0; v < n; v++)
+    if (dist[v] != INF32) s += off[v + 1] - off[v];
+  return s;
+}

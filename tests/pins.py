@@ -1,0 +1,127 @@
+"""Independent pins for the oracle: closed forms, brute force, Floyd–Warshall.
+
+None of this calls oracle/; each function is derived from the mathematics of
+the graph family, not from a BFS or relaxation loop (except brute force, which
+enumerates every simple path and so needs no shortest-path algorithm at all).
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+INF = 0xFFFFFFFF
+
+
+def ring_dist(a, b, L):
+    d = np.abs(np.asarray(a, np.int64) - np.asarray(b, np.int64))
+    return np.minimum(d, L - d)
+
+
+def torus_dist(L: int, src: int):
+    """d(v) = sum over the 3 dimensions of the ring distance (id = x + L(y + Lz))."""
+    ids = np.arange(L ** 3, dtype=np.int64)
+    sx, sy, sz = src % L, (src // L) % L, src // (L * L)
+    return (ring_dist(ids % L, sx, L) + ring_dist((ids // L) % L, sy, L)
+            + ring_dist(ids // (L * L), sz, L)).astype(np.uint32)
+
+
+def ring_shells(L: int):
+    """Number of ring vertices at ring distance k from a fixed vertex, k = 0..L//2."""
+    s = np.zeros(L // 2 + 1, np.int64)
+    for k in range(L):
+        s[min(k, L - k)] += 1
+    return s
+
+
+def torus_level_counts(L: int):
+    """Per-level vertex counts of BFS on the L^3 torus = triple convolution of shells."""
+    s = ring_shells(L)
+    return np.convolve(np.convolve(s, s), s)
+
+
+def torus_ecc(L: int) -> int:
+    return 3 * (L // 2)
+
+
+def path_graph(n: int):
+    edges = [(i, i + 1) for i in range(n - 1)]
+    return edges
+
+
+def grid_dist(a: int, b: int, src: int):
+    ids = np.arange(a * b)
+    return (np.abs(ids % a - src % a) + np.abs(ids // a - src // a)).astype(np.uint32)
+
+
+def grid_edges(a: int, b: int):
+    e = []
+    for y in range(b):
+        for x in range(a):
+            v = x + a * y
+            if x + 1 < a:
+                e.append((v, v + 1))
+            if y + 1 < b:
+                e.append((v, v + a))
+    return e
+
+
+def recursive_tree(n: int, seed: int):
+    """Random recursive tree: parent(i) = h(i) mod i.  Returns (edges, parent, depth)
+    with depth computed by the recurrence depth[i] = depth[parent[i]] + 1."""
+    rng = np.random.default_rng(seed)
+    par = np.zeros(n, np.int64)
+    depth = np.zeros(n, np.int64)
+    for i in range(1, n):
+        par[i] = rng.integers(0, i)
+        depth[i] = depth[par[i]] + 1
+    return [(int(par[i]), i) for i in range(1, n)], par, depth
+
+
+def brute_force_sssp(n: int, offsets, targets, weights, src: int):
+    """Minimum over ALL simple src->v paths of the path weight (n <= 9)."""
+    adj = {u: [(int(targets[e]), 1 if weights is None else int(weights[e]))
+               for e in range(offsets[u], offsets[u + 1])] for u in range(n)}
+    best = [None] * n
+    best[src] = 0
+
+    def dfs(u, acc, seen):
+        for v, w in adj[u]:
+            if v in seen:
+                continue
+            if best[v] is None or acc + w < best[v]:
+                best[v] = acc + w
+            seen.add(v)
+            dfs(v, acc + w, seen)
+            seen.remove(v)
+
+    dfs(src, 0, {src})
+    return np.array([INF if b is None else b for b in best], np.uint64)
+
+
+def floyd_warshall(n: int, offsets, targets, weights):
+    """All-pairs shortest paths by Floyd–Warshall in float (exact for small ints)."""
+    D = np.full((n, n), np.inf)
+    np.fill_diagonal(D, 0.0)
+    for u in range(n):
+        for e in range(offsets[u], offsets[u + 1]):
+            w = 1.0 if weights is None else float(weights[e])
+            D[u, targets[e]] = min(D[u, targets[e]], w)
+    for k in range(n):
+        D = np.minimum(D, D[:, k:k + 1] + D[k:k + 1, :])
+    return D
+
+
+def fw_row_u32(D, src):
+    row = D[src]
+    out = np.full(row.shape, INF, np.uint64)
+    fin = np.isfinite(row)
+    out[fin] = row[fin].astype(np.uint64)
+    return out
+
+
+def all_small_graphs(n: int):
+    """Every undirected simple graph on n labelled vertices (n <= 4)."""
+    pairs = list(itertools.combinations(range(n), 2))
+    for mask in range(1 << len(pairs)):
+        yield [p for i, p in enumerate(pairs) if mask >> i & 1]

@@ -1,0 +1,281 @@
+"""Pins for oracle/ (CPU only).  Each test checks the oracle against something
+other than itself: closed forms, brute force over all simple paths,
+Floyd–Warshall, a printed paper value, or an independent certificate — chosen so
+a dropped term, wrong sign/index or transposed operand in oracle.c fails one."""
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from golden_io import read_examples, read_kv
+from pins import (INF, all_small_graphs, brute_force_sssp, floyd_warshall, fw_row_u32,
+                  grid_dist, grid_edges, path_graph, recursive_tree, ring_dist, torus_dist,
+                  torus_ecc, torus_level_counts)
+
+
+
+
+# ---- BFS: closed forms ------------------------------------------------------------
+
+@pytest.mark.parametrize("n,src", [(1, 0), (2, 1), (7, 0), (7, 3), (50, 49)])
+def test_bfs_path_closed_form(n, src):
+    off, tgt = graphgen.from_edge_list(n, path_graph(n)) if n > 1 else (np.zeros(2, np.int64), np.zeros(0, np.uint32))
+    d, p = oracle.bfs(off, tgt, src)
+    assert (d == np.abs(np.arange(n) - src)).all()
+    # a path is a tree: parents are unique
+    exp_p = np.array([src if v == src else (v + 1 if v < src else v - 1) for v in range(n)])
+    assert (p == exp_p).all()
+
+
+@pytest.mark.parametrize("n,src", [(3, 0), (8, 5), (9, 2)])
+def test_bfs_cycle_closed_form(n, src):
+    edges = [(i, (i + 1) % n) for i in range(n)]
+    off, tgt = graphgen.from_edge_list(n, edges)
+    d, _ = oracle.bfs(off, tgt, src)
+    assert (d == ring_dist(np.arange(n), src, n)).all()
+
+
+def test_bfs_grid_manhattan():
+    a, b = 9, 6
+    off, tgt = graphgen.from_edge_list(a * b, grid_edges(a, b))
+    for src in (0, 13, a * b - 1):
+        d, _ = oracle.bfs(off, tgt, src)
+        assert (d == grid_dist(a, b, src)).all()
+
+
+@pytest.mark.parametrize("L", [3, 4, 5, 8])
+def test_bfs_torus_closed_form(L):
+    off, tgt = graphgen.torus3d(L)
+    for src in (0, L ** 3 // 2 + 1):
+        d, p = oracle.bfs(off, tgt, src)
+        assert (d == torus_dist(L, src)).all()
+        assert int(d.max()) == torus_ecc(L)
+        assert (np.bincount(d) == torus_level_counts(L)).all()
+        assert oracle.check_bfs(off, tgt, src, d, p)[0]
+
+
+def test_torus_closed_form_matches_paper_row():
+    """PAPER.md:2132 prints diam 1500 for the 1000^3 torus with 6e9 edges; the closed
+    form eccentricity 3*floor(L/2) and level counts must reproduce it."""
+    row = read_kv("paper_torus_row.txt")
+    L = row["side"]
+    assert L ** 3 == row["vertices"] and row["degree"] * L ** 3 == row["edges"]
+    assert torus_ecc(L) == row["diam"]
+    lv = torus_level_counts(L)
+    assert len(lv) - 1 == row["diam"] and lv.sum() == row["vertices"] and lv[-1] == 1
+
+
+def test_torus_c3_level_histogram_closed_form():
+    """c3 (L=256): 385 levels summing to 2^24; shells 1, 6, 18, 38, 66; peak at 192."""
+    lv = torus_level_counts(256)
+    assert len(lv) == 385 and lv.sum() == 1 << 24
+    assert list(lv[:5]) == [1, 6, 18, 38, 66]
+    assert int(lv.argmax()) == 192
+
+
+def test_bfs_complete_and_star_exact_parents():
+    n = 9
+    off, tgt = graphgen.from_edge_list(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+    d, p = oracle.bfs(off, tgt, 4)
+    assert (d == np.where(np.arange(n) == 4, 0, 1)).all() and (p == 4).all()
+    off, tgt = graphgen.from_edge_list(n, [(0, i) for i in range(1, n)])
+    d, p = oracle.bfs(off, tgt, 3)
+    assert list(d) == [1, 2, 2, 0, 2, 2, 2, 2, 2]
+    assert list(p) == [3, 0, 0, 3, 0, 0, 0, 0, 0]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_bfs_tree_exact(seed):
+    n = 300
+    edges, par, depth = recursive_tree(n, seed)
+    off, tgt = graphgen.from_edge_list(n, edges)
+    d, p = oracle.bfs(off, tgt, 0)
+    assert (d == depth).all()
+    assert p[0] == 0 and (p[1:] == par[1:]).all()
+
+
+def test_bfs_disconnected_and_directed():
+    off, tgt = graphgen.from_edge_list(5, [(0, 1), (1, 2), (3, 4)], symmetric=False)
+    d, p = oracle.bfs(off, tgt, 1)
+    assert list(d) == [INF, 0, 1, INF, INF]
+    assert list(p) == [INF, 1, 1, INF, INF]
+
+
+# ---- BFS vs brute force / Floyd–Warshall ------------------------------------------
+
+def test_bfs_all_graphs_on_4_vertices_brute_force():
+    for edges in all_small_graphs(4):
+        off, tgt = graphgen.from_edge_list(4, edges) if edges else (np.zeros(5, np.int64), np.zeros(0, np.uint32))
+        for src in range(4):
+            d, p = oracle.bfs(off, tgt, src)
+            bf = brute_force_sssp(4, off, tgt, None, src)
+            assert (d.astype(np.uint64) == bf).all()
+            assert oracle.check_bfs(off, tgt, src, d, p)[0]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_bfs_random_brute_force_and_fw(seed):
+    n = 8
+    off, tgt = graphgen.random_graph(n, 0.3, seed, symmetric=seed % 2 == 0)
+    D = floyd_warshall(n, off, tgt, None)
+    for src in range(n):
+        d, _ = oracle.bfs(off, tgt, src)
+        assert (d.astype(np.uint64) == brute_force_sssp(n, off, tgt, None, src)).all()
+        assert (d.astype(np.uint64) == fw_row_u32(D, src)).all()
+
+
+def test_bfs_fw_medium():
+    n = 200
+    off, tgt = graphgen.random_graph(n, 0.015, 11, symmetric=False)
+    D = floyd_warshall(n, off, tgt, None)
+    for src in (0, 77, 199):
+        d, p = oracle.bfs(off, tgt, src)
+        assert (d.astype(np.uint64) == fw_row_u32(D, src)).all()
+        assert oracle.check_bfs(off, tgt, src, d, p)[0]
+
+
+# ---- weighted: brute force, FW, closed forms ---------------------------------------
+
+@pytest.mark.parametrize("seed", range(8))
+def test_sssp_brute_force(seed):
+    n = 8
+    off, tgt = graphgen.random_graph(n, 0.35, 100 + seed, symmetric=seed % 2 == 1)
+    w = graphgen.pair_weights(off, tgt, seed, 9) if seed % 3 else \
+        (np.arange(tgt.shape[0]) % 7 + 1).astype(np.uint32)  # asymmetric weights too
+    for src in range(n):
+        bf = brute_force_sssp(n, off, tgt, w, src)
+        d64, _ = oracle.dijkstra64(off, tgt, w, src)
+        b64, _ = oracle.bellman_ford64(off, tgt, w, src)
+        f64, _ = oracle.frontier_bellman_ford64(off, tgt, w, src)
+        bf = np.where(bf == INF, oracle.INF64, bf)
+        assert (d64 == bf).all() and (b64 == bf).all() and (f64 == bf).all()
+
+
+def test_sssp_fw_medium_and_certificate():
+    n = 150
+    off, tgt = graphgen.random_graph(n, 0.03, 5, symmetric=True)
+    w = graphgen.pair_weights(off, tgt, 9, 7)
+    D = floyd_warshall(n, off, tgt, w)
+    for src in (0, 42):
+        d, p = oracle.dijkstra(off, tgt, w, src, want_parent=True)
+        assert (d.astype(np.uint64) == fw_row_u32(D, src)).all()
+        assert oracle.check_sssp(off, tgt, w, src, d)[0]
+        # Dijkstra's own parent edge is tight (equality on the parent edge)
+        reached = (d != INF) & (np.arange(n) != src)
+        for v in np.nonzero(reached)[0]:
+            u = p[v]
+            es = range(off[u], off[u + 1])
+            assert any(tgt[e] == v and int(d[u]) + int(w[e]) == int(d[v]) for e in es)
+
+
+def test_sssp_weighted_path_prefix_sums():
+    n = 40
+    rng = np.random.default_rng(3)
+    ws = rng.integers(1, 30, n - 1)
+    off, tgt, w = graphgen.from_edge_list(n, path_graph(n), True, list(ws))
+    d, _ = oracle.dijkstra(off, tgt, w, 0)
+    assert (d == np.concatenate([[0], np.cumsum(ws)])).all()
+    d2, _ = oracle.dijkstra(off, tgt, w, n - 1)
+    assert (d2 == np.concatenate([np.cumsum(ws[::-1])[::-1], [0]])).all()
+
+
+@pytest.mark.parametrize("c", [1, 7])
+def test_sssp_constant_weight_torus(c):
+    L = 6
+    off, tgt = graphgen.torus3d(L)
+    w = np.full(tgt.shape, c, np.uint32)
+    d, _ = oracle.dijkstra(off, tgt, w, 5)
+    assert (d == c * torus_dist(L, 5)).all()
+    f, rounds = oracle.frontier_bellman_ford64(off, tgt, w, 5)
+    assert (f == d).all() and rounds == torus_ecc(L) + 1
+
+
+def test_unit_weights_equal_bfs():
+    off, tgt = graphgen.rmat_graph(10, 1 << 13, 7, 0.57, 0.19, 0.19)
+    d, _ = oracle.bfs(off, tgt, 0)
+    for w in (None, np.ones(tgt.shape, np.uint32)):
+        assert (oracle.dijkstra(off, tgt, w, 0)[0] == d).all()
+        assert (oracle.narrow(oracle.frontier_bellman_ford64(off, tgt, w, 0)[0]) == d).all()
+
+
+def test_spec_examples():
+    for ex in read_examples():
+        if ex["kind"] == "bfs":
+            d, _ = oracle.bfs(ex["offsets"], ex["targets"], ex["src"])
+        else:
+            d, _ = oracle.dijkstra(ex["offsets"], ex["targets"], ex["weights"], ex["src"])
+        assert (d == ex["expected"]).all(), ex["line"]
+
+
+def test_narrow_overflow_and_zero_weight():
+    with pytest.raises(OverflowError):
+        oracle.narrow(np.array([0, 0xFFFFFFFF], np.uint64))
+    off, tgt = graphgen.from_edge_list(3, [(0, 1), (1, 2)])
+    w = np.array([0, 0, 1, 1], np.uint32)   # zero weights: oracle OK (reading A14)
+    d, _ = oracle.dijkstra(off, tgt, w, 0)
+    assert list(d) == [0, 0, 1]
+    with pytest.raises(ValueError):
+        oracle.check_sssp(off, tgt, w, 0, d)
+
+
+# ---- certificates detect plausible mistakes ------------------------------------
+
+def test_bfs_certificate_rejects_mutations():
+    off, tgt = graphgen.rmat_graph(12, 1 << 15, 3, 0.57, 0.19, 0.19)
+    d, p = oracle.bfs(off, tgt, 0)
+    assert oracle.check_bfs(off, tgt, 0, d, p)[0]
+    reached = np.nonzero((d != INF) & (d > 0))[0]
+    rng = np.random.default_rng(0)
+    for v in rng.choice(reached, 20, replace=False):
+        for delta in (-1, 1):
+            d2 = d.copy(); d2[v] = int(d[v]) + delta
+            assert not oracle.check_bfs(off, tgt, 0, d2, p)[0]
+        p2 = p.copy(); p2[v] = v            # not an in-neighbour one level closer
+        assert not oracle.check_bfs(off, tgt, 0, d, p2)[0]
+        # a same-level neighbour is a wrong parent
+        nbrs = tgt[off[v]:off[v + 1]]
+        same = nbrs[d[nbrs] == d[v]]
+        if same.size:
+            p3 = p.copy(); p3[v] = same[0]
+            assert not oracle.check_bfs(off, tgt, 0, d, p3)[0]
+    unreached = np.nonzero(d == INF)[0]
+    d4 = d.copy(); d4[unreached[0]] = 5
+    assert not oracle.check_bfs(off, tgt, 0, d4, None)[0]
+    d5 = d.copy(); d5[0] = 1
+    assert not oracle.check_bfs(off, tgt, 0, d5, p)[0]
+
+
+def test_sssp_certificate_rejects_mutations():
+    off, tgt = graphgen.rmat_graph(11, 1 << 14, 4, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 4, 11)
+    d, _ = oracle.dijkstra(off, tgt, w, 0)
+    assert oracle.check_sssp(off, tgt, w, 0, d)[0]
+    reached = np.nonzero((d != INF) & (d > 0))[0]
+    for v in reached[:: max(1, reached.size // 15)]:
+        for delta in (-1, 1):
+            d2 = d.copy(); d2[v] = int(d[v]) + delta
+            assert not oracle.check_sssp(off, tgt, w, 0, d2)[0]
+
+
+def test_oracle_rejects_bad_args():
+    off, tgt = graphgen.from_edge_list(3, [(0, 1)])
+    with pytest.raises(RuntimeError):
+        oracle.bfs(off, tgt, 3)
+    with pytest.raises(ValueError):
+        oracle.bfs(np.array([0, 5]), np.zeros(2, np.uint32), 0)
+
+
+def test_c1_oracle_self_consistent():
+    cfg = graphgen.CONFIGS["c1"]
+    off, tgt = graphgen.rmat_graph(cfg.levels, 1 << cfg.log_edges, cfg.graph_seed, *cfg.abc)
+    d, p = oracle.bfs(off, tgt, 0)
+    assert oracle.check_bfs(off, tgt, 0, d, p)[0]
+    # symmetric graph: |d(u) - d(v)| <= 1 across every edge (BASELINE.json north_star)
+    u = graphgen.edge_sources(off)
+    fin = d[u] != INF
+    assert (np.abs(d[u][fin].astype(np.int64) - d[tgt][fin].astype(np.int64)) <= 1).all()
+    w = graphgen.pair_weights(off, tgt, cfg.weight_seed, cfg.W)
+    dd, _ = oracle.dijkstra(off, tgt, w, 0)
+    f, _ = oracle.frontier_bellman_ford64(off, tgt, w, 0)
+    assert (oracle.narrow(f) == dd).all()
+    assert oracle.check_sssp(off, tgt, w, 0, dd)[0]
