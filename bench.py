@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py — GTEPS of libgbbs's frontier BFS / Bellman-Ford on one B200 per rank.
+
+Contract (task README + DESIGN.md §Measurement):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2] [--algo bfs|bf]
+One step = one pass of the hot path over the workload's batch: BFS (direction-
+optimising, T=20) from each of the config's seeded sources on the resident graph
+(default c2: 8 sources in the largest component of the medium rMAT graph).  The
+Bellman-Ford leg of the metric is measured in the same run on the same graph with
+weights in [1, floor(log2 n)] (reading A6) and reported under "bellman_ford".
+Multi-GPU = replicas: every rank runs the same batch on its
+own copy; value = total traversed edges of all ranks / max-over-ranks time.
+--impl reference times the CPU oracle (sequential C queue-BFS / Dijkstra) — the
+only place besides cpu_baseline where bench.py executes oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GTEPS per B200 for BFS and Bellman-Ford; achieved HBM GB/s vs roofline"
+INF = 0xFFFFFFFF
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--algo", default="bfs", choices=["bfs", "bf"])
+    ap.add_argument("--threshold", type=int, default=20)
+    ap.add_argument("--no-bf-leg", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no cpu baseline)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """Sample nvidia-smi clocks/throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs"), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def copy_bandwidth(torch):
+    """Stream copy, same method as MEASURED_PEAKS: 1 Gi bf16 copy_, best of 10."""
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda")
+    b = torch.empty_like(a)
+    best = 1e9
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); b.copy_(a); e1.record(); e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * (1 << 30) * 2 / (best * 1e-3) / 1e9
+
+
+def algorithmic_bytes(recs, n, m, algo):
+    """§8(d) per-round algorithmic bytes of offsets + targets + weights + frontier.
+
+    Push round: carried frontier entries read (v 4 + O 8 + base 8 B each), targets
+    4 B per edge (+4 B weight for BF), emitted entries: offsets 16 B read + 20 B
+    written.  Pull round: in-offsets 8 B per swept vertex + 8, 4 B per in-edge
+    loaded, visited bitmap n/8 read + n/8 written, plus emitted entries as above.
+    Returns (alg_bytes, state_bytes) — state (dist/parent) kept separate."""
+    alg = 0
+    for i, r in enumerate(recs):
+        acq = r["acquired"]
+        emit = 36 * acq  # offsets read + entry written
+        if r["dense"]:
+            alg += 8 * r["vertices_swept"] + 8 + 4 * r["edges_examined"] + 2 * ((n + 7) // 8) + emit
+        else:
+            per_edge = 8 if algo == "bf" else 4
+            alg += 20 * r["frontier"] + per_edge * r["frontier_edges"] + emit
+    state = 8 * n if algo == "bfs" else 4 * n
+    return alg, state
+
+
+def reached_edges(torch, off, d):
+    deg = off[1:] - off[:-1]
+    return int(deg[d != -1].sum())
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist_mod
+    from graphgen import device as gdev
+    from paper_1805_05208_b200 import gbbs
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist_mod.init_process_group("nccl", device_id=dev)
+
+    t0 = time.time()
+    want_w = (args.algo == "bf") or not args.no_bf_leg
+    G = gdev.build_config(args.workload, weights=want_w)
+    cfg = G["cfg"]
+    n, m = G["n"], G["m"]
+    g = gbbs.Graph(G["offsets"], G["targets"], G["weights"], symmetric=G["symmetric"])
+    setup_s = time.time() - t0
+    sources = G["sources"]
+    off = G["offsets"]
+    dist = torch.empty(n, dtype=torch.int32, device=dev)
+    par = torch.empty(n, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    opts = gbbs.make_opts(args.threshold, gbbs.GBBS_MODE_AUTO)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def one(src, algo, d=dist, p=par, stats=None):
+        if algo == "bfs":
+            g.bfs(src, d, p, stream=stream, opts=opts, stats=stats)
+        else:
+            g.bellman_ford(src, d, stream=stream, stats=stats)
+
+    # per-source traversed-edge counts (TEPS numerator, reading A20) and stats
+    per_src = {}
+    for algo in (["bfs", "bf"] if want_w else ["bfs"]):
+        for s in sources:
+            st = gbbs.make_stats(1 << 16)
+            one(s, algo, stats=st)
+            recs = gbbs.round_records(st)
+            alg, state = algorithmic_bytes(recs, n, m, algo)
+            per_src[(algo, s)] = dict(m_reach=reached_edges(torch, off, dist), rounds=st.rounds,
+                                      dense_rounds=st.dense_rounds, alg_bytes=alg, state_bytes=state,
+                                      relax=sum(r["frontier_edges"] for r in recs if not r["dense"]))
+
+    def timed(algo, steps, warmup, flush=True):
+        for _ in range(warmup):
+            for s in sources:
+                one(s, algo)
+        if world > 1:
+            dist_mod.barrier()
+        torch.cuda.synchronize()
+        evs = []
+        clocks = Clocks(local); clocks.start()
+        kms = []
+        for _ in range(steps):
+            if flush:
+                flush_buf.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for s in sources:
+                one(s, algo)
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        ck = clocks.stop()
+        if world > 1:
+            dist_mod.barrier()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        # kernel-only durations of the persistent traversal kernel (events inside libgbbs)
+        for s in sources:
+            if flush:
+                flush_buf.fill_(1)
+            st = gbbs.make_stats(0)
+            one(s, algo, stats=st)
+            kms.append(st.kernel_ms)
+        return ms, ck, kms
+
+    ms, clocks, kms = timed(args.algo, args.steps, args.warmup)
+    step_ms = float(np.mean(ms))
+    tmax = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist_mod.all_reduce(tmax, op=dist_mod.ReduceOp.MAX)
+    step_ms_max = float(tmax.item())
+    edges_step = sum(per_src[(args.algo, s)]["m_reach"] for s in sources)
+    value = world * edges_step / (step_ms_max * 1e-3) / 1e9
+
+    out = None
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        copy_gbs = copy_bandwidth(torch)
+        alg_bytes = sum(per_src[(args.algo, s)]["alg_bytes"] for s in sources)
+        kernel_ms = float(np.sum(kms))
+        achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+        # e2e: public API with pinned host output buffers (library copies D2H inside)
+        hd = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        hp = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        torch.cuda.synchronize()
+        e2e = []
+        for _ in range(max(1, min(args.steps, 5))):
+            t = time.perf_counter()
+            for s in sources:
+                if args.algo == "bfs":
+                    gbbs.gbbs_bfs(g.handle, s, hd.numpy(), hp.numpy(), stream=stream)
+                else:
+                    gbbs.gbbs_bellman_ford(g.handle, s, hd.numpy(), stream=stream)
+            e2e.append(time.perf_counter() - t)
+        e2e_s = float(np.median(e2e))
+        d2h = len(sources) * n * (8 if args.algo == "bfs" else 4)
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GTEPS",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(step_ms_max, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded counter-based rMAT/torus generators, DESIGN.md §Input recipe)",
+            "config": {"workload": f"{cfg.name}: {cfg.note}", "algo": args.algo,
+                       "n": n, "m": m, "sources": sources, "threshold_T": args.threshold,
+                       "traversals_per_step": len(sources), "edges_per_step": edges_step,
+                       "l2": "flushed (256 MB write) before every timed step; graph > L2",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": peak_src, "copy_gbs_same_run": round(copy_gbs, 1),
+                         "kernel": "gbbs_dev::traverse_kernel (persistent, one launch per traversal)",
+                         "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": round(kernel_ms, 4)},
+            "e2e": {"value": round(edges_step / e2e_s / 1e9, 3), "unit": "GTEPS",
+                    "h2d_bytes_per_step": 4 * len(sources), "d2h_bytes_per_step": d2h,
+                    "note": "gbbs_bfs with pinned host dist/parent; library copies D2H; "
+                            "sources travel as kernel arguments"},
+            "gpu_launches": args.steps * len(sources),
+            "clocks": clocks,
+            "per_source": [{"src": s, **{k: v for k, v in per_src[(args.algo, s)].items()}}
+                           for s in sources],
+            "setup_s": round(setup_s, 2),
+        }
+        if want_w and args.algo == "bfs" and not args.profile:
+            bms, bclk, bkms = timed("bf", max(1, args.steps // 2), 1)
+            be = sum(per_src[("bf", s)]["m_reach"] for s in sources)
+            brel = sum(per_src[("bf", s)]["relax"] for s in sources)
+            bt = float(np.mean(bms))
+            balg = sum(per_src[("bf", s)]["alg_bytes"] for s in sources)
+            out["bellman_ford"] = {
+                "value": round(be / (bt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective, reading A20)",
+                "relaxations_per_s": round(brel / (bt * 1e-3) / 1e9, 3), "ms_per_step": round(bt, 4),
+                "weights": f"[1,{cfg.W}] pair-hash (readings A5, A6)",
+                "roofline_frac": round(balg / (float(np.sum(bkms)) * 1e-3) / 1e9 / peak, 4),
+                "rounds": [per_src[("bf", s)]["rounds"] for s in sources]}
+        if not args.profile:
+            out["cpu_baseline"] = cpu_baseline(args, G["offsets"], G["targets"], sources, cfg)
+    g.close()
+    if world > 1:
+        dist_mod.destroy_process_group()
+    return out
+
+
+def cpu_baseline(args, off_dev, tgt_dev, sources, cfg):
+    """The oracle as it stands (sequential C queue-BFS), 1 core, bounded sample."""
+    import oracle
+    off = off_dev.cpu().numpy()
+    tgt = tgt_dev.cpu().numpy().view(np.uint32)
+    done, edges, t_all = [], 0, 0.0
+    for s in sources:
+        t = time.perf_counter()
+        d, _ = oracle.bfs(off, tgt, s)
+        dt = time.perf_counter() - t
+        edges += oracle.reached_edges(off, d)
+        t_all += dt
+        done.append(s)
+        if t_all > args.cpu_budget_s:
+            break
+    return {"value": round(edges / t_all / 1e9, 4), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+            "sample": f"oracle_bfs (sequential C FIFO BFS) from {len(done)} of {len(sources)} "
+                      f"sources of {cfg.name}, {t_all:.1f} s", "cpu": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" x{os.cpu_count()}"
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on the same workload (rank 0 only)."""
+    if rank != 0:
+        return None
+    import oracle
+    import graphgen
+    cfg = graphgen.CONFIGS[args.workload]
+    try:
+        from graphgen import device as gdev
+        import torch
+        G = gdev.build_config(cfg.name, weights=args.algo == "bf")
+        off = G["offsets"].cpu().numpy()
+        tgt = G["targets"].cpu().numpy().view(np.uint32)
+        w = G["weights"].cpu().numpy().view(np.uint32) if G["weights"] is not None else None
+        sources = G["sources"]
+        del G
+    except Exception:  # no GPU: build on the host (small configs only)
+        off, tgt = graphgen.rmat_graph(cfg.levels, 1 << cfg.log_edges, cfg.graph_seed, *cfg.abc,
+                                       symmetric=cfg.symmetric)
+        w = graphgen.pair_weights(off, tgt, cfg.weight_seed, cfg.W) if args.algo == "bf" else None
+        sources = graphgen.choose_sources(graphgen.largest_component(off, tgt), cfg.nsources,
+                                          cfg.source_seed) if cfg.sources == "lcc" else [0]
+    times, edges = [], 0
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    for step in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        e, used = 0, 0
+        for s in sources:
+            if args.algo == "bfs":
+                d, _ = oracle.bfs(off, tgt, s)
+            else:
+                d, _ = oracle.dijkstra(off, tgt, w, s)
+            e += oracle.reached_edges(off, d)
+            used += 1
+            if time.perf_counter() - t > budget:
+                break
+        dt = time.perf_counter() - t
+        if step >= args.warmup:
+            times.append(dt); edges += e
+    v = edges / sum(times) / 1e9
+    return {"metric": METRIC, "value": round(v, 4), "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * float(np.mean(times)), 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{cfg.name}: {cfg.note}", "algo": args.algo},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                             "sample": f"{used} of {len(sources)} sources per step (budget {budget:.0f} s)"},
+            "e2e": {"value": round(v, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        out = run_ours(args, rank, world, local)
+    if out is not None and rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/*
+ * gbbs.h — C ABI of libgbbs: frontier BFS and frontier Bellman-Ford on one
+ * NVIDIA B200 (sm_100a), after arxiv 1805.05208 (GBBS, "Theoretically
+ * Efficient Parallel Graph Algorithms Can Be Fast and Scalable").
+ *
+ * Citations are to /root/reference/PAPER.md lines ("P:<line>") with the
+ * section they fall in; SURVEY.md §8(b) is the design contract.
+ *
+ * The library implements the paper's edgeMap primitive (P:1851-1874,
+ * sec:prelims "Ligra, Ligra+, and Julienne") instantiated two ways:
+ *   - BFS: F = test-and-set acquire of unvisited neighbours (P:84-93,
+ *     sec:algs; TS semantics P:1821-1825);
+ *   - Bellman-Ford: F = priority-write of the minimum distance (P:93-97,
+ *     sec:algs; PW semantics P:1826-1831).
+ * Each round chooses a sparse (push over a vertex list, with the edge work cut
+ * into fixed-size blocks as in edgeMapBlocked) or dense (pull
+ * over in-edges with early exit) method from the number of edges
+ * incident to the frontier.
+ *
+ * Conventions common to every call:
+ *   - Status: 0 = GBBS_OK, negative = error.  No C++ exception crosses the
+ *     ABI.  gbbs_last_error() returns a thread-local message for the last
+ *     failing call on the calling thread.
+ *   - Vertex ids are uint32 in [0, n); edge indices and offsets are int64.
+ *   - Unreached vertices get GBBS_INF (0xFFFFFFFF) in dist and parent
+ *     (reading A2); parent[src] = src (reading A3).
+ *   - Pointers may be host or device memory (classified with
+ *     cudaPointerGetAttributes); device pointers must be on the current
+ *     device.  The CUDA device is the one current when the graph is created.
+ *   - A gbbs_graph owns per-handle scratch, so calls on ONE handle must not
+ *     run concurrently (different handles may).
+ */
+#ifndef GBBS_H
+#define GBBS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define GBBS_OK 0
+#define GBBS_EINVAL (-1)    /* bad argument or malformed CSR               */
+#define GBBS_ERANGE (-2)    /* sizes/weights outside what uint32 state holds */
+#define GBBS_ENOMEM (-3)    /* device or host allocation failed            */
+#define GBBS_ECUDA (-4)     /* CUDA error, including "no sm_100 device"     */
+#define GBBS_EINTERNAL (-5) /* round cap hit (cannot happen for w >= 0)    */
+
+#define GBBS_INF 0xFFFFFFFFu
+
+/* ---- gbbs_graph_create flags ------------------------------------------- */
+/* The caller asserts the CSR is symmetric (u->v iff v->u).  The in-edge CSC
+ * used by dense (pull) rounds then aliases the CSR instead of being built.
+ * An incorrect assertion makes dense-round results undefined. */
+#define GBBS_SYMMETRIC 0x1u
+/* Use device arrays in place (zero copy).  The caller keeps offsets, targets
+ * and weights alive and unmodified until gbbs_graph_destroy.  Host pointers
+ * with this flag are an error (GBBS_EINVAL). */
+#define GBBS_BORROW 0x2u
+/* Skip the O(n+m) device validation of the CSR (offsets/targets). */
+#define GBBS_NO_VALIDATE 0x4u
+
+typedef struct gbbs_graph gbbs_graph;
+
+/*
+ * gbbs_graph_create — make a graph resident in HBM.
+ *
+ * n        number of vertices, 1 <= n <= 2^32 - 2.
+ * m        number of directed edges (CSR entries), m >= 0.
+ * offsets  int64[n+1], offsets[0] = 0, non-decreasing, offsets[n] = m
+ *          (CSR, P:1813-1817 sec:prelims).  Host or device.
+ * targets  uint32[m], targets[e] < n: out-neighbours of u are
+ *          targets[offsets[u] .. offsets[u+1]).  Host or device.  Self-loops
+ *          and duplicates are accepted (reading A18) and only cost work.
+ * weights  uint32[m] edge weights for Bellman-Ford, or NULL for unit weights
+ *          (reading A17).  Host or device.
+ * flags    GBBS_SYMMETRIC | GBBS_BORROW | GBBS_NO_VALIDATE.
+ * out      receives the handle; set to NULL on any error (nothing leaks).
+ *
+ * Ownership: without GBBS_BORROW the library copies every array into its own
+ * device memory, so the caller may free its arrays as soon as this returns.
+ * For non-symmetric graphs an in-edge CSC (in-lists sorted by source) is built
+ * here on the device.  Per-handle traversal scratch (frontier lists, bitmaps,
+ * counters) is allocated once here.
+ *
+ * Errors: GBBS_EINVAL  n out of range, m < 0, NULL required pointer,
+ *                      offsets[0] != 0, offsets[n] != m, decreasing offsets,
+ *                      a target >= n (unless GBBS_NO_VALIDATE);
+ *         GBBS_ERANGE  n and m too large to pack the frontier counter
+ *                      (bits(n) + bits(m) > 64);
+ *         GBBS_ENOMEM, GBBS_ECUDA.
+ */
+int gbbs_graph_create(int64_t n, int64_t m, const int64_t *offsets,
+                      const uint32_t *targets, const uint32_t *weights,
+                      uint32_t flags, gbbs_graph **out);
+
+/* Free library-owned device memory; borrowed arrays are not freed.  NULL-safe. */
+void gbbs_graph_destroy(gbbs_graph *g);
+
+/* Query sizes/flags of a handle (any pointer may be NULL). */
+int gbbs_graph_info(const gbbs_graph *g, int64_t *n, int64_t *m,
+                    uint32_t *flags);
+
+/*
+ * gbbs_bfs — breadth-first search from src along out-edges
+ * (output spec P:1475-1478, sec:benchmark; algorithm, sec:algs).
+ *
+ * dist    uint32[n], caller-owned, host or device: dist[v] = hop distance
+ *         from src, GBBS_INF if unreachable.  Required.
+ * parent  uint32[n] or NULL: parent[v] = an in-neighbour u of v with
+ *         dist[u] = dist[v] - 1 (which one is unspecified: the test-and-set
+ *         winner in push rounds, the first frontier in-neighbour in CSC order
+ *         in pull rounds, reading A15); parent[src] = src; GBBS_INF if
+ *         unreached.
+ * cuda_stream  a cudaStream_t (NULL = legacy default stream).  All work is
+ *         enqueued on it and the call synchronizes it before returning, so the
+ *         status covers kernel errors; CUDA events recorded on the stream
+ *         around the call time it.
+ *
+ * Errors: GBBS_EINVAL (g NULL, dist NULL, src >= n; outputs untouched),
+ *         GBBS_ECUDA, GBBS_EINTERNAL.
+ */
+int gbbs_bfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
+             uint32_t *parent, void *cuda_stream);
+
+/*
+ * gbbs_bellman_ford — frontier Bellman-Ford from src (output spec
+ * P:1487-1490, sec:benchmark; algorithm, sec:algs).  Weights are the
+ * uint32 weights given at create (non-negative, so no negative cycles;
+ * reading A13), or 1 if none were given.
+ *
+ * dist    uint32[n], caller-owned, host or device: shortest weighted
+ *         distance from src, GBBS_INF if unreachable.
+ * Same stream/synchronization/error conventions as gbbs_bfs, plus
+ * GBBS_ERANGE if max(w) * (n-1) >= 2^32 - 1 (a finite distance, always a
+ * simple-path length, might not fit below the uint32 sentinel), and
+ * GBBS_EINTERNAL if more than n+1 rounds run (impossible with w >= 0).
+ */
+int gbbs_bellman_ford(const gbbs_graph *g, uint32_t src, uint32_t *dist,
+                      void *cuda_stream);
+
+/* ---- extended calls (bench / tests) ------------------------------------ */
+
+/* Direction choice per round (threshold rule reading A10). */
+#define GBBS_MODE_AUTO 0   /* dense iff |U| + sum_{u in U} deg(u) > m / T */
+#define GBBS_MODE_SPARSE 1 /* always push                                 */
+#define GBBS_MODE_DENSE 2  /* always pull (BFS only; BF always pushes)    */
+
+typedef struct {
+  uint32_t threshold_den; /* T; 0 selects the default 20                  */
+  int32_t mode;           /* GBBS_MODE_*                                   */
+  uint32_t reserved[6];   /* must be zero                                  */
+} gbbs_opts;
+
+/* One record per round, filled only when gbbs_stats.rounds_out != NULL. */
+typedef struct {
+  int32_t dense;          /* 1 = pull round, 0 = push round               */
+  int32_t reserved;
+  int64_t frontier;       /* |U|: frontier vertices with out-degree > 0   */
+  int64_t frontier_edges; /* sum of out-degrees of U                       */
+  int64_t acquired;       /* vertices won this round (incl. out-degree 0) */
+  int64_t edges_examined; /* push: edges of U; pull: in-edges loaded      */
+  int64_t vertices_swept; /* pull: unvisited vertices examined            */
+} gbbs_round_stat;
+
+typedef struct {
+  int64_t rounds;          /* rounds executed (edgeMap calls)             */
+  int64_t dense_rounds;
+  int64_t edges_examined;  /* total over rounds                           */
+  int64_t reached;         /* vertices with finite dist                  */
+  double kernel_ms;        /* device time of the traversal kernel, from
+                              CUDA events recorded on cuda_stream around
+                              its launch                                 */
+  gbbs_round_stat *rounds_out; /* host array or NULL                       */
+  int64_t rounds_cap;      /* capacity of rounds_out                      */
+} gbbs_stats;
+
+/* Defaults: T = 20, GBBS_MODE_AUTO. */
+void gbbs_default_opts(gbbs_opts *o);
+
+/* As gbbs_bfs / gbbs_bellman_ford with options (NULL = defaults) and optional
+ * statistics (NULL = none).  Collecting per-round records adds counters to
+ * the kernels; do not time runs that collect them.  GBBS_EINVAL also for a
+ * bad mode or nonzero reserved fields. */
+int gbbs_bfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
+                uint32_t *parent, void *cuda_stream, const gbbs_opts *opts,
+                gbbs_stats *stats);
+int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
+                         void *cuda_stream, const gbbs_opts *opts,
+                         gbbs_stats *stats);
+
+/* Launch geometry of the persistent traversal kernel on this device:
+ * *ctas = co-resident CTAs used, *threads = threads per CTA. */
+int gbbs_launch_info(const gbbs_graph *g, int32_t *ctas, int32_t *threads);
+
+/* Thread-local message describing the last error on this thread ("" if none). */
+const char *gbbs_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GBBS_H */

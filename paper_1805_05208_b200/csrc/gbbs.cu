@@ -1,0 +1,543 @@
+// gbbs.cu — libgbbs: the C ABI declared in include/gbbs.h.
+//
+// Host side of the library: graph residency (copy/borrow, device validation,
+// in-edge CSC by device radix sort), per-handle scratch, and the launch of the
+// persistent traversal kernel (traverse.cuh) for gbbs_bfs / gbbs_bellman_ford.
+// No torch types, no exceptions across the ABI, no CPU fallback: every step of
+// a traversal runs in the kernels of this file and traverse.cuh.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/gbbs.h"
+#include "traverse.cuh"
+
+using namespace gbbs_dev;
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CU(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      int code_ = (e_ == cudaErrorMemoryAllocation) ? GBBS_ENOMEM : GBBS_ECUDA;    \
+      return fail(code_, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+    }                                                                              \
+  } while (0)
+
+extern "C" const char *gbbs_last_error(void) { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+// the handle
+// ---------------------------------------------------------------------------
+struct gbbs_graph {
+  int device = 0;
+  long long n = 0, m = 0;
+  uint32_t flags = 0;
+  int ebits = 1;
+  uint32_t maxw = 1;
+  long long *off = nullptr;
+  uint32_t *tgt = nullptr;
+  uint32_t *wgt = nullptr;
+  bool own_arrays = true;
+  long long *in_off = nullptr;  // alias of off when symmetric
+  uint32_t *in_tgt = nullptr;
+  // scratch
+  uint32_t *bm[2] = {nullptr, nullptr};
+  uint32_t *fv[2] = {nullptr, nullptr};
+  long long *fo[2] = {nullptr, nullptr};
+  long long *fb[2] = {nullptr, nullptr};
+  unsigned long long *cnt = nullptr;  // [4] + ctrl
+  int *status = nullptr;
+  long long *rounds = nullptr;
+  uint32_t *tmp_dist = nullptr, *tmp_parent = nullptr;  // for host outputs
+  RoundStat *dstats = nullptr;
+  long long dstats_cap = 0;
+  unsigned long long *dcount = nullptr;
+  long long nwords = 0;
+  int grid[2][2] = {{0, 0}, {0, 0}};  // [algo][stats]
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+static void free_graph(gbbs_graph *g) {
+  if (!g) return;
+  if (g->own_arrays) {
+    cudaFree(g->off);
+    cudaFree(g->tgt);
+    cudaFree(g->wgt);
+  }
+  if (g->in_off && g->in_off != g->off) cudaFree(g->in_off);
+  if (g->in_tgt && g->in_tgt != g->tgt) cudaFree(g->in_tgt);
+  for (int i = 0; i < 2; i++) {
+    cudaFree(g->bm[i]);
+    cudaFree(g->fv[i]);
+    cudaFree(g->fo[i]);
+    cudaFree(g->fb[i]);
+  }
+  cudaFree(g->cnt);
+  cudaFree(g->tmp_dist);
+  cudaFree(g->tmp_parent);
+  cudaFree(g->dstats);
+  if (g->ev[0]) cudaEventDestroy(g->ev[0]);
+  if (g->ev[1]) cudaEventDestroy(g->ev[1]);
+  delete g;
+}
+
+// ---------------------------------------------------------------------------
+// create-time kernels (a0): validation, max weight, CSC construction
+// ---------------------------------------------------------------------------
+__global__ void k_validate(const long long *off, const uint32_t *tgt, long long n, long long m,
+                           unsigned long long *bad) {
+  long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long gs = (long long)gridDim.x * blockDim.x;
+  for (long long i = gt; i < n; i += gs)
+    if (off[i] > off[i + 1]) atomicOr(bad, 1ull);
+  for (long long e = gt; e < m; e += gs)
+    if (tgt[e] >= (unsigned long long)n) atomicOr(bad, 2ull);
+}
+
+__global__ void k_maxw(const uint32_t *w, long long m, unsigned int *out) {
+  long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long gs = (long long)gridDim.x * blockDim.x;
+  uint32_t mx = 0;
+  for (long long e = gt; e < m; e += gs) mx = max(mx, w[e]);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+// key = target << 32 | source for every edge; one warp per source vertex.
+__global__ void k_transpose_keys(const long long *off, const uint32_t *tgt, long long n,
+                                 unsigned long long *keys) {
+  long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  int lane = threadIdx.x & 31;
+  for (long long u = warp; u < n; u += nwarps) {
+    long long a = off[u], b = off[u + 1];
+    for (long long e = a + lane; e < b; e += 32)
+      keys[e] = ((unsigned long long)tgt[e] << 32) | (unsigned long long)u;
+  }
+}
+
+// From keys sorted by (target, source): in_tgt = source, in_off[v] = first index with target v.
+__global__ void k_csc_from_keys(const unsigned long long *keys, long long n, long long m,
+                                uint32_t *in_tgt, long long *in_off) {
+  long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long gs = (long long)gridDim.x * blockDim.x;
+  for (long long i = gt; i < m; i += gs) {
+    unsigned long long k = keys[i];
+    long long v = (long long)(k >> 32);
+    in_tgt[i] = (uint32_t)(k & 0xFFFFFFFFull);
+    long long pv = (i == 0) ? -1 : (long long)(keys[i - 1] >> 32);
+    for (long long x = pv + 1; x <= v; x++) in_off[x] = i;
+  }
+  if (gt == 0) {
+    long long last = (m == 0) ? -1 : (long long)(keys[m - 1] >> 32);
+    for (long long x = last + 1; x <= n; x++) in_off[x] = m;
+  }
+}
+
+static int bits_for(unsigned long long x) {  // bits needed to represent x (>= 1)
+  int b = 1;
+  while (b < 64 && (x >> b) != 0) b++;
+  return b;
+}
+
+static bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static int ensure_device_ok(int *dev_out) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    return fail(GBBS_ECUDA, "libgbbs is built for sm_100a (B200); device %d is sm_%d%d", dev,
+                prop.major, prop.minor);
+  int coop = 0;
+  CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) return fail(GBBS_ECUDA, "device %d lacks cooperative launch", dev);
+  *dev_out = dev;
+  return GBBS_OK;
+}
+
+template <int ALGO, bool STATS>
+static int occupancy_grid(int *grid) {
+  int dev = 0, nsm = 0, per = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, traverse_kernel<ALGO, STATS>, BLOCK, 0));
+  if (per < 1) return fail(GBBS_ECUDA, "traverse kernel cannot be resident");
+  *grid = per * nsm;
+  return GBBS_OK;
+}
+
+static int copy_in(void **dst, const void *src, size_t bytes) {
+  CU(cudaMalloc(dst, bytes ? bytes : 16));
+  if (bytes) CU(cudaMemcpy(*dst, src, bytes, cudaMemcpyDefault));
+  return GBBS_OK;
+}
+
+static int create_impl(long long n, long long m, const int64_t *offsets, const uint32_t *targets,
+                       const uint32_t *weights, uint32_t flags, gbbs_graph *g) {
+  int rc;
+  if ((rc = ensure_device_ok(&g->device))) return rc;
+  g->n = n;
+  g->m = m;
+  g->flags = flags;
+  g->ebits = bits_for((unsigned long long)m);
+  if (g->ebits + bits_for((unsigned long long)n) > 64)
+    return fail(GBBS_ERANGE, "bits(n)+bits(m) > 64: frontier counter cannot be packed");
+
+  const bool borrow = flags & GBBS_BORROW;
+  if (borrow) {
+    if (!is_device_ptr(offsets) || (m > 0 && !is_device_ptr(targets)) ||
+        (weights && !is_device_ptr(weights)))
+      return fail(GBBS_EINVAL, "GBBS_BORROW requires device pointers");
+    g->own_arrays = false;
+    g->off = (long long *)offsets;
+    g->tgt = (uint32_t *)targets;
+    g->wgt = (uint32_t *)weights;
+  } else {
+    g->own_arrays = true;
+    if ((rc = copy_in((void **)&g->off, offsets, (size_t)(n + 1) * 8))) return rc;
+    if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4))) return rc;
+    if (weights && (rc = copy_in((void **)&g->wgt, weights, (size_t)m * 4))) return rc;
+  }
+  // endpoints
+  long long o0 = -1, on = -1;
+  CU(cudaMemcpy(&o0, g->off, 8, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(&on, g->off + n, 8, cudaMemcpyDeviceToHost));
+  if (o0 != 0) return fail(GBBS_EINVAL, "offsets[0] = %lld, expected 0", o0);
+  if (on != m) return fail(GBBS_EINVAL, "offsets[n] = %lld, expected m = %lld", on, m);
+
+  unsigned long long *dscratch = nullptr;
+  CU(cudaMalloc(&dscratch, 16));
+  CU(cudaMemset(dscratch, 0, 16));
+  if (!(flags & GBBS_NO_VALIDATE)) {
+    k_validate<<<1184, 256>>>(g->off, g->tgt, n, m, dscratch);
+    CU(cudaGetLastError());
+    unsigned long long bad = 0;
+    CU(cudaMemcpy(&bad, dscratch, 8, cudaMemcpyDeviceToHost));
+    if (bad) {
+      cudaFree(dscratch);
+      return fail(GBBS_EINVAL, "invalid CSR:%s%s", (bad & 1) ? " decreasing offsets" : "",
+                  (bad & 2) ? " target >= n" : "");
+    }
+  }
+  g->maxw = 1;
+  if (g->wgt && m > 0) {
+    unsigned int *mx = (unsigned int *)(dscratch + 1);
+    k_maxw<<<1184, 256>>>(g->wgt, m, mx);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy(&g->maxw, mx, 4, cudaMemcpyDeviceToHost));
+  }
+  cudaFree(dscratch);
+
+  // in-edge CSC for pull rounds
+  if (flags & GBBS_SYMMETRIC) {
+    g->in_off = g->off;
+    g->in_tgt = g->tgt;
+  } else {
+    CU(cudaMalloc(&g->in_off, (size_t)(n + 1) * 8));
+    CU(cudaMalloc(&g->in_tgt, (size_t)(m ? m : 1) * 4));
+    if (m == 0) {
+      CU(cudaMemset(g->in_off, 0, (size_t)(n + 1) * 8));
+    } else {
+      unsigned long long *k0 = nullptr, *k1 = nullptr;
+      void *tmp = nullptr;
+      size_t tmp_bytes = 0;
+      CU(cudaMalloc(&k0, (size_t)m * 8));
+      cudaError_t e1 = cudaMalloc(&k1, (size_t)m * 8);
+      if (e1 != cudaSuccess) {
+        cudaFree(k0);
+        return fail(GBBS_ENOMEM, "CSC sort buffer: %s", cudaGetErrorString(e1));
+      }
+      k_transpose_keys<<<4736, 256>>>(g->off, g->tgt, n, k0);
+      cub::DoubleBuffer<unsigned long long> db(k0, k1);
+      int end_bit = 32 + bits_for((unsigned long long)(n - 1));
+      cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, m, 0, end_bit);
+      cudaError_t e2 = cudaMalloc(&tmp, tmp_bytes);
+      if (e2 == cudaSuccess) {
+        e2 = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, m, 0, end_bit);
+        if (e2 == cudaSuccess) {
+          k_csc_from_keys<<<4736, 256>>>(db.Current(), n, m, g->in_tgt, g->in_off);
+          e2 = cudaGetLastError();
+        }
+        if (e2 == cudaSuccess) e2 = cudaDeviceSynchronize();
+      }
+      cudaFree(tmp);
+      cudaFree(k0);
+      cudaFree(k1);
+      if (e2 != cudaSuccess)
+        return fail(e2 == cudaErrorMemoryAllocation ? GBBS_ENOMEM : GBBS_ECUDA, "CSC build: %s",
+                    cudaGetErrorString(e2));
+    }
+  }
+
+  // per-handle scratch
+  g->nwords = (n + 31) / 32;
+  for (int i = 0; i < 2; i++) {
+    CU(cudaMalloc(&g->bm[i], (size_t)g->nwords * 4));
+    CU(cudaMemset(g->bm[i], 0, (size_t)g->nwords * 4));
+    CU(cudaMalloc(&g->fv[i], (size_t)n * 4));
+    CU(cudaMalloc(&g->fo[i], (size_t)n * 8));
+    CU(cudaMalloc(&g->fb[i], (size_t)n * 8));
+  }
+  CU(cudaMalloc(&g->cnt, 8 * 8));
+  CU(cudaMemset(g->cnt, 0, 8 * 8));
+  g->status = (int *)(g->cnt + 4);
+  g->rounds = (long long *)(g->cnt + 5);
+  g->dcount = g->cnt + 6;
+  if ((rc = occupancy_grid<ALGO_BFS, false>(&g->grid[0][0]))) return rc;
+  if ((rc = occupancy_grid<ALGO_BFS, true>(&g->grid[0][1]))) return rc;
+  if ((rc = occupancy_grid<ALGO_BF, false>(&g->grid[1][0]))) return rc;
+  if ((rc = occupancy_grid<ALGO_BF, true>(&g->grid[1][1]))) return rc;
+  CU(cudaDeviceSynchronize());
+  return GBBS_OK;
+}
+
+extern "C" int gbbs_graph_create(int64_t n, int64_t m, const int64_t *offsets,
+                                 const uint32_t *targets, const uint32_t *weights,
+                                 uint32_t flags, gbbs_graph **out) {
+  g_last_error.clear();
+  if (!out) return fail(GBBS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n > (int64_t)0xFFFFFFFEll) return fail(GBBS_EINVAL, "n = %lld out of [1, 2^32-2]", (long long)n);
+  if (m < 0) return fail(GBBS_EINVAL, "m < 0");
+  if (!offsets || (m > 0 && !targets)) return fail(GBBS_EINVAL, "NULL offsets/targets");
+  if (flags & ~(uint32_t)(GBBS_SYMMETRIC | GBBS_BORROW | GBBS_NO_VALIDATE))
+    return fail(GBBS_EINVAL, "unknown flags 0x%x", flags);
+  gbbs_graph *g = new (std::nothrow) gbbs_graph();
+  if (!g) return fail(GBBS_ENOMEM, "host allocation");
+  int rc = create_impl(n, m, offsets, targets, weights, flags, g);
+  if (rc != GBBS_OK) {
+    free_graph(g);
+    return rc;
+  }
+  *out = g;
+  return GBBS_OK;
+}
+
+extern "C" void gbbs_graph_destroy(gbbs_graph *g) { free_graph(g); }
+
+extern "C" int gbbs_graph_info(const gbbs_graph *g, int64_t *n, int64_t *m, uint32_t *flags) {
+  if (!g) return fail(GBBS_EINVAL, "g is NULL");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (flags) *flags = g->flags;
+  return GBBS_OK;
+}
+
+extern "C" void gbbs_default_opts(gbbs_opts *o) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->threshold_den = 20;
+  o->mode = GBBS_MODE_AUTO;
+}
+
+extern "C" int gbbs_launch_info(const gbbs_graph *g, int32_t *ctas, int32_t *threads) {
+  if (!g) return fail(GBBS_EINVAL, "g is NULL");
+  if (ctas) *ctas = g->grid[0][0];
+  if (threads) *threads = BLOCK;
+  return GBBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// traversal driver
+// ---------------------------------------------------------------------------
+__global__ void k_count_reached(const uint32_t *dist, long long n, unsigned long long *out) {
+  long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long gs = (long long)gridDim.x * blockDim.x;
+  unsigned long long c = 0;
+  for (long long i = gt; i < n; i += gs) c += dist[i] != INF;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+
+template <int ALGO, bool STATS>
+static int launch(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+  void *args[] = {&p};
+  if (ev0) CU(cudaEventRecord(ev0, st));
+  CU(cudaLaunchCooperativeKernel((const void *)traverse_kernel<ALGO, STATS>, g->grid[ALGO][STATS],
+                                 BLOCK, args, 0, st));
+  if (ev1) CU(cudaEventRecord(ev1, st));
+  return GBBS_OK;
+}
+
+static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, uint32_t *parent,
+               void *stream, const gbbs_opts *opts, gbbs_stats *stats) {
+  g_last_error.clear();
+  if (!cg_) return fail(GBBS_EINVAL, "g is NULL");
+  gbbs_graph *g = const_cast<gbbs_graph *>(cg_);
+  if (!dist) return fail(GBBS_EINVAL, "dist is NULL");
+  if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
+  gbbs_opts o;
+  gbbs_default_opts(&o);
+  if (opts) {
+    o = *opts;
+    if (o.threshold_den == 0) o.threshold_den = 20;
+    for (int i = 0; i < 6; i++)
+      if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
+    if (o.mode < 0 || o.mode > 2) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
+  }
+  if (algo == ALGO_BF) {
+    // uint32 distances: every finite distance is a simple-path length <= maxw*(n-1)
+    unsigned long long bound = (unsigned long long)g->maxw * (unsigned long long)(g->n - 1);
+    if (g->maxw != 0 && bound / g->maxw != (unsigned long long)(g->n - 1)) bound = ~0ull;
+    if (bound >= 0xFFFFFFFFull)
+      return fail(GBBS_ERANGE, "max weight %u * (n-1) does not fit below 2^32-1", g->maxw);
+  }
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  if (dev != g->device) CU(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+
+  const bool dist_dev = is_device_ptr(dist);
+  const bool par_dev = parent ? is_device_ptr(parent) : true;
+  const size_t nb = (size_t)g->n * 4;
+  if (!dist_dev && !g->tmp_dist) CU(cudaMalloc(&g->tmp_dist, nb));
+  if (!par_dev && !g->tmp_parent) CU(cudaMalloc(&g->tmp_parent, nb));
+  uint32_t *ddist = dist_dev ? dist : g->tmp_dist;
+  uint32_t *dpar = parent ? (par_dev ? parent : g->tmp_parent) : nullptr;
+
+  const bool want_stats = stats != nullptr;
+  const bool want_rounds = want_stats && stats->rounds_out && stats->rounds_cap > 0;
+  long long cap = 0;
+  if (want_rounds) {
+    cap = stats->rounds_cap;
+    if (g->dstats_cap < cap) {
+      cudaFree(g->dstats);
+      g->dstats = nullptr;
+      g->dstats_cap = 0;
+      CU(cudaMalloc(&g->dstats, (size_t)cap * sizeof(RoundStat)));
+      g->dstats_cap = cap;
+    }
+    CU(cudaMemsetAsync(g->dstats, 0, (size_t)cap * sizeof(RoundStat), st));
+  }
+
+  Params p;
+  memset(&p, 0, sizeof p);
+  p.n = g->n;
+  p.m = g->m;
+  p.off = g->off;
+  p.tgt = g->tgt;
+  p.wgt = g->wgt;
+  p.in_off = g->in_off;
+  p.in_tgt = g->in_tgt;
+  p.dist = ddist;
+  p.parent = (algo == ALGO_BFS) ? dpar : nullptr;
+  for (int i = 0; i < 2; i++) {
+    p.bm[i] = g->bm[i];
+    p.fv[i] = g->fv[i];
+    p.fo[i] = g->fo[i];
+    p.fb[i] = g->fb[i];
+  }
+  p.cnt = g->cnt;
+  p.status = g->status;
+  p.rounds_out = g->rounds;
+  p.stats = want_rounds ? g->dstats : nullptr;
+  p.stats_cap = cap;
+  p.nwords = g->nwords;
+  p.dense_threshold = g->m / (long long)o.threshold_den;
+  p.max_rounds = g->n + 1;
+  p.ebits = g->ebits;
+  p.mode = (algo == ALGO_BFS) ? o.mode : 1;
+  p.src = src;
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (want_stats) {
+    if (!g->ev[0]) {
+      CU(cudaEventCreate(&g->ev[0]));
+      CU(cudaEventCreate(&g->ev[1]));
+    }
+    ev0 = g->ev[0];
+    ev1 = g->ev[1];
+  }
+  int rc;
+  if (algo == ALGO_BFS)
+    rc = want_rounds ? launch<ALGO_BFS, true>(g, p, st, ev0, ev1) : launch<ALGO_BFS, false>(g, p, st, ev0, ev1);
+  else
+    rc = want_rounds ? launch<ALGO_BF, true>(g, p, st, ev0, ev1) : launch<ALGO_BF, false>(g, p, st, ev0, ev1);
+  if (rc) return rc;
+  if (!dist_dev) CU(cudaMemcpyAsync(dist, ddist, nb, cudaMemcpyDeviceToHost, st));
+  if (parent && !par_dev) CU(cudaMemcpyAsync(parent, dpar, nb, cudaMemcpyDeviceToHost, st));
+  struct {
+    int status;
+    int pad;
+    long long rounds;
+  } ctrl;
+  CU(cudaMemcpyAsync(&ctrl, g->status, 16, cudaMemcpyDeviceToHost, st));
+  long long reached = -1;
+  if (want_stats) {
+    CU(cudaMemsetAsync(g->dcount, 0, 8, st));
+    k_count_reached<<<592, 256, 0, st>>>(ddist, g->n, g->dcount);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&reached, g->dcount, 8, cudaMemcpyDeviceToHost, st));
+  }
+  CU(cudaStreamSynchronize(st));
+  if (want_stats) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ev0, ev1));
+    stats->kernel_ms = ms;
+    stats->rounds = ctrl.rounds;
+    stats->reached = reached;
+    stats->dense_rounds = 0;
+    stats->edges_examined = 0;
+    if (want_rounds) {
+      long long nr = ctrl.rounds < cap ? ctrl.rounds : cap;
+      static_assert(sizeof(RoundStat) == sizeof(gbbs_round_stat), "stat layout");
+      CU(cudaMemcpy(stats->rounds_out, g->dstats, (size_t)nr * sizeof(RoundStat),
+                    cudaMemcpyDeviceToHost));
+      for (long long i = 0; i < nr; i++) {
+        stats->dense_rounds += stats->rounds_out[i].dense;
+        stats->edges_examined += stats->rounds_out[i].edges_examined;
+      }
+    }
+  }
+  if (ctrl.status != 0)
+    return fail(GBBS_EINTERNAL, "round cap (%lld rounds) exceeded", (long long)p.max_rounds);
+  return GBBS_OK;
+}
+
+extern "C" int gbbs_bfs(const gbbs_graph *g, uint32_t src, uint32_t *dist, uint32_t *parent,
+                        void *cuda_stream) {
+  return run(g, ALGO_BFS, src, dist, parent, cuda_stream, nullptr, nullptr);
+}
+
+extern "C" int gbbs_bellman_ford(const gbbs_graph *g, uint32_t src, uint32_t *dist,
+                                 void *cuda_stream) {
+  return run(g, ALGO_BF, src, dist, nullptr, cuda_stream, nullptr, nullptr);
+}
+
+extern "C" int gbbs_bfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist, uint32_t *parent,
+                           void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats) {
+  return run(g, ALGO_BFS, src, dist, parent, cuda_stream, opts, stats);
+}
+
+extern "C" int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
+                                    void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats) {
+  return run(g, ALGO_BF, src, dist, nullptr, cuda_stream, opts, stats);
+}

@@ -1,0 +1,215 @@
+"""Thin ctypes binding of libgbbs (include/gbbs.h): argument marshalling only.
+
+Every step of a traversal runs in libgbbs's CUDA kernels; there is no Python or
+CPU fallback.  If libgbbs.so is missing or fails to load, importing this module
+raises — the product path fails loudly instead of degrading.
+
+Arrays may be numpy arrays (host memory) or torch tensors (host or CUDA); the
+library classifies each pointer itself (gbbs.h "Conventions").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgbbs.so")
+
+GBBS_OK, GBBS_EINVAL, GBBS_ERANGE, GBBS_ENOMEM, GBBS_ECUDA, GBBS_EINTERNAL = 0, -1, -2, -3, -4, -5
+GBBS_INF = 0xFFFFFFFF
+GBBS_SYMMETRIC, GBBS_BORROW, GBBS_NO_VALIDATE = 0x1, 0x2, 0x4
+GBBS_MODE_AUTO, GBBS_MODE_SPARSE, GBBS_MODE_DENSE = 0, 1, 2
+
+EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_bfs",
+           "gbbs_bellman_ford", "gbbs_bfs_ex", "gbbs_bellman_ford_ex", "gbbs_default_opts",
+           "gbbs_launch_info", "gbbs_last_error")
+
+
+class GbbsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"gbbs error {code}: {msg}")
+        self.code = code
+
+
+class gbbs_opts(ctypes.Structure):
+    _fields_ = [("threshold_den", ctypes.c_uint32), ("mode", ctypes.c_int32),
+                ("reserved", ctypes.c_uint32 * 6)]
+
+
+class gbbs_round_stat(ctypes.Structure):
+    _fields_ = [("dense", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("frontier", ctypes.c_int64), ("frontier_edges", ctypes.c_int64),
+                ("acquired", ctypes.c_int64), ("edges_examined", ctypes.c_int64),
+                ("vertices_swept", ctypes.c_int64)]
+
+
+class gbbs_stats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int64), ("dense_rounds", ctypes.c_int64),
+                ("edges_examined", ctypes.c_int64), ("reached", ctypes.c_int64),
+                ("kernel_ms", ctypes.c_double), ("rounds_out", ctypes.POINTER(gbbs_round_stat)), ("rounds_cap", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python build.py` (nvcc, sm_100a)")
+    lib = ctypes.CDLL(LIB_PATH)
+    p, i64, u32, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int32
+    lib.gbbs_graph_create.argtypes = [i64, i64, p, p, p, u32, ctypes.POINTER(p)]
+    lib.gbbs_graph_destroy.argtypes = [p]
+    lib.gbbs_graph_destroy.restype = None
+    lib.gbbs_graph_info.argtypes = [p, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(u32)]
+    lib.gbbs_bfs.argtypes = [p, u32, p, p, p]
+    lib.gbbs_bellman_ford.argtypes = [p, u32, p, p]
+    lib.gbbs_bfs_ex.argtypes = [p, u32, p, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
+    lib.gbbs_bellman_ford_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
+    lib.gbbs_default_opts.argtypes = [ctypes.POINTER(gbbs_opts)]
+    lib.gbbs_default_opts.restype = None
+    lib.gbbs_launch_info.argtypes = [p, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    lib.gbbs_last_error.argtypes = []
+    lib.gbbs_last_error.restype = ctypes.c_char_p
+    for f in ("gbbs_graph_create", "gbbs_graph_info", "gbbs_bfs", "gbbs_bellman_ford", "gbbs_bfs_ex",
+              "gbbs_bellman_ford_ex", "gbbs_launch_info"):
+        getattr(lib, f).restype = ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    return lib.gbbs_last_error().decode()
+
+
+def _check(rc):
+    if rc != GBBS_OK:
+        raise GbbsError(rc, last_error())
+
+
+def _ptr(a):
+    """Raw address of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    if isinstance(a, int):
+        return a
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _stream(stream, *arrays):
+    if stream is not None:
+        return stream if isinstance(stream, int) else stream.cuda_stream
+    for a in arrays:
+        if a is not None and hasattr(a, "is_cuda") and a.is_cuda:
+            import torch
+            return torch.cuda.current_stream(a.device).cuda_stream
+    return None
+
+
+# ---- the four calls of the boundary, same names as the C ABI -------------------
+
+def gbbs_graph_create(n, m, offsets, targets, weights=None, flags=0):
+    """Returns an opaque handle (int).  See gbbs.h for ownership and errors."""
+    h = ctypes.c_void_p()
+    _check(lib.gbbs_graph_create(int(n), int(m), _ptr(offsets), _ptr(targets), _ptr(weights),
+                                 int(flags), ctypes.byref(h)))
+    return h.value
+
+
+def gbbs_graph_destroy(handle):
+    lib.gbbs_graph_destroy(handle)
+
+
+def gbbs_bfs(handle, src, dist, parent=None, stream=None, opts=None, stats=None):
+    st = _stream(stream, dist, parent)
+    if opts is None and stats is None:
+        _check(lib.gbbs_bfs(handle, int(src), _ptr(dist), _ptr(parent), st))
+    else:
+        _check(lib.gbbs_bfs_ex(handle, int(src), _ptr(dist), _ptr(parent), st,
+                               ctypes.byref(opts) if opts is not None else None,
+                               ctypes.byref(stats) if stats is not None else None))
+
+
+def gbbs_bellman_ford(handle, src, dist, stream=None, opts=None, stats=None):
+    st = _stream(stream, dist)
+    if opts is None and stats is None:
+        _check(lib.gbbs_bellman_ford(handle, int(src), _ptr(dist), st))
+    else:
+        _check(lib.gbbs_bellman_ford_ex(handle, int(src), _ptr(dist), st,
+                                        ctypes.byref(opts) if opts is not None else None,
+                                        ctypes.byref(stats) if stats is not None else None))
+
+
+def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO):
+    o = gbbs_opts()
+    lib.gbbs_default_opts(ctypes.byref(o))
+    o.threshold_den = threshold_den
+    o.mode = mode
+    return o
+
+
+def make_stats(rounds_cap=0):
+    s = gbbs_stats()
+    buf = None
+    if rounds_cap:
+        buf = (gbbs_round_stat * rounds_cap)()
+        s.rounds_out = ctypes.cast(buf, ctypes.POINTER(gbbs_round_stat))
+        s.rounds_cap = rounds_cap
+    s._buf = buf  # keep alive
+    return s
+
+
+def round_records(stats):
+    n = min(stats.rounds, stats.rounds_cap)
+    return [dict(dense=r.dense, frontier=r.frontier, frontier_edges=r.frontier_edges,
+                 acquired=r.acquired, edges_examined=r.edges_examined,
+                 vertices_swept=r.vertices_swept) for r in stats.rounds_out[:n]] if n else []
+
+
+class Graph:
+    """RAII wrapper around a gbbs_graph handle."""
+
+    def __init__(self, offsets, targets, weights=None, symmetric=False, borrow=False, validate=True):
+        n = int(offsets.shape[0]) - 1
+        m = int(targets.shape[0])
+        flags = (GBBS_SYMMETRIC if symmetric else 0) | (GBBS_BORROW if borrow else 0) | \
+            (0 if validate else GBBS_NO_VALIDATE)
+        self.n, self.m = n, m
+        self._keep = (offsets, targets, weights) if borrow else None
+        self.handle = gbbs_graph_create(n, m, offsets, targets, weights, flags)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            gbbs_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def launch_info(self):
+        c, t = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib.gbbs_launch_info(self.handle, ctypes.byref(c), ctypes.byref(t)))
+        return c.value, t.value
+
+    def bfs(self, src, dist, parent=None, stream=None, opts=None, stats=None):
+        gbbs_bfs(self.handle, src, dist, parent, stream, opts, stats)
+
+    def bellman_ford(self, src, dist, stream=None, opts=None, stats=None):
+        gbbs_bellman_ford(self.handle, src, dist, stream, opts, stats)

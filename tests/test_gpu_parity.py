@@ -1,0 +1,286 @@
+"""GPU parity: libgbbs (through its C ABI) vs the CPU oracle, element by element.
+
+Bar: distances bit-exact; every BFS parent certified (a
+valid in-neighbour one level closer, reading A15); forced-sparse, forced-dense,
+auto and T in {10,20,40} give identical distances.
+"""
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from golden_io import read_examples
+from pins import grid_edges, path_graph, recursive_tree, torus_dist, torus_level_counts
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+INF = 0xFFFFFFFF
+MODES = ("auto", "sparse", "dense")
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1805_05208_b200 import gbbs
+    return gbbs
+
+
+def _opts(G, mode, T=20):
+    return G.make_opts(threshold_den=T, mode={"auto": G.GBBS_MODE_AUTO, "sparse": G.GBBS_MODE_SPARSE,
+                                                "dense": G.GBBS_MODE_DENSE}[mode])
+
+
+def run_bfs(G, g, src, mode="auto", T=20, host=False, stats=None):
+    n = g.n
+    if host:
+        d = np.empty(n, np.uint32); p = np.empty(n, np.uint32)
+    else:
+        d = torch.empty(n, dtype=torch.int32, device="cuda"); p = torch.empty_like(d)
+    g.bfs(src, d, p, opts=_opts(G, mode, T), stats=stats)
+    if not host:
+        torch.cuda.synchronize()
+        d = d.cpu().numpy().view(np.uint32); p = p.cpu().numpy().view(np.uint32)
+    return d, p
+
+
+def run_bf(G, g, src, host=False, stats=None):
+    if host:
+        d = np.empty(g.n, np.uint32)
+    else:
+        d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    g.bellman_ford(src, d, stats=stats)
+    if not host:
+        d = d.cpu().numpy().view(np.uint32)
+    return d
+
+
+def check_bfs_all_modes(G, off, tgt, srcs, symmetric, host_variants=True):
+    g = G.Graph(off, tgt, symmetric=symmetric)
+    for src in srcs:
+        ref, _ = oracle.bfs(off, tgt, src)
+        for mode in MODES:
+            d, p = run_bfs(G, g, src, mode)
+            assert (d == ref).all(), (mode, src, np.nonzero(d != ref)[0][:5])
+            ok, bad = oracle.check_bfs(off, tgt, src, d, p)
+            assert ok, (mode, src, bad)
+        if host_variants:
+            d, p = run_bfs(G, g, src, "auto", host=True)
+            assert (d == ref).all()
+            assert oracle.check_bfs(off, tgt, src, d, p)[0]
+    g.close()
+
+
+def check_bf(G, off, tgt, w, srcs, symmetric):
+    g = G.Graph(off, tgt, w, symmetric=symmetric)
+    for src in srcs:
+        ref, _ = oracle.dijkstra(off, tgt, w, src)
+        d = run_bf(G, g, src)
+        assert (d == ref).all(), (src, np.nonzero(d != ref)[0][:5])
+        d = run_bf(G, g, src, host=True)
+        assert (d == ref).all()
+    g.close()
+
+
+# ---- small and closed-form graphs ---------------------------------------------------
+
+def test_spec_examples(G):
+    for ex in read_examples():
+        if ex["kind"] == "bfs":
+            g = G.Graph(ex["offsets"], ex["targets"], symmetric=True)
+            for mode in MODES:
+                d, _ = run_bfs(G, g, ex["src"], mode)
+                assert (d == ex["expected"]).all(), ex["line"]
+        else:
+            g = G.Graph(ex["offsets"], ex["targets"], ex["weights"], symmetric=True)
+            assert (run_bf(G, g, ex["src"]) == ex["expected"]).all(), ex["line"]
+        g.close()
+
+
+def test_single_vertex_and_isolated_source(G):
+    off = np.zeros(2, np.int64); tgt = np.zeros(0, np.uint32)
+    g = G.Graph(off, tgt, symmetric=True)
+    d, p = run_bfs(G, g, 0)
+    assert list(d) == [0] and list(p) == [0]
+    assert list(run_bf(G, g, 0)) == [0]
+    g.close()
+    off, tgt = graphgen.from_edge_list(5, [(1, 2), (2, 3)])
+    g = G.Graph(off, tgt, symmetric=True)
+    d, p = run_bfs(G, g, 0)
+    assert list(d) == [0, INF, INF, INF, INF] and list(p) == [0, INF, INF, INF, INF]
+    g.close()
+
+
+@pytest.mark.parametrize("n", [2, 33, 1000, 5000])
+def test_path_closed_form(G, n):
+    off, tgt = graphgen.from_edge_list(n, path_graph(n))
+    g = G.Graph(off, tgt, symmetric=True)
+    for src in (0, n // 2, n - 1):
+        for mode in MODES:
+            d, p = run_bfs(G, g, src, mode)
+            assert (d == np.abs(np.arange(n) - src)).all()
+            exp_p = np.array([src if v == src else (v + 1 if v < src else v - 1) for v in range(n)])
+            assert (p == exp_p).all()
+    g.close()
+
+
+def test_grid_and_trees(G):
+    a, b = 37, 29
+    off, tgt = graphgen.from_edge_list(a * b, grid_edges(a, b))
+    check_bfs_all_modes(G, off, tgt, [0, 500, a * b - 1], True)
+    for seed in (1, 2):
+        edges, par, depth = recursive_tree(3000, seed)
+        off, tgt = graphgen.from_edge_list(3000, edges)
+        g = G.Graph(off, tgt, symmetric=True)
+        for mode in MODES:
+            d, p = run_bfs(G, g, 0, mode)
+            assert (d == depth).all() and (p[1:] == par[1:]).all()
+        g.close()
+
+
+@pytest.mark.parametrize("L", [3, 7, 16, 33])
+def test_torus_closed_form_and_levels(G, L):
+    off, tgt = graphgen.torus3d(L)
+    g = G.Graph(off, tgt, symmetric=True)
+    for mode in MODES:
+        st = G.make_stats(4096)
+        d, p = run_bfs(G, g, 0, mode, stats=st)
+        assert (d == torus_dist(L, 0)).all()
+        assert oracle.check_bfs(off, tgt, 0, d, p)[0]
+        recs = G.round_records(st)
+        lv = torus_level_counts(L)
+        assert st.rounds == len(lv)                       # ecc + 1 edgeMap rounds
+        assert [r["frontier"] for r in recs] == list(lv)  # frontier r = level-r count
+        assert st.reached == L ** 3
+    c = 5
+    w = np.full(tgt.shape, c, np.uint32)
+    g2 = G.Graph(off, tgt, w, symmetric=True)
+    assert (run_bf(G, g2, 0) == c * torus_dist(L, 0)).all()
+    g.close(); g2.close()
+
+
+def test_complete_graph_exact_parent(G):
+    n = 300
+    off, tgt = graphgen.from_edge_list(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+    g = G.Graph(off, tgt, symmetric=True)
+    for mode in MODES:
+        d, p = run_bfs(G, g, 7, mode)
+        assert (d == np.where(np.arange(n) == 7, 0, 1)).all() and (p == 7).all()
+    g.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_symmetric_and_directed(G, seed):
+    for sym in (True, False):
+        off, tgt = graphgen.random_graph(700, 0.004 * (1 + seed), seed, symmetric=sym)
+        check_bfs_all_modes(G, off, tgt, [0, 1, 699], sym, host_variants=(seed == 0))
+        w = graphgen.pair_weights(off, tgt, seed, 50)
+        check_bf(G, off, tgt, w, [0, 3], sym)
+
+
+def test_directed_rmat_threshold_sweep(G):
+    off, tgt = graphgen.rmat_graph(16, 1 << 20, 9, 0.6, 0.15, 0.15, symmetric=False)
+    g = G.Graph(off, tgt, symmetric=False)
+    cand = np.nonzero(np.diff(off) > 0)[0]
+    for src in graphgen.choose_sources(cand, 3, 55):
+        ref, _ = oracle.bfs(off, tgt, src)
+        for mode in MODES:
+            for T in (10, 20, 40):
+                d, p = run_bfs(G, g, src, mode, T)
+                assert (d == ref).all()
+                assert oracle.check_bfs(off, tgt, src, d, p)[0]
+    g.close()
+
+
+def test_unit_weights_and_null_weights_equal_bfs(G):
+    off, tgt = graphgen.rmat_graph(15, 1 << 19, 3, 0.57, 0.19, 0.19)
+    g = G.Graph(off, tgt, symmetric=True)
+    g1 = G.Graph(off, tgt, np.ones(tgt.shape, np.uint32), symmetric=True)
+    ref, _ = oracle.bfs(off, tgt, 0)
+    assert (run_bf(G, g, 0) == ref).all()
+    assert (run_bf(G, g1, 0) == ref).all()
+    g.close(); g1.close()
+
+
+def test_borrow_and_device_inputs(G):
+    off, tgt = graphgen.rmat_graph(14, 1 << 17, 21, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 2, 14)
+    doff = torch.from_numpy(off).cuda()
+    dtgt = torch.from_numpy(tgt.view(np.int32)).cuda()
+    dw = torch.from_numpy(w.view(np.int32)).cuda()
+    ref, _ = oracle.bfs(off, tgt, 0)
+    refw, _ = oracle.dijkstra(off, tgt, w, 0)
+    for borrow in (False, True):
+        g = G.Graph(doff, dtgt, dw, symmetric=True, borrow=borrow)
+        d, p = run_bfs(G, g, 0)
+        assert (d == ref).all()
+        assert (run_bf(G, g, 0) == refw).all()
+        g.close()
+
+
+def test_repeated_calls_are_deterministic(G):
+    off, tgt = graphgen.rmat_graph(16, 1 << 20, 5, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 5, 16)
+    g = G.Graph(off, tgt, w, symmetric=True)
+    d0, _ = run_bfs(G, g, 0)
+    b0 = run_bf(G, g, 0)
+    for _ in range(5):
+        assert (run_bfs(G, g, 0)[0] == d0).all()
+        assert (run_bf(G, g, 0) == b0).all()
+    g.close()
+
+
+# ---- error conventions ---------------------------------------------------------------
+
+def test_error_conventions(G):
+    off, tgt = graphgen.from_edge_list(4, [(0, 1), (1, 2)])
+    g = G.Graph(off, tgt, symmetric=True)
+    d = np.full(4, 77, np.uint32)
+    with pytest.raises(G.GbbsError) as e:
+        g.bfs(4, d)
+    assert e.value.code == -1 and (d == 77).all()
+    with pytest.raises(G.GbbsError):
+        g.bellman_ford(9, d)
+    with pytest.raises(G.GbbsError):
+        g.bfs(0, None)
+    g.close()
+    bad = off.copy(); bad[2] = 0
+    with pytest.raises(G.GbbsError) as e:
+        G.Graph(bad, tgt)
+    assert e.value.code == -1
+    badt = tgt.copy(); badt[0] = 4
+    with pytest.raises(G.GbbsError):
+        G.Graph(off, badt)
+    with pytest.raises(G.GbbsError):
+        G.gbbs_graph_create(4, tgt.shape[0] + 1, off, tgt)
+    with pytest.raises(G.GbbsError) as e:
+        G.Graph(off, tgt, borrow=True)          # host arrays cannot be borrowed
+    assert e.value.code == -1
+    # weights whose max * (n-1) overflows uint32 distances
+    big = np.full(tgt.shape, 0xF0000000, np.uint32)
+    g = G.Graph(off, tgt, big, symmetric=True)
+    with pytest.raises(G.GbbsError) as e:
+        g.bellman_ford(0, d)
+    assert e.value.code == -2
+    g.bfs(0, d)      # BFS ignores weights
+    g.close()
+
+
+# ---- the BASELINE configs ------------------------------------------------------------
+
+def test_c1_generator_bit_identical_and_parity(G):
+    from graphgen import device
+    cfg = graphgen.CONFIGS["c1"]
+    off, tgt = graphgen.rmat_graph(cfg.levels, 1 << cfg.log_edges, cfg.graph_seed, *cfg.abc)
+    w = graphgen.pair_weights(off, tgt, cfg.weight_seed, cfg.W)
+    dg = device.build_config("c1")
+    assert (dg["offsets"].cpu().numpy() == off).all()
+    assert (dg["targets"].cpu().numpy().view(np.uint32) == tgt).all()
+    assert (dg["weights"].cpu().numpy().view(np.uint32) == w).all()
+    check_bfs_all_modes(G, off, tgt, [0], True)
+    check_bf(G, off, tgt, w, [0], True)
+    L = 9
+    toff, ttgt = graphgen.torus3d(L)
+    o2, t2 = device.torus_csr(L)
+    assert (o2.cpu().numpy() == toff).all() and (t2.cpu().numpy().view(np.uint32) == ttgt).all()
