@@ -162,6 +162,9 @@ typedef struct {
   int64_t acquired;       /* vertices won this round (incl. out-degree 0) */
   int64_t edges_examined; /* push: edges of U; pull: in-edges loaded      */
   int64_t vertices_swept; /* pull: unvisited vertices examined            */
+  int64_t t_start_ns;     /* device %globaltimer when the round started;  
+                             the record after the last round holds the   
+                             end time when rounds_cap allows             */
 } gbbs_round_stat;
 
 typedef struct {

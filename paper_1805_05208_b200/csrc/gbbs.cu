@@ -507,7 +507,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
     stats->dense_rounds = 0;
     stats->edges_examined = 0;
     if (want_rounds) {
-      long long nr = ctrl.rounds < cap ? ctrl.rounds : cap;
+      long long nr = ctrl.rounds + 1 < cap ? ctrl.rounds + 1 : cap;
       static_assert(sizeof(RoundStat) == sizeof(gbbs_round_stat), "stat layout");
       CU(cudaMemcpy(stats->rounds_out, g->dstats, (size_t)nr * sizeof(RoundStat),
                     cudaMemcpyDeviceToHost));

@@ -52,6 +52,7 @@ struct RoundStat {           // mirrors gbbs_round_stat
   long long acquired;
   long long edges_examined;
   long long vertices_swept;
+  long long t_start_ns;
 };
 
 struct Params {
@@ -108,6 +109,12 @@ __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long l
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -465,6 +472,8 @@ __global__ void __launch_bounds__(BLOCK) traverse_kernel(Params p) {
     const unsigned long long c = s.cnt;
     const long long f = (long long)(c >> p.ebits);
     const long long E = (long long)(c & emask);
+    if (STATS && blockIdx.x == 0 && tid == 0 && p.stats && r < p.stats_cap)
+      p.stats[r].t_start_ns = (long long)globaltimer_ns();
     if (f == 0) break;
     if (r >= p.max_rounds) {
       if (blockIdx.x == 0 && tid == 0) *p.status = 1;

@@ -42,7 +42,7 @@ class gbbs_round_stat(ctypes.Structure):
     _fields_ = [("dense", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("frontier", ctypes.c_int64), ("frontier_edges", ctypes.c_int64),
                 ("acquired", ctypes.c_int64), ("edges_examined", ctypes.c_int64),
-                ("vertices_swept", ctypes.c_int64)]
+                ("vertices_swept", ctypes.c_int64), ("t_start_ns", ctypes.c_int64)]
 
 
 class gbbs_stats(ctypes.Structure):
@@ -168,10 +168,19 @@ def make_stats(rounds_cap=0):
 
 
 def round_records(stats):
+    """Per-round dicts; `us` = device time of the round when the next record's
+    timestamp is available (the record after the last round holds the end time)."""
     n = min(stats.rounds, stats.rounds_cap)
-    return [dict(dense=r.dense, frontier=r.frontier, frontier_edges=r.frontier_edges,
-                 acquired=r.acquired, edges_examined=r.edges_examined,
-                 vertices_swept=r.vertices_swept) for r in stats.rounds_out[:n]] if n else []
+    if not n:
+        return []
+    raw = stats.rounds_out[:min(stats.rounds + 1, stats.rounds_cap)]
+    out = []
+    for i, r in enumerate(raw[:n]):
+        us = (raw[i + 1].t_start_ns - r.t_start_ns) / 1e3 if i + 1 < len(raw) else None
+        out.append(dict(dense=r.dense, frontier=r.frontier, frontier_edges=r.frontier_edges,
+                        acquired=r.acquired, edges_examined=r.edges_examined,
+                        vertices_swept=r.vertices_swept, us=us))
+    return out
 
 
 class Graph:
