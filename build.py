@@ -74,5 +74,5 @@ def build_all(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    for o in build_all(force="--force" in sys.argv, verbose=True):
+    for o in build_all(force="--force" in sys.argv, verbose="-v" in sys.argv):
         print("built", o)

@@ -162,9 +162,11 @@ typedef struct {
   int64_t acquired;       /* vertices won this round (incl. out-degree 0) */
   int64_t edges_examined; /* push: edges of U; pull: in-edges loaded      */
   int64_t vertices_swept; /* pull: unvisited vertices examined            */
-  int64_t t_start_ns;     /* device %globaltimer when the round started;  
-                             the record after the last round holds the   
+  int64_t t_start_ns;     /* device %globaltimer when the round started;
+                             the record after the last round holds the
                              end time when rounds_cap allows             */
+  int64_t t_work_ns;      /* latest end of edge work over all CTAs      */
+  int64_t t_flush_ns;     /* latest end of the final flush over all CTAs */
 } gbbs_round_stat;
 
 typedef struct {

@@ -56,14 +56,18 @@ struct gbbs_graph {
   long long *off = nullptr;
   uint32_t *tgt = nullptr;
   uint32_t *wgt = nullptr;
-  bool own_arrays = true;
+  bool own_off = true, own_tgt = true, own_wgt = true;
+  uint32_t *odeg = nullptr;  // out-degrees, directed graphs only
   long long *in_off = nullptr;  // alias of off when symmetric
   uint32_t *in_tgt = nullptr;
   // scratch
   uint32_t *bm[2] = {nullptr, nullptr};
-  uint32_t *fv[2] = {nullptr, nullptr};
-  long long *fo[2] = {nullptr, nullptr};
-  long long *fb[2] = {nullptr, nullptr};
+  uint32_t *fv[3] = {nullptr, nullptr, nullptr};  // round lists 0/1, heavy list 2
+  long long *fo[3] = {nullptr, nullptr, nullptr};
+  long long *fb[3] = {nullptr, nullptr, nullptr};
+  uint32_t *tab[3] = {nullptr, nullptr, nullptr};
+  uint32_t *iso = nullptr;
+  unsigned long long *part = nullptr;
   unsigned long long *cnt = nullptr;  // [4] + ctrl
   int *status = nullptr;
   long long *rounds = nullptr;
@@ -78,20 +82,22 @@ struct gbbs_graph {
 
 static void free_graph(gbbs_graph *g) {
   if (!g) return;
-  if (g->own_arrays) {
-    cudaFree(g->off);
-    cudaFree(g->tgt);
-    cudaFree(g->wgt);
-  }
+  if (g->own_off) cudaFree(g->off);
+  if (g->own_tgt) cudaFree(g->tgt);
+  if (g->own_wgt) cudaFree(g->wgt);
+  cudaFree(g->odeg);
   if (g->in_off && g->in_off != g->off) cudaFree(g->in_off);
   if (g->in_tgt && g->in_tgt != g->tgt) cudaFree(g->in_tgt);
-  for (int i = 0; i < 2; i++) {
-    cudaFree(g->bm[i]);
+  for (int i = 0; i < 3; i++) {
+    if (i < 2) cudaFree(g->bm[i]);
     cudaFree(g->fv[i]);
     cudaFree(g->fo[i]);
     cudaFree(g->fb[i]);
+    cudaFree(g->tab[i]);
   }
   cudaFree(g->cnt);
+  cudaFree(g->iso);
+  cudaFree(g->part);
   cudaFree(g->tmp_dist);
   cudaFree(g->tmp_parent);
   cudaFree(g->dstats);
@@ -151,6 +157,24 @@ __global__ void k_csc_from_keys(const unsigned long long *keys, long long n, lon
     long long last = (m == 0) ? -1 : (long long)(keys[m - 1] >> 32);
     for (long long x = last + 1; x <= n; x++) in_off[x] = m;
   }
+}
+
+// Bit v of word v/32 set iff v has no in- and no out-edges (or v >= n, padding):
+// such vertices can never be reached nor be anyone's in-neighbour, so BFS starts
+// with them marked visited and dense rounds skip them.
+__global__ void k_isolated(const long long *off, const long long *in_off, long long n,
+                           long long nwords, uint32_t *iso) {
+  long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((v >> 5) >= nwords) return;
+  bool z = true;
+  if (v < n) z = off[v] == off[v + 1] && in_off[v] == in_off[v + 1];
+  unsigned b = __ballot_sync(0xffffffffu, z);
+  if ((threadIdx.x & 31) == 0) iso[v >> 5] = b;
+}
+
+__global__ void k_out_degree(const long long *off, long long n, uint32_t *deg) {
+  long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n) deg[v] = (uint32_t)(off[v + 1] - off[v]);
 }
 
 static int bits_for(unsigned long long x) {  // bits needed to represent x (>= 1)
@@ -216,12 +240,17 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
     if (!is_device_ptr(offsets) || (m > 0 && !is_device_ptr(targets)) ||
         (weights && !is_device_ptr(weights)))
       return fail(GBBS_EINVAL, "GBBS_BORROW requires device pointers");
-    g->own_arrays = false;
+    g->own_off = g->own_tgt = g->own_wgt = false;
     g->off = (long long *)offsets;
     g->tgt = (uint32_t *)targets;
     g->wgt = (uint32_t *)weights;
+    // dense rounds read in-edges with 16-byte vector loads: copy a misaligned array
+    if (((uintptr_t)targets & 15) != 0) {
+      g->tgt = nullptr;
+      g->own_tgt = true;
+      if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4))) return rc;
+    }
   } else {
-    g->own_arrays = true;
     if ((rc = copy_in((void **)&g->off, offsets, (size_t)(n + 1) * 8))) return rc;
     if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4))) return rc;
     if (weights && (rc = copy_in((void **)&g->wgt, weights, (size_t)m * 4))) return rc;
@@ -302,12 +331,23 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
   for (int i = 0; i < 2; i++) {
     CU(cudaMalloc(&g->bm[i], (size_t)g->nwords * 4));
     CU(cudaMemset(g->bm[i], 0, (size_t)g->nwords * 4));
+  }
+  for (int i = 0; i < 3; i++) {
     CU(cudaMalloc(&g->fv[i], (size_t)n * 4));
     CU(cudaMalloc(&g->fo[i], (size_t)n * 8));
     CU(cudaMalloc(&g->fb[i], (size_t)n * 8));
+    CU(cudaMalloc(&g->tab[i], (size_t)(m / TE + 2) * 4));
   }
-  CU(cudaMalloc(&g->cnt, 8 * 8));
-  CU(cudaMemset(g->cnt, 0, 8 * 8));
+  if (!(flags & GBBS_SYMMETRIC)) {
+    CU(cudaMalloc(&g->odeg, (size_t)n * 4));
+    k_out_degree<<<(unsigned)((n + 255) / 256), 256>>>(g->off, n, g->odeg);
+    CU(cudaGetLastError());
+  }
+  CU(cudaMalloc(&g->iso, (size_t)g->nwords * 4));
+  k_isolated<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->in_off, n, g->nwords, g->iso);
+  CU(cudaGetLastError());
+  CU(cudaMalloc(&g->cnt, 10 * 8));  // ring[4], status, rounds, count, -, heavy[2]
+  CU(cudaMemset(g->cnt, 0, 10 * 8));
   g->status = (int *)(g->cnt + 4);
   g->rounds = (long long *)(g->cnt + 5);
   g->dcount = g->cnt + 6;
@@ -315,6 +355,10 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
   if ((rc = occupancy_grid<ALGO_BFS, true>(&g->grid[0][1]))) return rc;
   if ((rc = occupancy_grid<ALGO_BF, false>(&g->grid[1][0]))) return rc;
   if ((rc = occupancy_grid<ALGO_BF, true>(&g->grid[1][1]))) return rc;
+  int gmax = 0;
+  for (int a = 0; a < 2; a++)
+    for (int b = 0; b < 2; b++) gmax = gmax > g->grid[a][b] ? gmax : g->grid[a][b];
+  CU(cudaMalloc(&g->part, (size_t)gmax * 16));
   CU(cudaDeviceSynchronize());
   return GBBS_OK;
 }
@@ -449,13 +493,16 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   p.in_tgt = g->in_tgt;
   p.dist = ddist;
   p.parent = (algo == ALGO_BFS) ? dpar : nullptr;
-  for (int i = 0; i < 2; i++) {
-    p.bm[i] = g->bm[i];
+  p.bm[0] = g->bm[0];
+  p.bm[1] = g->bm[1];
+  for (int i = 0; i < 3; i++) {
     p.fv[i] = g->fv[i];
     p.fo[i] = g->fo[i];
     p.fb[i] = g->fb[i];
+    p.tab[i] = g->tab[i];
   }
   p.cnt = g->cnt;
+  p.hcnt = g->cnt + 8;
   p.status = g->status;
   p.rounds_out = g->rounds;
   p.stats = want_rounds ? g->dstats : nullptr;
@@ -464,7 +511,10 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   p.dense_threshold = g->m / (long long)o.threshold_den;
   p.max_rounds = g->n + 1;
   p.ebits = g->ebits;
-  p.mode = (algo == ALGO_BFS) ? o.mode : 1;
+  p.iso = g->iso;
+  p.odeg = g->odeg;
+  p.symmetric = (g->flags & GBBS_SYMMETRIC) ? 1 : 0;
+  p.mode = o.mode;
   p.src = src;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -512,7 +562,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
       CU(cudaMemcpy(stats->rounds_out, g->dstats, (size_t)nr * sizeof(RoundStat),
                     cudaMemcpyDeviceToHost));
       for (long long i = 0; i < nr; i++) {
-        stats->dense_rounds += stats->rounds_out[i].dense;
+        stats->dense_rounds += stats->rounds_out[i].dense == 1;
         stats->edges_examined += stats->rounds_out[i].edges_examined;
       }
     }

@@ -1,28 +1,39 @@
 // traverse.cuh — the persistent frontier-traversal kernel (BFS and Bellman-Ford).
 //
-// One cooperative launch runs the whole traversal: init, then
-// rounds of the paper's edgeMap (sec:prelims) separated by
-// a grid-wide barrier (the round synchronisation of PAPER.md:89-90).  Each
-// round is either
-//   * sparse push (a3-a7): the frontier is a vertex list whose entries carry
-//     their exclusive edge prefix O (the scan of PAPER.md:1079-1080, computed
-//     when the entry was appended, see flush()) and base = offset - O.  The
-//     round's d_U edges are cut into fixed tiles of TE edges (edgeMapBlocked's
-//     blocks); a tile finds its first/last
-//     owner by a warp-wide 32-ary search of O, expands owner ids over its
-//     edges with a shared-memory max-scan, loads targets coalesced, and
-//     applies F: BFS test-and-set as an atomic fetch-or
-//     on the visited bit, Bellman-Ford priority-write as
-//     atomicMin on dist followed by a test-and-set on the next-frontier bit.
-//     Winners are packed (warp ballot -> shared staging -> one global atomic per
-//     flush), i.e. at most LN(U) writes;
-//   * dense pull (a8, BFS only): every unvisited vertex scans its in-edges in
-//     order and stops at the first one from the frontier (the early-exit dense
-//     method of PAPER.md:1870-1874).  A warp owns one 32-vertex bitmap word,
-//     so the next visited word is written without atomics.
-// The direction is chosen per round from |U| + sum deg(U) against m/T
-// (reading A10), read from the packed counter that the
-// previous round's flushes produced.
+// One cooperative launch runs a whole traversal: per-run init (SURVEY §8(a)
+// a1), then rounds of the paper's edgeMap (sec:prelims)
+// separated by a grid-wide barrier (the round synchronisation of
+// PAPER.md:89-90).  Inside a round every warp works on its own; the only other
+// barrier is the one before heavy vertices of a bitmap-forward round.
+//
+// Round kinds (the representation is chosen per round from |U| + sum deg(U)
+// against m/T; reading A10):
+//  * list push (sparse, a3-a7).  The frontier is a vertex list whose entries
+//    carry their exclusive edge prefix O (the scan of PAPER.md:1079-1080) and
+//    base = offset(v) - O, both produced when the entry was appended.  The
+//    round's d_U edges are cut into fixed tiles of TE edges, one warp per tile
+//    (edgeMapBlocked's fixed-size blocks: a
+//    high-degree vertex spans many tiles).  Instead of a binary search of O
+//     a tile reads its first owner from a tile->owner table
+//    written by the producer of the list.
+//  * dense pull (a8, BFS).  Each unvisited vertex scans its in-edges in order
+//    and stops at the first visited one (the early-exit dense method,
+//    PAPER.md:1870-1874).  Every visited in-neighbour of an unvisited vertex
+//    lies on the current level, so the visited bitmap (snapshot, double
+//    buffered) serves as the frontier.  A warp owns whole 32-vertex words, so
+//    the next bitmap is written without atomics; only (|U'|, sum deg) is
+//    emitted.
+//  * bitmap-forward push (a9/a10).  The frontier is a bitmap (BFS: the
+//    vertices a dense round just added; Bellman-Ford: the next-frontier TS
+//    bits); warps sweep its words and push the out-edges of its vertices
+//    (lane per vertex, warp per vertex above 32 edges).  Vertices above HEAVY
+//    edges are appended to a heavy list that is pushed with list-push tiles
+//    after a grid barrier, so hubs are spread over many warps.
+// F is the BFS test-and-set as an atomic fetch-or on the
+// visited bit, or the Bellman-Ford priority-write as
+// atomicMin on dist followed by a test-and-set on the next-frontier bit.
+// Winners are packed per warp (ballot -> shared staging -> one packed 64-bit
+// atomicAdd per flush), i.e. at most LN(U) writes.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -34,15 +45,23 @@ namespace cg = cooperative_groups;
 
 constexpr int BLOCK = 256;            // threads per CTA
 constexpr int NWARPS = BLOCK / 32;
-constexpr int EPT = 4;                // edges per thread per tile
-constexpr int TE = BLOCK * EPT;       // edges per tile (edgeMapBlocked bsize)
-constexpr int CAP = 2 * TE;           // shared staging capacity (vertices)
+constexpr int TE = 256;               // edges per warp tile (edgeMapBlocked bsize)
+constexpr int NCH = 4;                // 32-edge chunks in flight per batch
+constexpr int WCAP = 384;             // per-warp staging capacity (vertices)
+#ifndef GBBS_PW
+#define GBBS_PW 2
+#endif
+constexpr int PW = GBBS_PW;           // bitmap words per warp iteration
+constexpr long long HEAVY = 512;      // bitmap-forward: deferred to heavy tiles above this
 constexpr uint32_t INF = 0xFFFFFFFFu;
-constexpr int KBITS = 11;             // head = (tag << KBITS) | owner slot
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int KBITS = 10;             // head slot = (tag << KBITS) | owner index
 constexpr int32_t KMASK = (1 << KBITS) - 1;
 constexpr int32_t TAG_MAX = (1 << (31 - KBITS)) - 1;
 
 enum Algo { ALGO_BFS = 0, ALGO_BF = 1 };
+enum Emit { EMIT_LIST = 0, EMIT_COUNT = 1 };
+enum { LIST_HEAVY = 2 };
 
 struct RoundStat {           // mirrors gbbs_round_stat
   int32_t dense;
@@ -53,6 +72,8 @@ struct RoundStat {           // mirrors gbbs_round_stat
   long long edges_examined;
   long long vertices_swept;
   long long t_start_ns;
+  long long t_work_ns;
+  long long t_flush_ns;
 };
 
 struct Params {
@@ -62,13 +83,17 @@ struct Params {
   const uint32_t *wgt;       // weights [m] or nullptr (unit)
   const long long *in_off;   // in-CSC (alias of CSR when symmetric)
   const uint32_t *in_tgt;
+  const uint32_t *iso;       // [nwords] isolated-vertex (+padding) mask
+  const uint32_t *odeg;      // out-degrees (directed graphs; nullptr if symmetric)
   uint32_t *dist;            // [n]
   uint32_t *parent;          // [n] or nullptr
-  uint32_t *bm[2];           // BFS: visited (double-buffered); BF: next-frontier bits
-  uint32_t *fv[2];           // frontier lists: vertex
-  long long *fo[2];          //                 exclusive edge prefix O
-  long long *fb[2];          //                 base = offset(v) - O
+  uint32_t *bm[2];           // BFS: visited (double-buffered); BF: frontier TS bits
+  uint32_t *fv[3];           // lists 0/1 (rounds) and 2 (heavy): vertex
+  long long *fo[3];          //   exclusive edge prefix O
+  long long *fb[3];          //   base = offset(v) - O
+  uint32_t *tab[3];          //   tile -> first owner entry
   unsigned long long *cnt;   // packed (count << ebits | edges) ring [4]
+  unsigned long long *hcnt;  // heavy-list packed counters [2]
   int *status;               // 0 ok, 1 = round cap hit
   long long *rounds_out;
   RoundStat *stats;          // per round, or nullptr
@@ -78,23 +103,30 @@ struct Params {
   long long max_rounds;
   int ebits;
   int mode;                  // 0 auto, 1 sparse, 2 dense
+  int symmetric;
   uint32_t src;
 };
 
+struct WarpSmem {             // one per warp; nothing here is shared across warps
+  alignas(16) int32_t head[TE];  // owner index of every edge slot of the tile
+  long long base[TE + 1];        // owner base (offset - O)
+  uint32_t own[TE + 1];          // owner vertex (BFS) or its distance (BF)
+  uint32_t stage[WCAP];          // winners awaiting warp_flush
+};
+
 struct Smem {
-  int64_t own_base[TE];
-  uint32_t own_u[TE];
-  uint32_t own_du[TE];
-  int32_t head[TE];
-  uint32_t stage[CAP];
-  unsigned long long wk[NWARPS];
-  unsigned long long wd[NWARPS];
-  int32_t wmax[NWARPS];
-  long long i0, i1;
-  unsigned long long base_k, base_d;
-  unsigned long long cnt;
-  int stage_n;
-  int tag;
+  WarpSmem w[NWARPS];
+  unsigned long long sacc[5];
+  unsigned long long cnt, hcnt;
+};
+
+// Per-warp round state kept in registers: staging count, emitted (K, D) for
+// EMIT_COUNT rounds, and gbbs_round_stat counters (STATS builds only).
+struct WarpState {
+  int scnt = 0;
+  int tag = 0;
+  unsigned long long K = 0, D = 0;
+  unsigned long long edges = 0, swept = 0, acquired = 0;
 };
 
 // ---- small device helpers --------------------------------------------------
@@ -123,9 +155,15 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return r;
 }
 
+__device__ __forceinline__ unsigned lanemask_le() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ long long warp_sum64(long long x) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
   return x;
 }
 
@@ -133,301 +171,677 @@ __device__ __forceinline__ long long warp_excl_sum64(long long x, int lane) {
   long long inc = x;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    long long y = __shfl_up_sync(0xffffffffu, inc, o);
+    long long y = __shfl_up_sync(FULL, inc, o);
     if (lane >= o) inc += y;
   }
   return inc - x;
 }
 
-// Largest i in [0, f) with O[i] <= key (O strictly increasing, O[0] = 0 <= key).
-// Warp-cooperative 32-ary search: ~log32(f) dependent L2 round trips.
-__device__ __forceinline__ long long warp_owner_search(const long long *O, long long f,
-                                                       long long key, int lane) {
-  long long lo = 0, hi = f;
-  while (hi - lo > 32) {
-    long long step = (hi - lo + 31) >> 5;
-    long long idx = lo + (long long)lane * step;
-    bool ok = idx < hi && __ldcg(O + idx) <= key;
-    unsigned b = __ballot_sync(0xffffffffu, ok);
-    int last = 31 - __clz(b);
-    lo = lo + (long long)last * step;
-    long long nh = lo + step;
-    hi = nh < hi ? nh : hi;
-  }
-  long long idx = lo + lane;
-  bool ok = idx < hi && __ldcg(O + idx) <= key;
-  unsigned b = __ballot_sync(0xffffffffu, ok);
-  return lo + (31 - __clz(b));
+// Record, for every TE-edge tile whose first edge falls in [o, o+deg), that
+// entry `pos` owns it (the tile's starting owner for the next round).
+__device__ __forceinline__ void mark_tiles(uint32_t *tab, unsigned long long pos, long long o,
+                                           long long deg) {
+  long long t = (o + TE - 1) / TE;
+  const long long tl = (o + deg - 1) / TE;
+  for (; t <= tl; t++) tab[t] = (uint32_t)pos;
 }
 
-// Append the calling lanes with `win` set to the shared staging buffer.
-__device__ __forceinline__ void stage_push(Smem &s, bool win, uint32_t v, int lane) {
-  unsigned b = __ballot_sync(0xffffffffu, win);
-  if (b == 0) return;
-  int base = 0;
-  if (lane == 0) base = atomicAdd(&s.stage_n, __popc(b));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (win) s.stage[base + __popc(b & lanemask_lt())] = v;
+// Append the lanes' (v, a = offset(v), deg > 0) to list `nb` at positions and
+// edge prefixes reserved by one packed atomicAdd on *ctr (warp-uniform call).
+__device__ __forceinline__ void warp_append(const Params &p, int nb, unsigned long long *ctr,
+                                            bool keep, uint32_t v, long long a, long long deg) {
+  const int lane = threadIdx.x & 31;
+  const unsigned bal = __ballot_sync(FULL, keep);
+  if (!bal) return;
+  const long long dg = keep ? deg : 0;
+  const long long dex = warp_excl_sum64(dg, lane);
+  const long long tot = __shfl_sync(FULL, dex + dg, 31);
+  unsigned long long old = 0;
+  if (lane == 0) old = atomicAdd(ctr, ((unsigned long long)__popc(bal) << p.ebits) | (unsigned long long)tot);
+  old = __shfl_sync(FULL, old, 0);
+  if (keep) {
+    const unsigned long long pos = (old >> p.ebits) + __popc(bal & lanemask_lt());
+    const long long o = (long long)(old & ((1ull << p.ebits) - 1)) + dex;
+    p.fv[nb][pos] = v;
+    p.fo[nb][pos] = o;
+    p.fb[nb][pos] = a - o;
+    mark_tiles(p.tab[nb], pos, o, deg);
+  }
 }
 
-// Flush the staging buffer into the next frontier list (a7).  Entries with
-// out-degree 0 are dropped (they have no edges to process); the others are
-// written at positions reserved with ONE 64-bit atomicAdd of the packed
-// (count, edge-sum) pair, which also yields their exclusive edge prefix O —
-// so the next round needs no separate degree scan.  Block-uniform call.
-template <int ALGO, bool STATS>
-__device__ void flush(Smem &s, const Params &p, int nb, int r, uint32_t *bits_next) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cnt = s.stage_n;  // read after the caller's __syncthreads
-  if (cnt == 0) return;
-  int per = (cnt + NWARPS - 1) / NWARPS;
-  per = (per + 31) & ~31;
-  const int lo = warp * per;
-  const int hi = min(lo + per, cnt);
-  const unsigned long long emask = (1ull << p.ebits) - 1;
-
-  unsigned long long K = 0, D = 0;
-  for (int b0 = lo; b0 < hi; b0 += 32) {
-    int i = b0 + lane;
-    long long deg = 0;
-    if (i < hi) {
-      uint32_t v = s.stage[i];
-      deg = __ldg(p.off + v + 1) - __ldg(p.off + v);
+// Write `cnt` staged vertices of this warp into the next frontier list (a7).
+// Out-degree-0 vertices are dropped (no edges to process).  ONE packed 64-bit
+// atomicAdd of (count, edge-sum) reserves positions AND their exclusive edge
+// prefix O, so the next round needs no degree scan.  Offsets are loaded FL
+// entries per lane at a time.  Warp-uniform call.
+template <int ALGO>
+__device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, int cnt, int nb,
+                                           int r, uint32_t *bits_next) {
+  constexpr int FL = 4;
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  long long Kl = 0, Dl = 0;
+  for (int b0 = 0; b0 < cnt; b0 += 32 * FL) {
+    long long lo[FL], hi[FL];
+#pragma unroll
+    for (int u = 0; u < FL; u++) {
+      const int i = b0 + 32 * u + lane;
+      lo[u] = hi[u] = 0;
+      if (i < cnt) {
+        const uint32_t v = st[i];
+        lo[u] = __ldg(p.off + v);
+        hi[u] = __ldg(p.off + v + 1);
+      }
     }
-    K += __popc(__ballot_sync(0xffffffffu, deg > 0));
-    D += (unsigned long long)warp_sum64(deg);
-  }
-  if (lane == 0) { s.wk[warp] = K; s.wd[warp] = D; }
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long ak = 0, ad = 0;
-    for (int w = 0; w < NWARPS; w++) {
-      unsigned long long k = s.wk[w], d = s.wd[w];
-      s.wk[w] = ak; s.wd[w] = ad;
-      ak += k; ad += d;
+#pragma unroll
+    for (int u = 0; u < FL; u++) {
+      Kl += hi[u] > lo[u];
+      Dl += hi[u] - lo[u];
     }
-    unsigned long long old = 0;
-    if (ak > 0) old = atomicAdd(p.cnt + ((r + 1) & 3), (ak << p.ebits) | ad);
-    s.base_k = old >> p.ebits;
-    s.base_d = old & emask;
-    if (STATS && p.stats && r < p.stats_cap)
-      atomicAdd((unsigned long long *)&p.stats[r].acquired, (unsigned long long)cnt);
   }
-  __syncthreads();
-  unsigned long long k = s.base_k + s.wk[warp];
-  unsigned long long d = s.base_d + s.wd[warp];
+  const unsigned long long K = warp_sum64(Kl), D = warp_sum64(Dl);
+  unsigned long long old = 0;
+  if (lane == 0 && K) old = atomicAdd(p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
+  old = __shfl_sync(FULL, old, 0);
+  unsigned long long k = old >> p.ebits;
+  unsigned long long d = old & ((1ull << p.ebits) - 1);
   uint32_t *fv = p.fv[nb];
   long long *fo = p.fo[nb];
   long long *fb = p.fb[nb];
-  for (int b0 = lo; b0 < hi; b0 += 32) {
-    int i = b0 + lane;
-    long long deg = 0, a = 0;
-    uint32_t v = 0;
-    if (i < hi) {
-      v = s.stage[i];
-      a = __ldg(p.off + v);
-      deg = __ldg(p.off + v + 1) - a;
+  uint32_t *tab = p.tab[nb];
+  for (int b0 = 0; b0 < cnt; b0 += 32 * FL) {
+    uint32_t vv[FL];
+    long long lo[FL], hi[FL];
+#pragma unroll
+    for (int u = 0; u < FL; u++) {
+      const int i = b0 + 32 * u + lane;
+      vv[u] = 0;
+      lo[u] = hi[u] = 0;
+      if (i < cnt) {
+        vv[u] = st[i];
+        lo[u] = __ldg(p.off + vv[u]);
+        hi[u] = __ldg(p.off + vv[u] + 1);
+      }
     }
-    bool keep = deg > 0;
-    unsigned bal = __ballot_sync(0xffffffffu, keep);
-    long long dex = warp_excl_sum64(deg, lane);
-    if (keep) {
-      unsigned long long pos = k + __popc(bal & lanemask_lt());
-      long long o = (long long)d + dex;
-      fv[pos] = v;
-      fo[pos] = o;
-      fb[pos] = a - o;
-    } else if (ALGO == ALGO_BF && i < hi) {
-      // out-degree-0 vertex: it never enters a frontier; release its TS bit.
-      atomicAnd(bits_next + (v >> 5), ~(1u << (v & 31)));
+#pragma unroll
+    for (int u = 0; u < FL; u++) {
+      const int i = b0 + 32 * u + lane;
+      const long long deg = hi[u] - lo[u];
+      const bool keep = deg > 0;
+      const unsigned bal = __ballot_sync(FULL, keep);
+      const long long dex = warp_excl_sum64(deg, lane);
+      if (keep) {
+        const unsigned long long pos = k + __popc(bal & lanemask_lt());
+        const long long o = (long long)d + dex;
+        fv[pos] = vv[u];
+        fo[pos] = o;
+        fb[pos] = lo[u] - o;
+        mark_tiles(tab, pos, o, deg);
+      } else if (ALGO == ALGO_BF && i < cnt) {
+        // out-degree-0 vertex: it never enters a frontier; release its TS bit.
+        atomicAnd(bits_next + (vv[u] >> 5), ~(1u << (vv[u] & 31)));
+      }
+      k += __popc(bal);
+      d += (unsigned long long)__shfl_sync(FULL, dex + deg, 31);
     }
-    k += __popc(bal);
-    d += (unsigned long long)__shfl_sync(0xffffffffu, dex + deg, 31);
   }
-  __syncthreads();
-  if (tid == 0) s.stage_n = 0;
-  __syncthreads();
+  __syncwarp();
 }
 
-// ---- sparse push: one tile of TE edges --------------------------------------
+// ---- F: apply one batch of NCH 32-edge chunks -------------------------------------
+// vv = targets, uu = owner id (BFS parent) or owner distance (BF), ww = weights.
+// EMIT_LIST: winners go to the warp's staging buffer (flushed into list cb^1).
+// EMIT_COUNT: winners are only counted (K, D) — the TS bits are the frontier.
+template <int ALGO, bool STATS, int EMIT>
+__device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpState &ws,
+                                            const uint32_t (&vv)[NCH], const uint32_t (&uu)[NCH],
+                                            const uint32_t (&ww)[NCH], const bool (&act)[NCH],
+                                            int nb, int r, uint32_t *bits, const uint32_t *prebits) {
+  const int lane = threadIdx.x & 31;
+  bool win[NCH];
+  if (ALGO == ALGO_BFS) {
+    uint32_t pre[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) pre[j] = act[j] ? prebits[vv[j] >> 5] : FULL;
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      const uint32_t bit = 1u << (vv[j] & 31);
+      win[j] = false;
+      if (!(pre[j] & bit)) {
+        const uint32_t old = atomicOr(bits + (vv[j] >> 5), bit);  // test-and-set
+        win[j] = !(old & bit);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      if (win[j]) {
+        p.dist[vv[j]] = (uint32_t)(r + 1);
+        if (p.parent) p.parent[vv[j]] = uu[j];
+      }
+    }
+  } else {
+    unsigned long long nd[NCH];
+    uint32_t cur[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      nd[j] = (unsigned long long)uu[j] + ww[j];
+      cur[j] = act[j] ? p.dist[vv[j]] : 0u;
+    }
+    bool cand[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      cand[j] = false;
+      if (nd[j] < (unsigned long long)cur[j]) {
+        const uint32_t old = atomicMin(p.dist + vv[j], (uint32_t)nd[j]);  // priority-write
+        cand[j] = nd[j] < (unsigned long long)old;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      win[j] = false;
+      if (cand[j]) {
+        const uint32_t bit = 1u << (vv[j] & 31);
+        const uint32_t ob = atomicOr(bits + (vv[j] >> 5), bit);  // next-frontier TS
+        win[j] = !(ob & bit);
+      }
+    }
+  }
+  if (EMIT == EMIT_COUNT) {
+    long long lo[NCH], hi[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      lo[j] = hi[j] = 0;
+      if (win[j]) {
+        lo[j] = __ldg(p.off + vv[j]);
+        hi[j] = __ldg(p.off + vv[j] + 1);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      ws.K += hi[j] > lo[j];
+      ws.D += (unsigned long long)(hi[j] - lo[j]);
+      if (STATS) ws.acquired += win[j];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      const unsigned b = __ballot_sync(FULL, win[j]);
+      if (win[j]) st[ws.scnt + __popc(b & lanemask_lt())] = vv[j];
+      ws.scnt += __popc(b);
+    }
+    if (ws.scnt > WCAP - 32 * NCH) {
+      if (STATS && lane == 0) ws.acquired += ws.scnt;
+      warp_flush<ALGO>(p, st, ws.scnt, nb, r, bits);
+      ws.scnt = 0;
+    }
+  }
+}
 
-template <int ALGO, bool STATS>
-__device__ void push_tile(Smem &s, const Params &p, long long tile, long long f, long long E,
-                          int cb, int r, uint32_t *bits) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long ts = tile * TE;
+// ---- list push: one warp, one tile of TE edges of list `lb` ---------------------
+
+template <int ALGO, bool STATS, int EMIT>
+__device__ __forceinline__ void push_tile(const Params &p, WarpSmem &w, WarpState &ws, int lb,
+                                          long long t, long long ntiles, long long f, long long E,
+                                          int nb, int r, uint32_t *bits, const uint32_t *prebits) {
+  const int lane = threadIdx.x & 31;
+  const long long ts = t * TE;
   const long long te = min(ts + (long long)TE, E);
-  const long long *O = p.fo[cb];
-  const long long *B = p.fb[cb];
-  const uint32_t *F = p.fv[cb];
+  const long long *O = p.fo[lb];
+  const long long *B = p.fb[lb];
+  const uint32_t *F = p.fv[lb];
+  const long long i0 = __ldcg(p.tab[lb] + t);
+  const long long il = (t + 1 < ntiles) ? (long long)__ldcg(p.tab[lb] + t + 1) : f - 1;
+  const int nown = (int)(il - i0 + 1);
+  if (STATS && lane == 0) ws.edges += (unsigned long long)(te - ts);
 
-  if (warp == 0) {
-    long long i0 = warp_owner_search(O, f, ts, lane);
-    if (lane == 0) s.i0 = i0;
-  } else if (warp == 1) {
-    long long i1 = warp_owner_search(O, f, te - 1, lane);
-    if (lane == 0) s.i1 = i1;
-  }
-  if (tid == 0) {
-    if (++s.tag >= TAG_MAX) {  // tag wrap: clear heads (rare)
-      for (int i = 0; i < TE; i++) s.head[i] = 0;
-      s.tag = 1;
-    }
-  }
-  __syncthreads();
-  const long long i0 = s.i0;
-  const int nown = (int)(s.i1 - i0 + 1);
-  const int32_t tagv = s.tag << KBITS;
-  // Stage the owners of this tile: u, base, (BF) current dist[u]; mark heads.
-  for (int kk = tid; kk < nown; kk += BLOCK) {
-    long long i = i0 + kk;
-    uint32_t u = __ldcg(F + i);
-    s.own_u[kk] = u;
-    s.own_base[kk] = __ldcg(B + i);
-    if (ALGO == ALGO_BF) s.own_du[kk] = ld_relaxed(p.dist + u);
-    if (nown > 1) {
-      long long o = __ldcg(O + i) - ts;
-      s.head[o > 0 ? o : 0] = tagv | kk;
-    }
-  }
-  __syncthreads();
-  if (nown > 1) {
-    // inclusive max-scan of head[] (owner id of every edge slot in the tile)
-    int4 h = reinterpret_cast<int4 *>(s.head)[tid];
-    int32_t a0 = h.x, a1 = max(a0, h.y), a2 = max(a1, h.z), a3 = max(a2, h.w);
-    int32_t inc = a3;
+  if (nown <= 32) {
+    // Register path: lane k holds owner i0+k; a chunk's owners come from a
+    // ballot (owners starting at or before the chunk) plus an or-reduce of the
+    // owners starting inside it.
+    const bool valid = lane < nown;
+    const long long k = i0 + lane;
+    const long long Ok = valid ? __ldcg(O + k) : 0x7FFFFFFFFFFFFFFFll;
+    const long long Bk = valid ? __ldcg(B + k) : 0;
+    const uint32_t Uk = valid ? __ldcg(F + k) : 0;
+    uint32_t Xk = Uk;
+    if (ALGO == ALGO_BF) Xk = valid ? ld_relaxed(p.dist + Uk) : 0;
+    for (long long cs = ts; cs < te; cs += 32 * NCH) {
+      uint32_t vv[NCH], ww[NCH], uu[NCH];
+      bool act[NCH];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc = max(inc, y);
-    }
-    if (lane == 31) s.wmax[warp] = inc;
-    int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane == 0) ex = 0;
-    __syncthreads();
-    for (int w = 0; w < warp; w++) ex = max(ex, s.wmax[w]);
-    reinterpret_cast<int4 *>(s.head)[tid] = make_int4(max(ex, a0), max(ex, a1), max(ex, a2), max(ex, a3));
-    __syncthreads();
-  }
-
-  uint32_t vv[EPT];
-  uint32_t ww[EPT];
-  int kk[EPT];
-  bool act[EPT];
-#pragma unroll
-  for (int j = 0; j < EPT; j++) {
-    int pos = j * BLOCK + tid;
-    long long e = ts + pos;
-    act[j] = e < te;
-    kk[j] = 0;
-    if (act[j]) {
-      int k = nown > 1 ? (s.head[pos] & KMASK) : 0;
-      kk[j] = k;
-      long long idx = s.own_base[k] + e;
-      vv[j] = __ldcs(p.tgt + idx);
-      if (ALGO == ALGO_BF) ww[j] = p.wgt ? __ldcs(p.wgt + idx) : 1u;
-    }
-  }
-  const uint32_t next_d = (uint32_t)(r + 1);
-#pragma unroll
-  for (int j = 0; j < EPT; j++) {
-    bool win = false;
-    uint32_t v = vv[j];
-    if (ALGO == ALGO_BFS) {
-      if (act[j]) {
-        uint32_t bit = 1u << (v & 31);
-        if (!(ld_relaxed(bits + (v >> 5)) & bit)) {
-          uint32_t old = atomicOr(bits + (v >> 5), bit);   // test-and-set
-          if (!(old & bit)) {
-            win = true;
-            p.dist[v] = next_d;
-            if (p.parent) p.parent[v] = s.own_u[kk[j]];
+      for (int j = 0; j < NCH; j++) {
+        const long long cst = cs + 32 * j;
+        const long long e = cst + lane;
+        act[j] = e < te;
+        vv[j] = 0;
+        ww[j] = 0;
+        uu[j] = 0;
+        if (cst < te) {  // warp-uniform
+          const int c0 = __popc(__ballot_sync(FULL, Ok <= cst)) - 1;
+          const long long rel = Ok - cst;
+          const unsigned hb = (rel > 0 && rel < 32) ? (1u << rel) : 0u;
+          const unsigned hm = __reduce_or_sync(FULL, hb);
+          const int own = c0 + __popc(hm & lanemask_le());
+          const long long bb = __shfl_sync(FULL, Bk, own);
+          uu[j] = __shfl_sync(FULL, Xk, own);
+          if (act[j]) {
+            vv[j] = __ldcs(p.tgt + bb + e);
+            if (ALGO == ALGO_BF) ww[j] = p.wgt ? __ldcs(p.wgt + bb + e) : 1u;
           }
         }
       }
-    } else {
-      if (act[j]) {
-        unsigned long long nd = (unsigned long long)s.own_du[kk[j]] + ww[j];
-        if (nd < (unsigned long long)ld_relaxed(p.dist + v)) {
-          uint32_t old = atomicMin(p.dist + v, (uint32_t)nd);  // priority-write
-          if (nd < old) {
-            uint32_t bit = 1u << (v & 31);
-            uint32_t ob = atomicOr(bits + (v >> 5), bit);      // next-frontier TS
-            win = !(ob & bit);
-          }
+      apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+    }
+  } else {
+    // Shared-memory path (many low-degree owners): stage every owner of the tile,
+    // mark the slot where each owner's first in-tile edge lies, and expand owner
+    // ids over the TE slots with a warp max-scan (slots hold tag << KBITS | k, so
+    // stale slots from earlier tiles lose to the current tag).
+    if (++ws.tag >= TAG_MAX) {
+      for (int i = lane; i < TE; i += 32) w.head[i] = 0;
+      ws.tag = 1;
+    }
+    const int32_t tv = ws.tag << KBITS;
+    for (int kb = 0; kb < nown; kb += 64) {
+      long long o2[2], b2[2];
+      uint32_t u2[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int kk = kb + 32 * h + lane;
+        o2[h] = 0x7FFFFFFFFFFFFFFFll;
+        b2[h] = 0;
+        u2[h] = 0;
+        if (kk < nown) {
+          o2[h] = __ldcg(O + i0 + kk) - ts;
+          b2[h] = __ldcg(B + i0 + kk);
+          u2[h] = __ldcg(F + i0 + kk);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int kk = kb + 32 * h + lane;
+        if (kk < nown) {
+          w.base[kk] = b2[h];
+          w.own[kk] = (ALGO == ALGO_BF) ? ld_relaxed(p.dist + u2[h]) : u2[h];
+          if (o2[h] < TE) w.head[o2[h] > 0 ? o2[h] : 0] = tv | kk;
         }
       }
     }
-    stage_push(s, win, v, lane);
+    __syncwarp();
+    {
+      constexpr int PER = TE / 32;
+      int32_t a[PER];
+      const int4 *h4 = reinterpret_cast<const int4 *>(w.head + lane * PER);
+#pragma unroll
+      for (int q = 0; q < PER / 4; q++) {
+        const int4 x = h4[q];
+        a[4 * q] = x.x; a[4 * q + 1] = x.y; a[4 * q + 2] = x.z; a[4 * q + 3] = x.w;
+      }
+#pragma unroll
+      for (int q = 1; q < PER; q++) a[q] = max(a[q], a[q - 1]);
+      int32_t inc = a[PER - 1];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc = max(inc, y);
+      }
+      int32_t ex = __shfl_up_sync(FULL, inc, 1);
+      if (lane == 0) ex = 0;
+      int4 *o4 = reinterpret_cast<int4 *>(w.head + lane * PER);
+#pragma unroll
+      for (int q = 0; q < PER / 4; q++)
+        o4[q] = make_int4(max(ex, a[4 * q]), max(ex, a[4 * q + 1]), max(ex, a[4 * q + 2]),
+                          max(ex, a[4 * q + 3]));
+    }
+    __syncwarp();
+    for (long long cs = ts; cs < te; cs += 32 * NCH) {
+      uint32_t vv[NCH], ww[NCH], uu[NCH];
+      bool act[NCH];
+#pragma unroll
+      for (int j = 0; j < NCH; j++) {
+        const long long e = cs + 32 * j + lane;
+        act[j] = e < te;
+        vv[j] = 0;
+        ww[j] = 0;
+        uu[j] = 0;
+        if (act[j]) {
+          const int kk = w.head[e - ts] & KMASK;
+          const long long bb = w.base[kk];
+          uu[j] = w.own[kk];
+          vv[j] = __ldcs(p.tgt + bb + e);
+          if (ALGO == ALGO_BF) ww[j] = p.wgt ? __ldcs(p.wgt + bb + e) : 1u;
+        }
+      }
+      apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+    }
+    __syncwarp();
   }
-  if (STATS && p.stats && r < p.stats_cap) {
-    long long ne = te - ts;
-    if (tid == 0) atomicAdd((unsigned long long *)&p.stats[r].edges_examined, (unsigned long long)ne);
-  }
-  __syncthreads();
 }
 
-// ---- dense pull (BFS): 8 bitmap words (256 vertices) per CTA iteration -------
+// ---- bitmap-forward push: PW frontier words per warp iteration ----------------------
+// BFS: frontier = vis_cur & ~vis_old (what the last dense round added); the TS
+// target is vis_old, which also absorbs the frontier bits (atomicOr) so that it
+// becomes the next visited set; vis_cur is read-only and serves as the pre-check.
+// BF: frontier = fr (this round's TS bits), cleared as swept; TS target = bits.
+// Each lane owns one vertex per word (PW vertices); the light vertices' edges
+// are walked as one flattened per-lane sequence, NCH edges per batch, so the
+// loads of different vertices overlap.
+template <int ALGO, bool STATS, int EMIT>
+__device__ __forceinline__ void forward_words(const Params &p, WarpSmem &w, WarpState &ws,
+                                              long long w0, uint32_t *fr, uint32_t *bits,
+                                              const uint32_t *precheck, int nb, int r) {
+  const uint32_t *prebits = (ALGO == ALGO_BFS) ? precheck : bits;
+  const int lane = threadIdx.x & 31;
+  uint32_t fw[PW];
+#pragma unroll
+  for (int q = 0; q < PW; q++) {
+    fw[q] = 0;
+    if (w0 + q < p.nwords) {
+      if (ALGO == ALGO_BFS) fw[q] = precheck[w0 + q] & ~ld_relaxed(bits + w0 + q);
+      else fw[q] = fr[w0 + q];
+    }
+  }
+  unsigned any = 0;
+#pragma unroll
+  for (int q = 0; q < PW; q++) {
+    any |= fw[q];
+    if (fw[q] && lane == 0) {
+      if (ALGO == ALGO_BFS) atomicOr(bits + w0 + q, fw[q]);
+      else fr[w0 + q] = 0;
+    }
+  }
+  if (!any) return;  // warp-uniform
+  long long a[PW];
+  int dg[PW];
+  uint32_t x[PW];
+#pragma unroll
+  for (int q = 0; q < PW; q++) {
+    a[q] = 0;
+    dg[q] = 0;
+    if ((fw[q] >> lane) & 1u) {
+      const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
+      a[q] = __ldg(p.off + v);
+      dg[q] = (int)(__ldg(p.off + v + 1) - a[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PW; q++) {
+    const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
+    x[q] = v;
+    if (ALGO == ALGO_BF) x[q] = dg[q] > 0 ? ld_relaxed(p.dist + v) : 0u;
+  }
+  int mine[PW];
+#pragma unroll
+  for (int q = 0; q < PW; q++) {
+    if (!fw[q]) {  // warp-uniform
+      mine[q] = 0;
+      continue;
+    }
+    const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
+    if (STATS && lane == 0) ws.swept += __popc(fw[q]);
+    // heavy vertices -> heavy list (pushed in tiles after the grid barrier)
+    const bool heavy = dg[q] > (int)HEAVY;
+    warp_append(p, LIST_HEAVY, p.hcnt + (r & 1), heavy, v, a[q], dg[q]);
+    // medium vertices: the whole warp walks one vertex's edges at a time
+    unsigned med = __ballot_sync(FULL, dg[q] > 32 && !heavy);
+    while (med) {
+      const int l = __ffs(med) - 1;
+      med &= med - 1;
+      const long long la = __shfl_sync(FULL, a[q], l);
+      const int ld = __shfl_sync(FULL, dg[q], l);
+      const uint32_t lx = __shfl_sync(FULL, x[q], l);
+      if (STATS && lane == 0) ws.edges += ld;
+      for (int cs = 0; cs < ld; cs += 32 * NCH) {
+        uint32_t vv[NCH], ww[NCH], uu[NCH];
+        bool act[NCH];
+#pragma unroll
+        for (int j = 0; j < NCH; j++) {
+          const int e = cs + 32 * j + lane;
+          act[j] = e < ld;
+          vv[j] = act[j] ? __ldcs(p.tgt + la + e) : 0;
+          ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? __ldcs(p.wgt + la + e) : 1u) : 0;
+          uu[j] = lx;
+        }
+        apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+      }
+    }
+    mine[q] = (dg[q] <= 32) ? dg[q] : 0;
+  }
+  // light vertices: one flattened edge sequence per lane over its PW vertices
+  int tot = 0;
+#pragma unroll
+  for (int q = 0; q < PW; q++) tot += mine[q];
+  if (STATS) ws.edges += tot;
+  int mx = tot;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+  for (int jj = 0; jj < mx; jj += NCH) {
+    uint32_t vv[NCH], ww[NCH], uu[NCH];
+    bool act[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      int idx = jj + j;
+      act[j] = idx < tot;
+      long long base = a[0];
+      uint32_t xo = x[0];
+#pragma unroll
+      for (int q = 0; q < PW - 1; q++) {  // locate the vertex holding flattened edge idx
+        if (idx >= mine[q]) {
+          idx -= mine[q];
+          base = a[q + 1];
+          xo = x[q + 1];
+        } else {
+          break;
+        }
+      }
+      vv[j] = act[j] ? __ldg(p.tgt + base + idx) : 0;
+      ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? __ldg(p.wgt + base + idx) : 1u) : 0;
+      uu[j] = xo;
+    }
+    apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+  }
+}
+
+// ---- dense pull (BFS): PW bitmap words per warp iteration -------------------------
+// Every lane owns one vertex per word.  In-edges are read as 16-byte aligned
+// groups of 4 (one vector load covers the group containing the scan position),
+// all PW vertices' loads and visited probes issued together.  A vertex with more
+// than LONG_IN in-edges left after PULL_STEPS steps is finished cooperatively by
+// the whole warp, 128 in-edges per step, so one long in-list cannot hold the
+// warp (and the round) hostage.
+constexpr int PULL_STEPS = 2;
+constexpr int LONG_IN = 24;
+
+__device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) {
+  return __ldg(reinterpret_cast<const uint4 *>(p));
+}
+
+__device__ __forceinline__ bool vbit(const uint32_t *vis, uint32_t u) {
+  return (vis[u >> 5] >> (u & 31)) & 1u;
+}
 
 template <bool STATS>
-__device__ void pull_chunk(Smem &s, const Params &p, long long chunk, const uint32_t *vis,
-                           uint32_t *vis_next, int r) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long word = chunk * NWARPS + warp;
-  if (word >= p.nwords) return;
-  const uint32_t vw = vis[word];
-  uint32_t nw = vw;
-  if (vw != 0xFFFFFFFFu) {
-    const uint32_t v = (uint32_t)(word * 32 + lane);
-    const bool need = !((vw >> lane) & 1u);
-    uint32_t par = INF;
-    long long loaded = 0;
-    if (need) {
-      long long j = __ldg(p.in_off + v);
-      const long long e = __ldg(p.in_off + v + 1);
-      for (; j < e && par == INF; j += 4) {
-        uint32_t u0 = __ldg(p.in_tgt + j);
-        uint32_t u1 = j + 1 < e ? __ldg(p.in_tgt + j + 1) : u0;
-        uint32_t u2 = j + 2 < e ? __ldg(p.in_tgt + j + 2) : u0;
-        uint32_t u3 = j + 3 < e ? __ldg(p.in_tgt + j + 3) : u0;
-        bool b0 = (vis[u0 >> 5] >> (u0 & 31)) & 1u;
-        bool b1 = (vis[u1 >> 5] >> (u1 & 31)) & 1u;
-        bool b2 = (vis[u2 >> 5] >> (u2 & 31)) & 1u;
-        bool b3 = (vis[u3 >> 5] >> (u3 & 31)) & 1u;
-        if (STATS) loaded += min(4ll, e - j);
-        par = b0 ? u0 : b1 ? u1 : b2 ? u2 : b3 ? u3 : INF;
+__device__ __forceinline__ void pull_words(const Params &p, long long w0, const uint32_t *vis,
+                                           uint32_t *vis_next, int r, WarpState &ws) {
+  const int lane = threadIdx.x & 31;
+  uint32_t vw[PW];
+#pragma unroll
+  for (int q = 0; q < PW; q++) vw[q] = (w0 + q < p.nwords) ? vis[w0 + q] : FULL;
+  unsigned todo = 0;
+#pragma unroll
+  for (int q = 0; q < PW; q++) todo |= ~vw[q];
+  if (!todo) {  // all visited (warp-uniform): carry the words over
+    if (lane < PW && w0 + lane < p.nwords) vis_next[w0 + lane] = FULL;
+    return;
+  }
+  long long js[PW];
+  int rem[PW], deg_in[PW];
+#pragma unroll
+  for (int q = 0; q < PW; q++) {
+    js[q] = 0;
+    rem[q] = 0;
+    if (!((vw[q] >> lane) & 1u)) {
+      const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
+      js[q] = __ldg(p.in_off + v);
+      rem[q] = (int)(__ldg(p.in_off + v + 1) - js[q]);
+      if (STATS) ws.swept += 1;
+    }
+    deg_in[q] = rem[q];
+  }
+  uint32_t par[PW];
+#pragma unroll
+  for (int q = 0; q < PW; q++) par[q] = INF;
+  for (int step = 0; step < PULL_STEPS; step++) {
+    uint4 g[PW];
+#pragma unroll
+    for (int q = 0; q < PW; q++)
+      if (rem[q] > 0) g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+    bool live = false;
+#pragma unroll
+    for (int q = 0; q < PW; q++) {
+      if (rem[q] <= 0) continue;
+      const int lo = (int)(js[q] & 3);
+      const int hi = min(4, lo + rem[q]);
+      const uint32_t e[4] = {g[q].x, g[q].y, g[q].z, g[q].w};
+      bool b[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) b[k] = (k >= lo && k < hi) ? vbit(vis, e[k]) : false;
+      uint32_t hit = INF;
+#pragma unroll
+      for (int k = 3; k >= 0; k--)
+        if (b[k]) hit = e[k];
+      if (STATS) ws.edges += hi - lo;
+      js[q] += hi - lo;
+      rem[q] -= hi - lo;
+      if (hit != INF) {
+        par[q] = hit;
+        rem[q] = 0;
+      }
+      live |= rem[q] > 0;
+    }
+    if (!__any_sync(FULL, live)) break;
+  }
+  // short remainders: per lane; long remainders: the whole warp, one vertex at a time
+#pragma unroll
+  for (int q = 0; q < PW; q++) {
+    for (;;) {
+      const bool go = rem[q] > 0 && rem[q] <= LONG_IN;
+      if (!__any_sync(FULL, go)) break;
+      if (go) {
+        const uint4 g = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+        const int lo = (int)(js[q] & 3);
+        const int hi = min(4, lo + rem[q]);
+        const uint32_t e[4] = {g.x, g.y, g.z, g.w};
+        uint32_t hit = INF;
+#pragma unroll
+        for (int k = 3; k >= 0; k--)
+          if (k >= lo && k < hi && vbit(vis, e[k])) hit = e[k];
+        if (STATS) ws.edges += hi - lo;
+        js[q] += hi - lo;
+        rem[q] -= hi - lo;
+        if (hit != INF) {
+          par[q] = hit;
+          rem[q] = 0;
+        }
       }
     }
-    const bool found = par != INF;
-    const unsigned nb = __ballot_sync(0xffffffffu, found);
-    nw |= nb;
-    if (found) {
-      p.dist[v] = (uint32_t)(r + 1);
-      if (p.parent) p.parent[v] = par;
-    }
-    stage_push(s, found, v, lane);
-    if (STATS && p.stats && r < p.stats_cap) {
-      long long sl = warp_sum64(loaded);
-      int sw = __popc(__ballot_sync(0xffffffffu, need));
-      if (lane == 0) {
-        atomicAdd((unsigned long long *)&p.stats[r].edges_examined, (unsigned long long)sl);
-        atomicAdd((unsigned long long *)&p.stats[r].vertices_swept, (unsigned long long)sw);
+    unsigned longs = __ballot_sync(FULL, rem[q] > LONG_IN);
+    while (longs) {
+      const int l = __ffs(longs) - 1;
+      longs &= longs - 1;
+      long long a = __shfl_sync(FULL, js[q], l);
+      const long long e_end = a + __shfl_sync(FULL, rem[q], l);
+      uint32_t found = INF;
+      while (a < e_end) {
+        // lane k reads the aligned group a0 + 4k .. a0 + 4k + 3
+        const long long a0 = a & ~3ll;
+        const long long gk = a0 + 4 * lane;
+        uint32_t hit = INF;
+        if (gk < e_end) {
+          const uint4 g = ldg_v4(p.in_tgt + gk);
+          const uint32_t e[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+          for (int k = 3; k >= 0; k--)
+            if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit = e[k];
+        }
+        const unsigned hb = __ballot_sync(FULL, hit != INF);
+        if (STATS && lane == 0) ws.edges += min(a0 + 128, e_end) - a;
+        if (hb) {
+          found = __shfl_sync(FULL, hit, __ffs(hb) - 1);
+          break;
+        }
+        a = a0 + 128;
+      }
+      if (lane == l) {
+        rem[q] = 0;
+        par[q] = found;
       }
     }
   }
-  if (lane == 0) vis_next[word] = nw;
+#pragma unroll
+  for (int q = 0; q < PW; q++) {
+    const bool found = par[q] != INF;
+    const unsigned nbm = __ballot_sync(FULL, found);
+    if (w0 + q < p.nwords && lane == 0) vis_next[w0 + q] = vw[q] | nbm;
+    if (found) {
+      const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
+      if (STATS) ws.acquired += 1;
+      p.dist[v] = (uint32_t)(r + 1);
+      if (p.parent) p.parent[v] = par[q];
+      const uint32_t dgo = p.symmetric ? (uint32_t)deg_in[q] : __ldg(p.odeg + v);
+      if (dgo > 0) {
+        ws.K += 1;
+        ws.D += dgo;
+      }
+    }
+  }
 }
 
 // ---- the persistent kernel ---------------------------------------------------
 
+template <int ALGO, bool STATS, int EMIT>
+__device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpState &ws, int lb,
+                                           long long f, long long E, int nb, int r, uint32_t *bits,
+                                           const uint32_t *prebits, long long gw, long long nw) {
+  const long long ntiles = (E + TE - 1) / TE;
+  for (long long t = gw; t < ntiles; t += nw)
+    push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, t, ntiles, f, E, nb, r, bits, prebits);
+}
+
+template <int ALGO, bool STATS, int EMIT>
+__device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid_group &grid,
+                                              WarpSmem &w, WarpState &ws, uint32_t *fr,
+                                              uint32_t *bits, const uint32_t *precheck, int nb,
+                                              int r, long long gw, long long nw) {
+  for (long long w0 = gw * PW; w0 < p.nwords; w0 += nw * PW)
+    forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, fr, bits, precheck, nb, r);
+  grid.sync();  // heavy list complete
+  if (threadIdx.x == 0) s.hcnt = ld_relaxed64(p.hcnt + (r & 1));
+  __syncthreads();
+  const unsigned long long hc = s.hcnt;
+  const long long hf = (long long)(hc >> p.ebits);
+  const long long hE = (long long)(hc & ((1ull << p.ebits) - 1));
+  if (hf > 0)
+    list_round<ALGO, STATS, EMIT>(p, w, ws, LIST_HEAVY, hf, hE, nb, r, bits,
+                                  (ALGO == ALGO_BFS) ? precheck : bits, gw, nw);
+}
+
 template <int ALGO, bool STATS>
-__global__ void __launch_bounds__(BLOCK) traverse_kernel(Params p) {
+#ifndef GBBS_MIN_CTAS
+#define GBBS_MIN_CTAS 4
+#endif
+__global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p) {
   __shared__ Smem s;
   cg::grid_group grid = cg::this_grid();
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long gtid = (long long)blockIdx.x * BLOCK + tid;
   const long long gstride = (long long)gridDim.x * BLOCK;
+  const long long gw = (long long)blockIdx.x * NWARPS + warp;
+  const long long nw = (long long)gridDim.x * NWARPS;
   const uint32_t src = p.src;
+  WarpSmem &wsm = s.w[warp];
+  for (int i = lane; i < TE; i += 32) wsm.head[i] = 0;
+  int tag = 0;
 
   // a1: per-run init
   for (long long i = gtid; i < p.n; i += gstride) {
@@ -436,35 +850,34 @@ __global__ void __launch_bounds__(BLOCK) traverse_kernel(Params p) {
   }
   for (long long w = gtid; w < p.nwords; w += gstride) {
     if (ALGO == ALGO_BFS) {
-      uint32_t x = 0;
-      long long lo = w * 32;
-      if (lo + 32 > p.n) x = 0xFFFFFFFFu << (uint32_t)(p.n - lo);  // padding = visited
+      uint32_t x = p.iso[w];  // isolated vertices + padding count as visited
       if ((long long)(src >> 5) == w) x |= 1u << (src & 31);
       p.bm[0][w] = x;
-    } else {
-      p.bm[0][w] = 0;
+    } else {  // round 0's frontier {src} as TS bits (bitmap-forward reads them)
+      p.bm[0][w] = ((long long)(src >> 5) == w) ? (1u << (src & 31)) : 0u;
       p.bm[1][w] = 0;
     }
   }
+  const long long a0 = p.off[src], d0 = p.off[src + 1] - a0;
+  for (long long t = gtid; t < (d0 + TE - 1) / TE; t += gstride) p.tab[0][t] = 0;
   if (blockIdx.x == 0 && tid == 0) {
-    long long a = p.off[src], d0 = p.off[src + 1] - a;
     p.cnt[1] = p.cnt[2] = p.cnt[3] = 0;
+    p.hcnt[0] = p.hcnt[1] = 0;
     if (d0 > 0) {
       p.fv[0][0] = src;
       p.fo[0][0] = 0;
-      p.fb[0][0] = a;
+      p.fb[0][0] = a0;
       p.cnt[0] = (1ull << p.ebits) | (unsigned long long)d0;
     } else {
       p.cnt[0] = 0;
     }
     *p.status = 0;
   }
-  if (tid == 0) { s.stage_n = 0; s.tag = 0; }
-  for (int i = tid; i < TE; i += BLOCK) s.head[i] = 0;
   grid.sync();
 
   const unsigned long long emask = (1ull << p.ebits) - 1;
-  int vc = 0;  // BFS: index of the current visited bitmap
+  int vc = 0;              // BFS: index of the current visited bitmap
+  bool list_valid = true;  // is this round's frontier materialised as a list?
   long long r = 0;
   for (;; r++) {
     if (tid == 0) s.cnt = ld_relaxed64(p.cnt + (r & 3));
@@ -479,44 +892,99 @@ __global__ void __launch_bounds__(BLOCK) traverse_kernel(Params p) {
       if (blockIdx.x == 0 && tid == 0) *p.status = 1;
       break;
     }
-    bool dense = false;
-    if (ALGO == ALGO_BFS)
-      dense = p.mode == 2 || (p.mode == 0 && f + E > p.dense_threshold);
+    // kind: 0 list push, 1 dense pull, 2 bitmap-forward.  BFS: dense pull iff
+    // |U| + sum deg(U) > m/T.  Bellman-Ford: list push unless GBBS_MODE_DENSE
+    // forces bitmap-forward rounds (reading A11: measured slower on rMAT).
+    const bool big = (ALGO == ALGO_BFS)
+                         ? (p.mode == 2 || (p.mode == 0 && f + E > p.dense_threshold))
+                         : p.mode == 2;
+    int kind;
+    if (ALGO == ALGO_BFS) kind = big ? 1 : (list_valid ? 0 : 2);
+    else kind = (big || !list_valid) ? 2 : 0;
     if (blockIdx.x == 0 && tid == 0) {
       p.cnt[(r + 2) & 3] = 0;
+      p.hcnt[(r + 1) & 1] = 0;
       if (STATS && p.stats && r < p.stats_cap) {
-        p.stats[r].dense = dense;
+        p.stats[r].dense = kind;
         p.stats[r].frontier = f;
         p.stats[r].frontier_edges = E;
       }
     }
-    const int cb = (int)(r & 1), nbuf = cb ^ 1;
-    if (dense) {
+    const int cb = (int)(r & 1), nb = cb ^ 1;
+    WarpState ws;
+    ws.tag = tag;
+    bool emit_count = false;
+    if (kind == 1) {  // dense pull (BFS)
       const uint32_t *vis = p.bm[vc];
       uint32_t *vis_next = p.bm[vc ^ 1];
-      const long long nchunks = (p.nwords + NWARPS - 1) / NWARPS;
-      for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-        pull_chunk<STATS>(s, p, ch, vis, vis_next, (int)r);
-        __syncthreads();
-        if (s.stage_n > CAP - BLOCK) flush<ALGO, STATS>(s, p, nbuf, (int)r, nullptr);
-      }
+      for (long long w0 = gw * PW; w0 < p.nwords; w0 += nw * PW)
+        pull_words<STATS>(p, w0, vis, vis_next, (int)r, ws);
       vc ^= 1;
-    } else {
-      uint32_t *bits = (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nbuf];
+      list_valid = false;
+      emit_count = true;
+    } else if (kind == 2) {  // bitmap-forward
+      if (ALGO == ALGO_BFS) {
+        forward_round<ALGO, STATS, EMIT_LIST>(s, p, grid, wsm, ws, nullptr, p.bm[vc ^ 1], p.bm[vc],
+                                              nb, (int)r, gw, nw);
+        vc ^= 1;
+        list_valid = true;
+      } else if (big) {
+        forward_round<ALGO, STATS, EMIT_COUNT>(s, p, grid, wsm, ws, p.bm[cb], p.bm[nb], nullptr,
+                                               nb, (int)r, gw, nw);
+        list_valid = false;
+        emit_count = true;
+      } else {
+        forward_round<ALGO, STATS, EMIT_LIST>(s, p, grid, wsm, ws, p.bm[cb], p.bm[nb], nullptr,
+                                              nb, (int)r, gw, nw);
+        list_valid = true;
+      }
+    } else {  // list push
+      uint32_t *bits = (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nb];
       if (ALGO == ALGO_BF) {
         // a11: release the current frontier's TS bits (buffer cb is idle this round)
         uint32_t *cur_bits = p.bm[cb];
         const uint32_t *F = p.fv[cb];
         for (long long i = gtid; i < f; i += gstride) cur_bits[__ldcg(F + i) >> 5] = 0;
       }
-      const long long ntiles = (E + TE - 1) / TE;
-      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        push_tile<ALGO, STATS>(s, p, t, f, E, cb, (int)r, bits);
-        if (s.stage_n > CAP - TE) flush<ALGO, STATS>(s, p, nbuf, (int)r, bits);
+      list_round<ALGO, STATS, EMIT_LIST>(p, wsm, ws, cb, f, E, nb, (int)r, bits, bits, gw, nw);
+      list_valid = true;
+    }
+    unsigned long long t_work = 0, t_flush = 0;
+    if (STATS) t_work = globaltimer_ns();
+    if (ws.scnt > 0) {
+      if (STATS && lane == 0) ws.acquired += ws.scnt;
+      warp_flush<ALGO>(p, wsm.stage, ws.scnt, nb, (int)r,
+                       (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nb]);
+    }
+    if (emit_count) {
+      const unsigned long long K = warp_sum64((long long)ws.K), D = warp_sum64((long long)ws.D);
+      if (lane == 0 && K) atomicAdd(p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
+    }
+    tag = ws.tag;
+    if (STATS) t_flush = globaltimer_ns();
+    if (STATS && p.stats && r < p.stats_cap) {
+      // one global atomic per CTA and counter
+      if (tid < 5) s.sacc[tid] = 0;
+      __syncthreads();
+      const unsigned long long e = warp_sum64((long long)ws.edges);
+      const unsigned long long sw = warp_sum64((long long)ws.swept);
+      const unsigned long long aq = warp_sum64((long long)ws.acquired);
+      if (lane == 0) {
+        atomicAdd(&s.sacc[0], e);
+        atomicAdd(&s.sacc[1], sw);
+        atomicAdd(&s.sacc[2], aq);
+        atomicMax(&s.sacc[3], t_work);
+        atomicMax(&s.sacc[4], t_flush);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        atomicAdd((unsigned long long *)&p.stats[r].edges_examined, s.sacc[0]);
+        atomicAdd((unsigned long long *)&p.stats[r].vertices_swept, s.sacc[1]);
+        atomicAdd((unsigned long long *)&p.stats[r].acquired, s.sacc[2]);
+        atomicMax((unsigned long long *)&p.stats[r].t_work_ns, s.sacc[3]);
+        atomicMax((unsigned long long *)&p.stats[r].t_flush_ns, s.sacc[4]);
       }
     }
-    __syncthreads();
-    flush<ALGO, STATS>(s, p, nbuf, (int)r, (ALGO == ALGO_BF) ? p.bm[nbuf] : nullptr);
     grid.sync();
   }
   if (blockIdx.x == 0 && tid == 0) *p.rounds_out = r;

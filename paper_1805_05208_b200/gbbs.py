@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgbbs.so")
+LIB_PATH = os.environ.get("GBBS_LIB") or os.path.join(_HERE, "libgbbs.so")
 
 GBBS_OK, GBBS_EINVAL, GBBS_ERANGE, GBBS_ENOMEM, GBBS_ECUDA, GBBS_EINTERNAL = 0, -1, -2, -3, -4, -5
 GBBS_INF = 0xFFFFFFFF
@@ -42,7 +42,8 @@ class gbbs_round_stat(ctypes.Structure):
     _fields_ = [("dense", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("frontier", ctypes.c_int64), ("frontier_edges", ctypes.c_int64),
                 ("acquired", ctypes.c_int64), ("edges_examined", ctypes.c_int64),
-                ("vertices_swept", ctypes.c_int64), ("t_start_ns", ctypes.c_int64)]
+                ("vertices_swept", ctypes.c_int64), ("t_start_ns", ctypes.c_int64),
+                ("t_work_ns", ctypes.c_int64), ("t_flush_ns", ctypes.c_int64)]
 
 
 class gbbs_stats(ctypes.Structure):
@@ -179,7 +180,9 @@ def round_records(stats):
         us = (raw[i + 1].t_start_ns - r.t_start_ns) / 1e3 if i + 1 < len(raw) else None
         out.append(dict(dense=r.dense, frontier=r.frontier, frontier_edges=r.frontier_edges,
                         acquired=r.acquired, edges_examined=r.edges_examined,
-                        vertices_swept=r.vertices_swept, us=us))
+                        vertices_swept=r.vertices_swept, us=us,
+                        work_us=(r.t_work_ns - r.t_start_ns) / 1e3,
+                        flush_us=(r.t_flush_ns - r.t_start_ns) / 1e3))
     return out
 
 

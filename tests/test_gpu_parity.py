@@ -193,6 +193,25 @@ def test_directed_rmat_threshold_sweep(G):
     g.close()
 
 
+@pytest.mark.parametrize("sym", [False, True])
+def test_long_in_lists_dense(G, sym):
+    """A vertex whose in-list is long and whose only frontier in-neighbour comes
+    last (and one with none at all) — exercises the warp-cooperative pull scan."""
+    n = 5000
+    edges = [(0, 1), (1, n - 1), (1, n - 2)]
+    edges += [(u, n - 1) for u in range(2, n - 3)]   # unreachable in-neighbours first
+    edges += [(u, n - 3) for u in range(2, 40)]      # never reached
+    edges += [(u, n - 2) for u in range(2, 30)]
+    off, tgt = graphgen.from_edge_list(n, edges, symmetric=sym)
+    g = G.Graph(off, tgt, symmetric=sym)
+    ref, _ = oracle.bfs(off, tgt, 0)
+    for mode in MODES:
+        d, p = run_bfs(G, g, 0, mode)
+        assert (d == ref).all(), mode
+        assert oracle.check_bfs(off, tgt, 0, d, p)[0]
+    g.close()
+
+
 def test_unit_weights_and_null_weights_equal_bfs(G):
     off, tgt = graphgen.rmat_graph(15, 1 << 19, 3, 0.57, 0.19, 0.19)
     g = G.Graph(off, tgt, symmetric=True)

@@ -68,12 +68,15 @@ def main():
                         print(f"   r{i:<4d} {'D' if r['dense'] else 'S'} U={r['frontier']:>10d} "
                               f"E={r['frontier_edges']:>11d} acq={r['acquired']:>9d} "
                               f"ex={r['edges_examined']:>11d} sw={r['vertices_swept']:>9d} "
-                              f"{(r['us'] or 0):9.1f}us")
+                              f"{(r['us'] or 0):9.1f}us  work<{r['work_us']:.1f} flush<{r['flush_us']:.1f}")
                 else:
                     us = np.array([r["us"] or 0 for r in recs])
                     fr = np.array([r["frontier"] for r in recs])
+                    wk = np.array([r["work_us"] for r in recs])
+                    fl = np.array([r["flush_us"] for r in recs])
                     print(f"   per-round us: median {np.median(us):.2f} p90 {np.percentile(us, 90):.2f} "
-                          f"max {us.max():.1f}; frontier median {np.median(fr):.0f} max {fr.max()}")
+                          f"max {us.max():.1f}; work-end median {np.median(wk):.2f} flush-end median "
+                          f"{np.median(fl):.2f}; frontier median {np.median(fr):.0f} max {fr.max()}")
                 if a.check:
                     import oracle
                     ho = off.cpu().numpy()
