@@ -19,7 +19,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import time
 
@@ -55,43 +54,57 @@ def dist_env():
 
 
 class Clocks:
-    """Sample nvidia-smi clocks/throttle reasons during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Sample SM clocks and clock-event (throttle) reasons with NVML every `period`
+    seconds in a background thread while the timed region runs (the recipe's
+    clocks line, B200_PROFILING.md).  Falls back to nvidia-smi if NVML fails."""
 
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, index, period=0.002):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = None
+        self._thr = None
 
     def start(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001
+            self.err = f"nvml unavailable: {e}"
+            return
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for nm, attr in self.NAMES:
+                        if bits & getattr(pynvml, attr, 0):
+                            self.reasons.add(nm)
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(self.period)
+
+        self._thr = threading.Thread(target=run, daemon=True)
+        self._thr.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1])); mx = float(f[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self._thr is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [getattr(self, "err", "no samples")]}
+        self._stop.set()
+        self._thr.join()
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "nvml"}
 
 
 def measured_peaks():
@@ -117,21 +130,27 @@ def copy_bandwidth(torch):
 
 
 def algorithmic_bytes(recs, n, m, algo):
-    """§8(d) per-round algorithmic bytes of offsets + targets + weights + frontier.
-
-    Push round: carried frontier entries read (v 4 + O 8 + base 8 B each), targets
-    4 B per edge (+4 B weight for BF), emitted entries: offsets 16 B read + 20 B
-    written.  Pull round: in-offsets 8 B per swept vertex + 8, 4 B per in-edge
-    loaded, visited bitmap n/8 read + n/8 written, plus emitted entries as above.
-    Returns (alg_bytes, state_bytes) — state (dist/parent) kept separate."""
+    """SURVEY §8(d) algorithmic bytes of offsets + targets + weights + frontier, per
+    traversal, from the per-round records:
+      list push   : frontier entries read 20 B (v 4 + O 8 + base 8), targets 4 B/edge
+                    (+ weights 4 B/edge for BF), each emitted vertex 16 B of offsets
+                    read + 20 B entry written;
+      dense pull  : in-offsets 8 B per swept vertex + 8, in-edges 4 B per edge loaded,
+                    visited bitmap n/8 read + n/8 written;
+      bitmap fwd  : frontier bitmap(s) swept (n/8, x2 for BFS), offsets 16 B per
+                    frontier vertex, targets (+weights) per edge, emitted entries.
+    Probes of the L2-resident bitmaps and dist/parent state are not counted (state
+    bytes are returned separately)."""
     alg = 0
-    for i, r in enumerate(recs):
-        acq = r["acquired"]
-        emit = 36 * acq  # offsets read + entry written
-        if r["dense"]:
-            alg += 8 * r["vertices_swept"] + 8 + 4 * r["edges_examined"] + 2 * ((n + 7) // 8) + emit
+    wb = (n + 7) // 8
+    per_edge = 8 if algo == "bf" else 4
+    for r in recs:
+        emit = 36 * r["acquired"]
+        if r["dense"] == 1:
+            alg += 8 * r["vertices_swept"] + 8 + 4 * r["edges_examined"] + 2 * wb
+        elif r["dense"] == 2:
+            alg += (2 if algo == "bfs" else 1) * wb + 16 * r["vertices_swept"] + per_edge * r["edges_examined"] + emit
         else:
-            per_edge = 8 if algo == "bf" else 4
             alg += 20 * r["frontier"] + per_edge * r["frontier_edges"] + emit
     state = 8 * n if algo == "bfs" else 4 * n
     return alg, state
@@ -140,6 +159,17 @@ def algorithmic_bytes(recs, n, m, algo):
 def reached_edges(torch, off, d):
     deg = off[1:] - off[:-1]
     return int(deg[d != -1].sum())
+
+
+def ncu_traffic(workload, algo):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of traverse_kernel from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload, {}).get(algo)
+    except (OSError, ValueError):
+        return None
 
 
 def run_ours(args, rank, world, local):
@@ -168,15 +198,16 @@ def run_ours(args, rank, world, local):
     opts = gbbs.make_opts(args.threshold, gbbs.GBBS_MODE_AUTO)
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def one(src, algo, d=dist, p=par, stats=None):
+    def one(src, algo, stats=None):
         if algo == "bfs":
-            g.bfs(src, d, p, stream=stream, opts=opts, stats=stats)
+            g.bfs(src, dist, par, stream=stream, opts=opts, stats=stats)
         else:
-            g.bellman_ford(src, d, stream=stream, stats=stats)
+            g.bellman_ford(src, dist, stream=stream, stats=stats)
 
-    # per-source traversed-edge counts (TEPS numerator, reading A20) and stats
+    algos = [args.algo] + (["bf"] if (want_w and args.algo == "bfs" and not args.profile) else [])
+    # per-source traversed edges (TEPS numerator, reading A20) and algorithmic bytes
     per_src = {}
-    for algo in (["bfs", "bf"] if want_w else ["bfs"]):
+    for algo in algos:
         for s in sources:
             st = gbbs.make_stats(1 << 16)
             one(s, algo, stats=st)
@@ -184,21 +215,20 @@ def run_ours(args, rank, world, local):
             alg, state = algorithmic_bytes(recs, n, m, algo)
             per_src[(algo, s)] = dict(m_reach=reached_edges(torch, off, dist), rounds=st.rounds,
                                       dense_rounds=st.dense_rounds, alg_bytes=alg, state_bytes=state,
-                                      relax=sum(r["frontier_edges"] for r in recs if not r["dense"]))
+                                      relax=sum(r["edges_examined"] for r in recs))
 
-    def timed(algo, steps, warmup, flush=True):
+    def timed(algo, steps, warmup):
         for _ in range(warmup):
             for s in sources:
                 one(s, algo)
         if world > 1:
             dist_mod.barrier()
         torch.cuda.synchronize()
+        clocks = Clocks(local)
+        clocks.start()
         evs = []
-        clocks = Clocks(local); clocks.start()
-        kms = []
         for _ in range(steps):
-            if flush:
-                flush_buf.fill_(1)
+            flush_buf.fill_(1)  # L2 flush between timed steps (outside the events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for s in sources:
@@ -209,51 +239,54 @@ def run_ours(args, rank, world, local):
         ck = clocks.stop()
         if world > 1:
             dist_mod.barrier()
-        ms = [a.elapsed_time(b) for a, b in evs]
-        # kernel-only durations of the persistent traversal kernel (events inside libgbbs)
+        ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+        tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist_mod.all_reduce(tmax, op=dist_mod.ReduceOp.MAX)
+        # kernel-only time of the persistent traversal kernel: CUDA events that libgbbs
+        # records on `stream` around its cooperative launch (gbbs_stats.kernel_ms)
+        kms = []
         for s in sources:
-            if flush:
-                flush_buf.fill_(1)
+            flush_buf.fill_(1)
             st = gbbs.make_stats(0)
             one(s, algo, stats=st)
             kms.append(st.kernel_ms)
-        return ms, ck, kms
+        return float(tmax.item()), ck, float(np.sum(kms))
 
-    ms, clocks, kms = timed(args.algo, args.steps, args.warmup)
-    step_ms = float(np.mean(ms))
-    tmax = torch.tensor([step_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist_mod.all_reduce(tmax, op=dist_mod.ReduceOp.MAX)
-    step_ms_max = float(tmax.item())
+    res = {algo: timed(algo, args.steps if algo == args.algo else max(2, args.steps // 2),
+                       args.warmup if algo == args.algo else 1) for algo in algos}
+    step_ms, clocks, kernel_ms = res[args.algo]
     edges_step = sum(per_src[(args.algo, s)]["m_reach"] for s in sources)
-    value = world * edges_step / (step_ms_max * 1e-3) / 1e9
+    value = world * edges_step / (step_ms * 1e-3) / 1e9
 
     out = None
     if rank == 0:
         peak, peak_src = measured_peaks()
         copy_gbs = copy_bandwidth(torch)
         alg_bytes = sum(per_src[(args.algo, s)]["alg_bytes"] for s in sources)
-        kernel_ms = float(np.sum(kms))
         achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
-        # e2e: public API with pinned host output buffers (library copies D2H inside)
+        traffic = ncu_traffic(cfg.name, args.algo)
+        # e2e: the public API with pinned host output buffers; libgbbs copies dist/parent
+        # device->host inside the call (sources travel as kernel arguments)
         hd = torch.empty(n, dtype=torch.int32, pin_memory=True)
         hp = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        hdn, hpn = hd.numpy(), hp.numpy()
         torch.cuda.synchronize()
         e2e = []
-        for _ in range(max(1, min(args.steps, 5))):
+        for _ in range(max(2, min(args.steps, 5))):
             t = time.perf_counter()
             for s in sources:
                 if args.algo == "bfs":
-                    gbbs.gbbs_bfs(g.handle, s, hd.numpy(), hp.numpy(), stream=stream)
+                    gbbs.gbbs_bfs(g.handle, s, hdn, hpn, stream=stream)
                 else:
-                    gbbs.gbbs_bellman_ford(g.handle, s, hd.numpy(), stream=stream)
+                    gbbs.gbbs_bellman_ford(g.handle, s, hdn, stream=stream)
             e2e.append(time.perf_counter() - t)
         e2e_s = float(np.median(e2e))
         d2h = len(sources) * n * (8 if args.algo == "bfs" else 4)
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "GTEPS",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(step_ms_max, 4), "higher_is_better": True,
+            "ms_per_step": round(step_ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded counter-based rMAT/torus generators, DESIGN.md §Input recipe)",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "algo": args.algo,
@@ -262,31 +295,33 @@ def run_ours(args, rank, world, local):
                        "l2": "flushed (256 MB write) before every timed step; graph > L2",
                        "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic,
                          "peak_source": peak_src, "copy_gbs_same_run": round(copy_gbs, 1),
-                         "kernel": "gbbs_dev::traverse_kernel (persistent, one launch per traversal)",
-                         "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": round(kernel_ms, 4)},
+                         "frac_of_copy_same_run": round(achieved / copy_gbs, 4),
+                         "kernel": "gbbs_dev::traverse_kernel (persistent; one launch per traversal)",
+                         "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": round(kernel_ms, 4),
+                         "kernel_gteps": round(edges_step / (kernel_ms * 1e-3) / 1e9, 3)},
             "e2e": {"value": round(edges_step / e2e_s / 1e9, 3), "unit": "GTEPS",
                     "h2d_bytes_per_step": 4 * len(sources), "d2h_bytes_per_step": d2h,
-                    "note": "gbbs_bfs with pinned host dist/parent; library copies D2H; "
-                            "sources travel as kernel arguments"},
+                    "note": "gbbs_bfs with pinned host dist/parent (library copies D2H); "
+                            "h2d = the source ids, passed as kernel arguments"},
             "gpu_launches": args.steps * len(sources),
             "clocks": clocks,
-            "per_source": [{"src": s, **{k: v for k, v in per_src[(args.algo, s)].items()}}
-                           for s in sources],
+            "per_source": [{"src": s, **per_src[(args.algo, s)]} for s in sources],
             "setup_s": round(setup_s, 2),
         }
-        if want_w and args.algo == "bfs" and not args.profile:
-            bms, bclk, bkms = timed("bf", max(1, args.steps // 2), 1)
+        if "bf" in algos and args.algo == "bfs":
+            bt, bclk, bkms = res["bf"]
             be = sum(per_src[("bf", s)]["m_reach"] for s in sources)
             brel = sum(per_src[("bf", s)]["relax"] for s in sources)
-            bt = float(np.mean(bms))
             balg = sum(per_src[("bf", s)]["alg_bytes"] for s in sources)
             out["bellman_ford"] = {
                 "value": round(be / (bt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective, reading A20)",
-                "relaxations_per_s": round(brel / (bt * 1e-3) / 1e9, 3), "ms_per_step": round(bt, 4),
+                "relaxations_per_s_G": round(brel / (bt * 1e-3) / 1e9, 3), "ms_per_step": round(bt, 4),
                 "weights": f"[1,{cfg.W}] pair-hash (readings A5, A6)",
-                "roofline_frac": round(balg / (float(np.sum(bkms)) * 1e-3) / 1e9 / peak, 4),
+                "roofline_frac": round(balg / (bkms * 1e-3) / 1e9 / peak, 4),
+                "kernel_ms_per_step": round(bkms, 4), "clocks": bclk,
                 "rounds": [per_src[("bf", s)]["rounds"] for s in sources]}
         if not args.profile:
             out["cpu_baseline"] = cpu_baseline(args, G["offsets"], G["targets"], sources, cfg)

@@ -65,7 +65,6 @@ struct gbbs_graph {
   uint32_t *fv[3] = {nullptr, nullptr, nullptr};  // round lists 0/1, heavy list 2
   long long *fo[3] = {nullptr, nullptr, nullptr};
   long long *fb[3] = {nullptr, nullptr, nullptr};
-  uint32_t *tab[3] = {nullptr, nullptr, nullptr};
   uint32_t *iso = nullptr;
   unsigned long long *part = nullptr;
   unsigned long long *cnt = nullptr;  // [4] + ctrl
@@ -93,7 +92,6 @@ static void free_graph(gbbs_graph *g) {
     cudaFree(g->fv[i]);
     cudaFree(g->fo[i]);
     cudaFree(g->fb[i]);
-    cudaFree(g->tab[i]);
   }
   cudaFree(g->cnt);
   cudaFree(g->iso);
@@ -336,7 +334,6 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
     CU(cudaMalloc(&g->fv[i], (size_t)n * 4));
     CU(cudaMalloc(&g->fo[i], (size_t)n * 8));
     CU(cudaMalloc(&g->fb[i], (size_t)n * 8));
-    CU(cudaMalloc(&g->tab[i], (size_t)(m / TE + 2) * 4));
   }
   if (!(flags & GBBS_SYMMETRIC)) {
     CU(cudaMalloc(&g->odeg, (size_t)n * 4));
@@ -499,7 +496,6 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
     p.fv[i] = g->fv[i];
     p.fo[i] = g->fo[i];
     p.fb[i] = g->fb[i];
-    p.tab[i] = g->tab[i];
   }
   p.cnt = g->cnt;
   p.hcnt = g->cnt + 8;
@@ -517,6 +513,12 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   p.mode = o.mode;
   p.src = src;
 
+#ifdef GBBS_DBG_PHASE
+  static unsigned long long *dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, 64 * 4 * 8);
+  cudaMemsetAsync(dbg, 0, 64 * 4 * 8, st);
+  p.dbg = dbg;
+#endif
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (want_stats) {
     if (!g->ev[0]) {
@@ -567,6 +569,15 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
       }
     }
   }
+#ifdef GBBS_DBG_PHASE
+  {
+    unsigned long long h[256];
+    cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 12 && i < ctrl.rounds; i++)
+      fprintf(stderr, "dbg r%d flush: pass1 %.1fus atomic %.1fus pass2 %.1fus maxcnt %llu\n", i,
+              h[4 * i] / 1e3, h[4 * i + 1] / 1e3, h[4 * i + 2] / 1e3, h[4 * i + 3]);
+  }
+#endif
   if (ctrl.status != 0)
     return fail(GBBS_EINTERNAL, "round cap (%lld rounds) exceeded", (long long)p.max_rounds);
   return GBBS_OK;

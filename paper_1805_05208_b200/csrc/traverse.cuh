@@ -13,9 +13,8 @@
 //    base = offset(v) - O, both produced when the entry was appended.  The
 //    round's d_U edges are cut into fixed tiles of TE edges, one warp per tile
 //    (edgeMapBlocked's fixed-size blocks: a
-//    high-degree vertex spans many tiles).  Instead of a binary search of O
-//     a tile reads its first owner from a tile->owner table
-//    written by the producer of the list.
+//    high-degree vertex spans many tiles); a tile finds its owners with a
+//    warp-wide 32-ary search of O (PAPER.md:1082's binary search).
 //  * dense pull (a8, BFS).  Each unvisited vertex scans its in-edges in order
 //    and stops at the first visited one (the early-exit dense method,
 //    PAPER.md:1870-1874).  Every visited in-neighbour of an unvisited vertex
@@ -91,7 +90,6 @@ struct Params {
   uint32_t *fv[3];           // lists 0/1 (rounds) and 2 (heavy): vertex
   long long *fo[3];          //   exclusive edge prefix O
   long long *fb[3];          //   base = offset(v) - O
-  uint32_t *tab[3];          //   tile -> first owner entry
   unsigned long long *cnt;   // packed (count << ebits | edges) ring [4]
   unsigned long long *hcnt;  // heavy-list packed counters [2]
   int *status;               // 0 ok, 1 = round cap hit
@@ -105,6 +103,9 @@ struct Params {
   int mode;                  // 0 auto, 1 sparse, 2 dense
   int symmetric;
   uint32_t src;
+#ifdef GBBS_DBG_PHASE
+  unsigned long long *dbg;   // [64][4] per-round max phase durations (ns)
+#endif
 };
 
 struct WarpSmem {             // one per warp; nothing here is shared across warps
@@ -143,6 +144,42 @@ __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long l
   return v;
 }
 
+// Streaming accesses to graph arrays and outputs carry an L2 evict-first hint so
+// that the multi-GB streams do not evict what must stay resident in the 126 MB
+// L2: the visited/frontier bitmaps, the frontier lists, the counters and the
+// kernel's own instructions (a cold instruction fetch from HBM costs ~1 us per
+// line, which showed up as 10-60 us stalls on rarely run paths).
+__device__ __forceinline__ unsigned long long ef_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t *a) {
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(ef_policy()));
+  return v;
+}
+
+__device__ __forceinline__ long long ld_stream64(const long long *a) {
+  long long v;
+  asm("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(ef_policy()));
+  return v;
+}
+
+__device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *a) {
+  uint4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(a), "l"(ef_policy()));
+  return v;
+}
+
+__device__ __forceinline__ void st_stream(uint32_t *a, uint32_t v) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(ef_policy())
+               : "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -177,13 +214,23 @@ __device__ __forceinline__ long long warp_excl_sum64(long long x, int lane) {
   return inc - x;
 }
 
-// Record, for every TE-edge tile whose first edge falls in [o, o+deg), that
-// entry `pos` owns it (the tile's starting owner for the next round).
-__device__ __forceinline__ void mark_tiles(uint32_t *tab, unsigned long long pos, long long o,
-                                           long long deg) {
-  long long t = (o + TE - 1) / TE;
-  const long long tl = (o + deg - 1) / TE;
-  for (; t <= tl; t++) tab[t] = (uint32_t)pos;
+// Largest i in [lo, hi) with O[i] <= key, given O[lo] <= key and O strictly
+// increasing: a warp-cooperative 32-ary search (log32(hi-lo) dependent L2 loads),
+// the binary search of edgeMapBlocked widened to a warp.
+__device__ __forceinline__ long long warp_upper(const long long *O, long long lo, long long hi,
+                                                long long key) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const long long step = (hi - lo + 31) >> 5;
+    const long long idx = lo + (long long)lane * step;
+    const bool ok = idx < hi && __ldcg(O + idx) <= key;
+    const unsigned bb = __ballot_sync(FULL, ok);
+    lo += (long long)(31 - __clz(bb)) * step;
+    hi = min(hi, lo + step);
+  }
+  const long long idx = lo + lane;
+  const bool ok = idx < hi && __ldcg(O + idx) <= key;
+  return lo + (31 - __clz(__ballot_sync(FULL, ok)));
 }
 
 // Append the lanes' (v, a = offset(v), deg > 0) to list `nb` at positions and
@@ -205,8 +252,9 @@ __device__ __forceinline__ void warp_append(const Params &p, int nb, unsigned lo
     p.fv[nb][pos] = v;
     p.fo[nb][pos] = o;
     p.fb[nb][pos] = a - o;
-    mark_tiles(p.tab[nb], pos, o, deg);
   }
+  const unsigned long long pos = (old >> p.ebits) + __popc(bal & lanemask_lt());
+  const long long o = (long long)(old & ((1ull << p.ebits) - 1)) + dex;
 }
 
 // Write `cnt` staged vertices of this warp into the next frontier list (a7).
@@ -216,9 +264,13 @@ __device__ __forceinline__ void warp_append(const Params &p, int nb, unsigned lo
 // entries per lane at a time.  Warp-uniform call.
 template <int ALGO>
 __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, int cnt, int nb,
-                                           int r, uint32_t *bits_next) {
+                                           int r, uint32_t *bits_next,
+                                           unsigned long long *tmark = nullptr) {
   constexpr int FL = 4;
   const int lane = threadIdx.x & 31;
+#ifdef GBBS_DBG_PHASE
+  const unsigned long long tA = globaltimer_ns();
+#endif
   __syncwarp();
   long long Kl = 0, Dl = 0;
   for (int b0 = 0; b0 < cnt; b0 += 32 * FL) {
@@ -240,15 +292,21 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
     }
   }
   const unsigned long long K = warp_sum64(Kl), D = warp_sum64(Dl);
+#ifdef GBBS_DBG_PHASE
+  const unsigned long long tB = globaltimer_ns();
+#endif
   unsigned long long old = 0;
   if (lane == 0 && K) old = atomicAdd(p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
   old = __shfl_sync(FULL, old, 0);
+#ifdef GBBS_DBG_PHASE
+  const unsigned long long tC = globaltimer_ns();
+  if (tmark) *tmark = tC;
+#endif
   unsigned long long k = old >> p.ebits;
   unsigned long long d = old & ((1ull << p.ebits) - 1);
   uint32_t *fv = p.fv[nb];
   long long *fo = p.fo[nb];
   long long *fb = p.fb[nb];
-  uint32_t *tab = p.tab[nb];
   for (int b0 = 0; b0 < cnt; b0 += 32 * FL) {
     uint32_t vv[FL];
     long long lo[FL], hi[FL];
@@ -270,13 +328,12 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
       const bool keep = deg > 0;
       const unsigned bal = __ballot_sync(FULL, keep);
       const long long dex = warp_excl_sum64(deg, lane);
+      const unsigned long long pos = k + __popc(bal & lanemask_lt());
+      const long long o = (long long)d + dex;
       if (keep) {
-        const unsigned long long pos = k + __popc(bal & lanemask_lt());
-        const long long o = (long long)d + dex;
         fv[pos] = vv[u];
         fo[pos] = o;
         fb[pos] = lo[u] - o;
-        mark_tiles(tab, pos, o, deg);
       } else if (ALGO == ALGO_BF && i < cnt) {
         // out-degree-0 vertex: it never enters a frontier; release its TS bit.
         atomicAnd(bits_next + (vv[u] >> 5), ~(1u << (vv[u] & 31)));
@@ -286,6 +343,15 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
     }
   }
   __syncwarp();
+#ifdef GBBS_DBG_PHASE
+  const unsigned long long tD = globaltimer_ns();
+  if (lane == 0 && r < 64 && p.dbg) {
+    atomicMax(p.dbg + 4 * r + 0, tB - tA);
+    atomicMax(p.dbg + 4 * r + 1, tC - tB);
+    atomicMax(p.dbg + 4 * r + 2, tD - tC);
+    atomicMax(p.dbg + 4 * r + 3, (unsigned long long)cnt);
+  }
+#endif
 }
 
 // ---- F: apply one batch of NCH 32-edge chunks -------------------------------------
@@ -315,8 +381,8 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       if (win[j]) {
-        p.dist[vv[j]] = (uint32_t)(r + 1);
-        if (p.parent) p.parent[vv[j]] = uu[j];
+        st_stream(p.dist + vv[j], (uint32_t)(r + 1));
+        if (p.parent) st_stream(p.parent + vv[j], uu[j]);
       }
     }
   } else {
@@ -389,8 +455,8 @@ __device__ __forceinline__ void push_tile(const Params &p, WarpSmem &w, WarpStat
   const long long *O = p.fo[lb];
   const long long *B = p.fb[lb];
   const uint32_t *F = p.fv[lb];
-  const long long i0 = __ldcg(p.tab[lb] + t);
-  const long long il = (t + 1 < ntiles) ? (long long)__ldcg(p.tab[lb] + t + 1) : f - 1;
+  const long long i0 = warp_upper(O, 0, f, ts);
+  const long long il = warp_upper(O, i0, min(f, i0 + TE + 1), te - 1);
   const int nown = (int)(il - i0 + 1);
   if (STATS && lane == 0) ws.edges += (unsigned long long)(te - ts);
 
@@ -425,8 +491,8 @@ __device__ __forceinline__ void push_tile(const Params &p, WarpSmem &w, WarpStat
           const long long bb = __shfl_sync(FULL, Bk, own);
           uu[j] = __shfl_sync(FULL, Xk, own);
           if (act[j]) {
-            vv[j] = __ldcs(p.tgt + bb + e);
-            if (ALGO == ALGO_BF) ww[j] = p.wgt ? __ldcs(p.wgt + bb + e) : 1u;
+            vv[j] = ld_stream(p.tgt + bb + e);
+            if (ALGO == ALGO_BF) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
           }
         }
       }
@@ -508,8 +574,8 @@ __device__ __forceinline__ void push_tile(const Params &p, WarpSmem &w, WarpStat
           const int kk = w.head[e - ts] & KMASK;
           const long long bb = w.base[kk];
           uu[j] = w.own[kk];
-          vv[j] = __ldcs(p.tgt + bb + e);
-          if (ALGO == ALGO_BF) ww[j] = p.wgt ? __ldcs(p.wgt + bb + e) : 1u;
+          vv[j] = ld_stream(p.tgt + bb + e);
+          if (ALGO == ALGO_BF) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
         }
       }
       apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
@@ -598,8 +664,8 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &w, Warp
         for (int j = 0; j < NCH; j++) {
           const int e = cs + 32 * j + lane;
           act[j] = e < ld;
-          vv[j] = act[j] ? __ldcs(p.tgt + la + e) : 0;
-          ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? __ldcs(p.wgt + la + e) : 1u) : 0;
+          vv[j] = act[j] ? ld_stream(p.tgt + la + e) : 0;
+          ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? ld_stream(p.wgt + la + e) : 1u) : 0;
           uu[j] = lx;
         }
         apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
@@ -634,8 +700,8 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &w, Warp
           break;
         }
       }
-      vv[j] = act[j] ? __ldg(p.tgt + base + idx) : 0;
-      ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? __ldg(p.wgt + base + idx) : 1u) : 0;
+      vv[j] = act[j] ? ld_stream(p.tgt + base + idx) : 0;
+      ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? ld_stream(p.wgt + base + idx) : 1u) : 0;
       uu[j] = xo;
     }
     apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
@@ -652,9 +718,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &w, Warp
 constexpr int PULL_STEPS = 2;
 constexpr int LONG_IN = 24;
 
-__device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) {
-  return __ldg(reinterpret_cast<const uint4 *>(p));
-}
+__device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4(p); }
 
 __device__ __forceinline__ bool vbit(const uint32_t *vis, uint32_t u) {
   return (vis[u >> 5] >> (u & 31)) & 1u;
@@ -682,8 +746,8 @@ __device__ __forceinline__ void pull_words(const Params &p, long long w0, const 
     rem[q] = 0;
     if (!((vw[q] >> lane) & 1u)) {
       const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
-      js[q] = __ldg(p.in_off + v);
-      rem[q] = (int)(__ldg(p.in_off + v + 1) - js[q]);
+      js[q] = ld_stream64(p.in_off + v);
+      rem[q] = (int)(ld_stream64(p.in_off + v + 1) - js[q]);
       if (STATS) ws.swept += 1;
     }
     deg_in[q] = rem[q];
@@ -786,8 +850,8 @@ __device__ __forceinline__ void pull_words(const Params &p, long long w0, const 
     if (found) {
       const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
       if (STATS) ws.acquired += 1;
-      p.dist[v] = (uint32_t)(r + 1);
-      if (p.parent) p.parent[v] = par[q];
+      st_stream(p.dist + v, (uint32_t)(r + 1));
+      if (p.parent) st_stream(p.parent + v, par[q]);
       const uint32_t dgo = p.symmetric ? (uint32_t)deg_in[q] : __ldg(p.odeg + v);
       if (dgo > 0) {
         ws.K += 1;
@@ -845,8 +909,8 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
 
   // a1: per-run init
   for (long long i = gtid; i < p.n; i += gstride) {
-    p.dist[i] = (i == src) ? 0u : INF;
-    if (ALGO == ALGO_BFS && p.parent) p.parent[i] = (i == src) ? src : INF;
+    st_stream(p.dist + i, (i == src) ? 0u : INF);
+    if (ALGO == ALGO_BFS && p.parent) st_stream(p.parent + i, (i == src) ? src : INF);
   }
   for (long long w = gtid; w < p.nwords; w += gstride) {
     if (ALGO == ALGO_BFS) {
@@ -859,7 +923,6 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     }
   }
   const long long a0 = p.off[src], d0 = p.off[src + 1] - a0;
-  for (long long t = gtid; t < (d0 + TE - 1) / TE; t += gstride) p.tab[0][t] = 0;
   if (blockIdx.x == 0 && tid == 0) {
     p.cnt[1] = p.cnt[2] = p.cnt[3] = 0;
     p.hcnt[0] = p.hcnt[1] = 0;
@@ -954,7 +1017,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     if (ws.scnt > 0) {
       if (STATS && lane == 0) ws.acquired += ws.scnt;
       warp_flush<ALGO>(p, wsm.stage, ws.scnt, nb, (int)r,
-                       (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nb]);
+                       (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nb], &t_work);
     }
     if (emit_count) {
       const unsigned long long K = warp_sum64((long long)ws.K), D = warp_sum64((long long)ws.D);
