@@ -172,6 +172,21 @@ def ncu_traffic(workload, algo):
         return None
 
 
+def replica_max(x, world, dist_mod=None, device="cpu"):
+    """Max over ranks of a per-rank time (replicas: no data-path collective; this
+    is the only reduction).  world == 1: identity."""
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_value(edges_per_rank_step, world, step_ms_max):
+    """Whole-job GTEPS: every rank traverses the same batch (weak scaling)."""
+    return world * edges_per_rank_step / (step_ms_max * 1e-3) / 1e9
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist_mod
@@ -240,9 +255,7 @@ def run_ours(args, rank, world, local):
         if world > 1:
             dist_mod.barrier()
         ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
-        tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist_mod.all_reduce(tmax, op=dist_mod.ReduceOp.MAX)
+        tmax = replica_max(ms, world, dist_mod, dev)
         # kernel-only time of the persistent traversal kernel: CUDA events that libgbbs
         # records on `stream` around its cooperative launch (gbbs_stats.kernel_ms)
         kms = []
@@ -251,13 +264,13 @@ def run_ours(args, rank, world, local):
             st = gbbs.make_stats(0)
             one(s, algo, stats=st)
             kms.append(st.kernel_ms)
-        return float(tmax.item()), ck, float(np.sum(kms))
+        return tmax, ck, float(np.sum(kms))
 
     res = {algo: timed(algo, args.steps if algo == args.algo else max(2, args.steps // 2),
                        args.warmup if algo == args.algo else 1) for algo in algos}
     step_ms, clocks, kernel_ms = res[args.algo]
     edges_step = sum(per_src[(args.algo, s)]["m_reach"] for s in sources)
-    value = world * edges_step / (step_ms * 1e-3) / 1e9
+    value = replica_value(edges_step, world, step_ms)
 
     out = None
     if rank == 0:

@@ -142,10 +142,14 @@ int gbbs_bellman_ford(const gbbs_graph *g, uint32_t src, uint32_t *dist,
 
 /* ---- extended calls (bench / tests) ------------------------------------ */
 
-/* Direction choice per round (threshold rule reading A10). */
-#define GBBS_MODE_AUTO 0   /* dense iff |U| + sum_{u in U} deg(u) > m / T */
+/* Representation choice per round (threshold rule reading A10).
+ * BFS AUTO: a round is dense (pull over in-edges, early exit) iff
+ *   |U| + sum_{u in U} outdeg(u) > m / T, else sparse (push).
+ * Bellman-Ford AUTO: always list push; DENSE forces the bitmap-forward push
+ *   (the frontier as a bitmap, reading A11), kept as the measured alternative. */
+#define GBBS_MODE_AUTO 0
 #define GBBS_MODE_SPARSE 1 /* always push                                 */
-#define GBBS_MODE_DENSE 2  /* always pull (BFS only; BF always pushes)    */
+#define GBBS_MODE_DENSE 2  /* BFS: always pull; BF: bitmap-forward push   */
 
 typedef struct {
   uint32_t threshold_den; /* T; 0 selects the default 20                  */
@@ -155,13 +159,15 @@ typedef struct {
 
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */
 typedef struct {
-  int32_t dense;          /* 1 = pull round, 0 = push round               */
+  int32_t dense;          /* round kind: 0 = list push, 1 = dense pull,
+                             2 = bitmap-forward push                      */
   int32_t reserved;
   int64_t frontier;       /* |U|: frontier vertices with out-degree > 0   */
   int64_t frontier_edges; /* sum of out-degrees of U                       */
   int64_t acquired;       /* vertices won this round (incl. out-degree 0) */
   int64_t edges_examined; /* push: edges of U; pull: in-edges loaded      */
-  int64_t vertices_swept; /* pull: unvisited vertices examined            */
+  int64_t vertices_swept; /* pull: unvisited vertices examined; bitmap-
+                             forward: frontier vertices swept            */
   int64_t t_start_ns;     /* device %globaltimer when the round started;
                              the record after the last round holds the
                              end time when rounds_cap allows             */
@@ -171,7 +177,7 @@ typedef struct {
 
 typedef struct {
   int64_t rounds;          /* rounds executed (edgeMap calls)             */
-  int64_t dense_rounds;
+  int64_t dense_rounds;    /* rounds of kind 1 (dense pull)               */
   int64_t edges_examined;  /* total over rounds                           */
   int64_t reached;         /* vertices with finite dist                  */
   double kernel_ms;        /* device time of the traversal kernel, from
