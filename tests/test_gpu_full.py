@@ -1,0 +1,120 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (persistent kernel, AUTO direction, T = 20 unless swept).
+
+* c1, c2: distances bit-exact against the oracle for every source; parents certified.
+* c3: distances equal the torus closed form; per-round frontier sizes equal the
+  closed-form level counts (385 rounds); Bellman-Ford exact against Dijkstra.
+* c4, c5: the O(n+m) certificates (which imply exact distances and valid parents)
+  for the configs' sources; c5 distances identical across T in {10, 20, 40}.
+"""
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from pins import torus_dist, torus_level_counts
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1805_05208_b200 import gbbs
+    return gbbs
+
+
+def build(name, weights):
+    from graphgen import device
+    D = device.build_config(name, weights=weights)
+    host = dict(off=D["offsets"].cpu().numpy(), tgt=D["targets"].cpu().numpy().view(np.uint32),
+                w=None if D["weights"] is None else D["weights"].cpu().numpy().view(np.uint32))
+    return D, host
+
+
+def gpu_bfs(G, g, n, s, T=20):
+    d = torch.empty(n, dtype=torch.int32, device="cuda")
+    p = torch.empty_like(d)
+    st = G.make_stats(4096)
+    g.bfs(s, d, p, opts=G.make_opts(T, G.GBBS_MODE_AUTO), stats=st)
+    return d.cpu().numpy().view(np.uint32), p.cpu().numpy().view(np.uint32), st
+
+
+def gpu_bf(G, g, n, s):
+    d = torch.empty(n, dtype=torch.int32, device="cuda")
+    g.bellman_ford(s, d)
+    return d.cpu().numpy().view(np.uint32)
+
+
+def test_c1_full(G):
+    D, H = build("c1", True)
+    g = G.Graph(D["offsets"], D["targets"], D["weights"], symmetric=True)
+    for s in D["sources"]:
+        d, p, _ = gpu_bfs(G, g, D["n"], s)
+        assert (d == oracle.bfs(H["off"], H["tgt"], s)[0]).all()
+        assert oracle.check_bfs(H["off"], H["tgt"], s, d, p)[0]
+        assert (gpu_bf(G, g, D["n"], s) == oracle.dijkstra(H["off"], H["tgt"], H["w"], s)[0]).all()
+    g.close()
+
+
+def test_c2_full(G):
+    D, H = build("c2", True)   # weights [1,22] for the bench's Bellman-Ford leg
+    g = G.Graph(D["offsets"], D["targets"], D["weights"], symmetric=True)
+    n = D["n"]
+    for i, s in enumerate(D["sources"]):
+        ref, _ = oracle.bfs(H["off"], H["tgt"], s)
+        d, p, st = gpu_bfs(G, g, n, s)
+        assert (d == ref).all(), s
+        assert oracle.check_bfs(H["off"], H["tgt"], s, d, p)[0]
+        assert st.dense_rounds >= 1        # the direction optimisation engaged
+        if i == 0:
+            for T in (10, 40):
+                assert (gpu_bfs(G, g, n, s, T)[0] == ref).all()
+            assert (gpu_bf(G, g, n, s) == oracle.dijkstra(H["off"], H["tgt"], H["w"], s)[0]).all()
+    g.close()
+
+
+def test_c3_full(G):
+    D, H = build("c3", True)
+    g = G.Graph(D["offsets"], D["targets"], D["weights"], symmetric=True)
+    n, L = D["n"], graphgen.CONFIGS["c3"].L
+    d, p, st = gpu_bfs(G, g, n, 0)
+    assert (d == torus_dist(L, 0)).all()
+    assert oracle.check_bfs(H["off"], H["tgt"], 0, d, p)[0]
+    lv = torus_level_counts(L)
+    assert st.rounds == len(lv) == 385
+    assert [r["frontier"] for r in G.round_records(st)] == list(lv)
+    bf = gpu_bf(G, g, n, 0)
+    assert (bf == oracle.dijkstra(H["off"], H["tgt"], H["w"], 0)[0]).all()
+    g.close()
+
+
+def test_c4_full(G):
+    D, H = build("c4", True)
+    g = G.Graph(D["offsets"], D["targets"], D["weights"], symmetric=True)
+    n = D["n"]
+    for s in D["sources"][:2]:
+        bf = gpu_bf(G, g, n, s)
+        assert oracle.check_sssp(H["off"], H["tgt"], H["w"], s, bf)[0], s
+    s = D["sources"][0]
+    d, p, _ = gpu_bfs(G, g, n, s)
+    assert oracle.check_bfs(H["off"], H["tgt"], s, d, p)[0]
+    # symmetric graph: |d(u) - d(v)| <= 1 across every edge (BJ north star)
+    u = np.repeat(np.arange(n, dtype=np.uint32), np.diff(H["off"]))
+    fin = d[u] != 0xFFFFFFFF
+    assert (np.abs(d[u][fin].astype(np.int64) - d[H["tgt"]][fin].astype(np.int64)) <= 1).all()
+    g.close()
+
+
+def test_c5_full(G):
+    D, H = build("c5", False)
+    g = G.Graph(D["offsets"], D["targets"], None, symmetric=False)
+    n = D["n"]
+    for s in D["sources"][:2]:
+        base, p, st = gpu_bfs(G, g, n, s, 20)
+        assert oracle.check_bfs(H["off"], H["tgt"], s, base, p)[0], s
+        for T in (10, 40):
+            assert (gpu_bfs(G, g, n, s, T)[0] == base).all()
+    g.close()
