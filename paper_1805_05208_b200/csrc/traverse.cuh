@@ -47,16 +47,9 @@ constexpr int NWARPS = BLOCK / 32;
 constexpr int TE = 256;               // edges per warp tile (edgeMapBlocked bsize)
 constexpr int NCH = 4;                // 32-edge chunks in flight per batch
 constexpr int WCAP = 384;             // per-warp staging capacity (vertices)
-#ifndef GBBS_PW
-#define GBBS_PW 2
-#endif
-constexpr int PW = GBBS_PW;           // bitmap words per warp iteration
 constexpr long long HEAVY = 512;      // bitmap-forward: deferred to heavy tiles above this
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr int KBITS = 10;             // head slot = (tag << KBITS) | owner index
-constexpr int32_t KMASK = (1 << KBITS) - 1;
-constexpr int32_t TAG_MAX = (1 << (31 - KBITS)) - 1;
 
 enum Algo { ALGO_BFS = 0, ALGO_BF = 1 };
 enum Emit { EMIT_LIST = 0, EMIT_COUNT = 1 };
@@ -108,10 +101,24 @@ struct Params {
 #endif
 };
 
-struct WarpSmem {             // one per warp; nothing here is shared across warps
-  alignas(16) int32_t head[TE];  // owner index of every edge slot of the tile
+constexpr int SWEEP_WORDS = 32;        // bitmap words gathered per warp step (sweeps)
+
+struct TileSmem {              // list-push tile (shared-memory owner path)
+  alignas(16) int32_t head[TE];  // 1 + owner index of the first edge slot of each owner
   long long base[TE + 1];        // owner base (offset - O)
   uint32_t own[TE + 1];          // owner vertex (BFS) or its distance (BF)
+};
+
+struct SweepSmem {             // bitmap sweeps: candidates of SWEEP_WORDS words, compacted
+  uint32_t cand[SWEEP_WORDS * 32];
+  uint32_t found[SWEEP_WORDS];
+};
+
+struct WarpSmem {             // one per warp; nothing here is shared across warps
+  union {
+    TileSmem t;
+    SweepSmem s;
+  } u;
   uint32_t stage[WCAP];          // winners awaiting warp_flush
 };
 
@@ -125,7 +132,6 @@ struct Smem {
 // EMIT_COUNT rounds, and gbbs_round_stat counters (STATS builds only).
 struct WarpState {
   int scnt = 0;
-  int tag = 0;
   unsigned long long K = 0, D = 0;
   unsigned long long edges = 0, swept = 0, acquired = 0;
 };
@@ -446,7 +452,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
 // ---- list push: one warp, one tile of TE edges of list `lb` ---------------------
 
 template <int ALGO, bool STATS, int EMIT>
-__device__ __forceinline__ void push_tile(const Params &p, WarpSmem &w, WarpState &ws, int lb,
+__device__ __forceinline__ void push_tile(const Params &p, WarpSmem &wsm, WarpState &ws, int lb,
                                           long long t, long long ntiles, long long f, long long E,
                                           int nb, int r, uint32_t *bits, const uint32_t *prebits) {
   const int lane = threadIdx.x & 31;
@@ -496,18 +502,19 @@ __device__ __forceinline__ void push_tile(const Params &p, WarpSmem &w, WarpStat
           }
         }
       }
-      apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+      apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
     }
   } else {
     // Shared-memory path (many low-degree owners): stage every owner of the tile,
-    // mark the slot where each owner's first in-tile edge lies, and expand owner
-    // ids over the TE slots with a warp max-scan (slots hold tag << KBITS | k, so
-    // stale slots from earlier tiles lose to the current tag).
-    if (++ws.tag >= TAG_MAX) {
-      for (int i = lane; i < TE; i += 32) w.head[i] = 0;
-      ws.tag = 1;
+    // mark the slot where each owner's first in-tile edge lies (1 + owner index),
+    // and expand owner ids over the TE slots with a warp max-scan.
+    TileSmem &w = wsm.u.t;
+    {
+      int4 *h4 = reinterpret_cast<int4 *>(w.head);
+#pragma unroll
+      for (int q = 0; q < TE / 128; q++) h4[q * 32 + lane] = make_int4(0, 0, 0, 0);
     }
-    const int32_t tv = ws.tag << KBITS;
+    __syncwarp();
     for (int kb = 0; kb < nown; kb += 64) {
       long long o2[2], b2[2];
       uint32_t u2[2];
@@ -529,7 +536,7 @@ __device__ __forceinline__ void push_tile(const Params &p, WarpSmem &w, WarpStat
         if (kk < nown) {
           w.base[kk] = b2[h];
           w.own[kk] = (ALGO == ALGO_BF) ? ld_relaxed(p.dist + u2[h]) : u2[h];
-          if (o2[h] < TE) w.head[o2[h] > 0 ? o2[h] : 0] = tv | kk;
+          if (o2[h] < TE) w.head[o2[h] > 0 ? o2[h] : 0] = kk + 1;
         }
       }
     }
@@ -571,91 +578,94 @@ __device__ __forceinline__ void push_tile(const Params &p, WarpSmem &w, WarpStat
         ww[j] = 0;
         uu[j] = 0;
         if (act[j]) {
-          const int kk = w.head[e - ts] & KMASK;
+          const int kk = w.head[e - ts] - 1;
           const long long bb = w.base[kk];
           uu[j] = w.own[kk];
           vv[j] = ld_stream(p.tgt + bb + e);
           if (ALGO == ALGO_BF) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
         }
       }
-      apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+      apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
     }
     __syncwarp();
   }
 }
 
-// ---- bitmap-forward push: PW frontier words per warp iteration ----------------------
-// BFS: frontier = vis_cur & ~vis_old (what the last dense round added); the TS
-// target is vis_old, which also absorbs the frontier bits (atomicOr) so that it
-// becomes the next visited set; vis_cur is read-only and serves as the pre-check.
-// BF: frontier = fr (this round's TS bits), cleared as swept; TS target = bits.
-// Each lane owns one vertex per word (PW vertices); the light vertices' edges
-// are walked as one flattened per-lane sequence, NCH edges per batch, so the
-// loads of different vertices overlap.
+// ---- bitmap sweeps: gather + compact --------------------------------------------
+// A warp takes SWEEP_WORDS consecutive bitmap words (one per lane, coalesced),
+// compacts the candidate vertices of all of them into shared memory in vertex
+// order, and then works through them 32 (or 64) at a time, one per lane — so a
+// sparse bitmap costs one step per 32 candidates, not one per 32 vertices.
+
+// Compact the set bits of lane-owned words (word w0 + lane) into w.cand.
+// Returns the number of candidates (warp-uniform).
+__device__ __forceinline__ int warp_gather(SweepSmem &w, long long w0, uint32_t bits) {
+  const int lane = threadIdx.x & 31;
+  int c = __popc(bits), inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  int k = inc - c;
+  const uint32_t base = (uint32_t)((w0 + lane) * 32);
+  while (bits) {
+    const int b = __ffs(bits) - 1;
+    bits &= bits - 1;
+    w.cand[k++] = base + b;
+  }
+  __syncwarp();
+  return __shfl_sync(FULL, inc, 31);
+}
+
+// ---- bitmap-forward push ----------------------------------------------------------
+// BFS: frontier = precheck (vis_cur) & ~bits (vis_old): what the last dense round
+// added; the TS target is vis_old, which also absorbs the frontier bits (atomicOr)
+// so that it becomes the next visited set; vis_cur is read-only and is the
+// pre-check.  BF: frontier = fr (this round's TS bits), cleared as swept.
+// Each frontier vertex: lane-owned when <= 32 edges (NCH edges per batch),
+// warp-owned when <= HEAVY edges, appended to the heavy list above that.
 template <int ALGO, bool STATS, int EMIT>
-__device__ __forceinline__ void forward_words(const Params &p, WarpSmem &w, WarpState &ws,
+__device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, WarpState &ws,
                                               long long w0, uint32_t *fr, uint32_t *bits,
                                               const uint32_t *precheck, int nb, int r) {
   const uint32_t *prebits = (ALGO == ALGO_BFS) ? precheck : bits;
   const int lane = threadIdx.x & 31;
-  uint32_t fw[PW];
-#pragma unroll
-  for (int q = 0; q < PW; q++) {
-    fw[q] = 0;
-    if (w0 + q < p.nwords) {
-      if (ALGO == ALGO_BFS) fw[q] = precheck[w0 + q] & ~ld_relaxed(bits + w0 + q);
-      else fw[q] = fr[w0 + q];
+  SweepSmem &w = wsm.u.s;
+  const long long word = w0 + lane;
+  uint32_t fw = 0;
+  if (word < p.nwords) {
+    if (ALGO == ALGO_BFS) {
+      fw = precheck[word] & ~ld_relaxed(bits + word);
+      if (fw) atomicOr(bits + word, fw);
+    } else {
+      fw = fr[word];
+      if (fw) fr[word] = 0;
     }
   }
-  unsigned any = 0;
-#pragma unroll
-  for (int q = 0; q < PW; q++) {
-    any |= fw[q];
-    if (fw[q] && lane == 0) {
-      if (ALGO == ALGO_BFS) atomicOr(bits + w0 + q, fw[q]);
-      else fr[w0 + q] = 0;
+  if (!__any_sync(FULL, fw != 0)) return;
+  const int cnt = warp_gather(w, w0, fw);
+  if (STATS && lane == 0) ws.swept += cnt;
+  for (int c0 = 0; c0 < cnt; c0 += 32) {
+    const bool valid = c0 + lane < cnt;
+    const uint32_t v = valid ? w.cand[c0 + lane] : 0;
+    long long a = 0;
+    int dg = 0;
+    if (valid) {
+      a = __ldg(p.off + v);
+      dg = (int)(__ldg(p.off + v + 1) - a);
     }
-  }
-  if (!any) return;  // warp-uniform
-  long long a[PW];
-  int dg[PW];
-  uint32_t x[PW];
-#pragma unroll
-  for (int q = 0; q < PW; q++) {
-    a[q] = 0;
-    dg[q] = 0;
-    if ((fw[q] >> lane) & 1u) {
-      const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
-      a[q] = __ldg(p.off + v);
-      dg[q] = (int)(__ldg(p.off + v + 1) - a[q]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < PW; q++) {
-    const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
-    x[q] = v;
-    if (ALGO == ALGO_BF) x[q] = dg[q] > 0 ? ld_relaxed(p.dist + v) : 0u;
-  }
-  int mine[PW];
-#pragma unroll
-  for (int q = 0; q < PW; q++) {
-    if (!fw[q]) {  // warp-uniform
-      mine[q] = 0;
-      continue;
-    }
-    const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
-    if (STATS && lane == 0) ws.swept += __popc(fw[q]);
-    // heavy vertices -> heavy list (pushed in tiles after the grid barrier)
-    const bool heavy = dg[q] > (int)HEAVY;
-    warp_append(p, LIST_HEAVY, p.hcnt + (r & 1), heavy, v, a[q], dg[q]);
-    // medium vertices: the whole warp walks one vertex's edges at a time
-    unsigned med = __ballot_sync(FULL, dg[q] > 32 && !heavy);
+    uint32_t x = v;
+    if (ALGO == ALGO_BF) x = dg > 0 ? ld_relaxed(p.dist + v) : 0u;
+    const bool heavy = dg > (int)HEAVY;
+    warp_append(p, LIST_HEAVY, p.hcnt + (r & 1), heavy, v, a, dg);
+    unsigned med = __ballot_sync(FULL, dg > 32 && !heavy);
     while (med) {
       const int l = __ffs(med) - 1;
       med &= med - 1;
-      const long long la = __shfl_sync(FULL, a[q], l);
-      const int ld = __shfl_sync(FULL, dg[q], l);
-      const uint32_t lx = __shfl_sync(FULL, x[q], l);
+      const long long la = __shfl_sync(FULL, a, l);
+      const int ld = __shfl_sync(FULL, dg, l);
+      const uint32_t lx = __shfl_sync(FULL, x, l);
       if (STATS && lane == 0) ws.edges += ld;
       for (int cs = 0; cs < ld; cs += 32 * NCH) {
         uint32_t vv[NCH], ww[NCH], uu[NCH];
@@ -668,55 +678,39 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &w, Warp
           ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? ld_stream(p.wgt + la + e) : 1u) : 0;
           uu[j] = lx;
         }
-        apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+        apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
       }
     }
-    mine[q] = (dg[q] <= 32) ? dg[q] : 0;
-  }
-  // light vertices: one flattened edge sequence per lane over its PW vertices
-  int tot = 0;
+    const int mine = dg <= 32 ? dg : 0;
+    if (STATS) ws.edges += mine;
+    int mx = mine;
 #pragma unroll
-  for (int q = 0; q < PW; q++) tot += mine[q];
-  if (STATS) ws.edges += tot;
-  int mx = tot;
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+    for (int jj = 0; jj < mx; jj += NCH) {
+      uint32_t vv[NCH], ww[NCH], uu[NCH];
+      bool act[NCH];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
-  for (int jj = 0; jj < mx; jj += NCH) {
-    uint32_t vv[NCH], ww[NCH], uu[NCH];
-    bool act[NCH];
-#pragma unroll
-    for (int j = 0; j < NCH; j++) {
-      int idx = jj + j;
-      act[j] = idx < tot;
-      long long base = a[0];
-      uint32_t xo = x[0];
-#pragma unroll
-      for (int q = 0; q < PW - 1; q++) {  // locate the vertex holding flattened edge idx
-        if (idx >= mine[q]) {
-          idx -= mine[q];
-          base = a[q + 1];
-          xo = x[q + 1];
-        } else {
-          break;
-        }
+      for (int j = 0; j < NCH; j++) {
+        act[j] = jj + j < mine;
+        vv[j] = act[j] ? ld_stream(p.tgt + a + jj + j) : 0;
+        ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? ld_stream(p.wgt + a + jj + j) : 1u) : 0;
+        uu[j] = x;
       }
-      vv[j] = act[j] ? ld_stream(p.tgt + base + idx) : 0;
-      ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? ld_stream(p.wgt + base + idx) : 1u) : 0;
-      uu[j] = xo;
+      apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
     }
-    apply_batch<ALGO, STATS, EMIT>(p, w.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
   }
+  __syncwarp();
 }
 
-// ---- dense pull (BFS): PW bitmap words per warp iteration -------------------------
-// Every lane owns one vertex per word.  In-edges are read as 16-byte aligned
-// groups of 4 (one vector load covers the group containing the scan position),
-// all PW vertices' loads and visited probes issued together.  A vertex with more
-// than LONG_IN in-edges left after PULL_STEPS steps is finished cooperatively by
-// the whole warp, 128 in-edges per step, so one long in-list cannot hold the
-// warp (and the round) hostage.
+// ---- dense pull (BFS) ---------------------------------------------------------------
+// Candidates = unvisited vertices of SWEEP_WORDS words, PCH*32 in flight per step,
+// one per lane.  In-edges are read as 16-byte aligned groups of 4 (one vector
+// load covers the group containing the scan position); a vertex with more than
+// LONG_IN in-edges left after PULL_STEPS steps is finished by the whole warp,
+// 128 in-edges per step, so one long in-list cannot hold the warp hostage.
 constexpr int PULL_STEPS = 2;
 constexpr int LONG_IN = 24;
+constexpr int PCH = 2;
 
 __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4(p); }
 
@@ -725,81 +719,57 @@ __device__ __forceinline__ bool vbit(const uint32_t *vis, uint32_t u) {
 }
 
 template <bool STATS>
-__device__ __forceinline__ void pull_words(const Params &p, long long w0, const uint32_t *vis,
-                                           uint32_t *vis_next, int r, WarpState &ws) {
+__device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0,
+                                           const uint32_t *vis, uint32_t *vis_next, int r,
+                                           WarpState &ws) {
   const int lane = threadIdx.x & 31;
-  uint32_t vw[PW];
-#pragma unroll
-  for (int q = 0; q < PW; q++) vw[q] = (w0 + q < p.nwords) ? vis[w0 + q] : FULL;
-  unsigned todo = 0;
-#pragma unroll
-  for (int q = 0; q < PW; q++) todo |= ~vw[q];
-  if (!todo) {  // all visited (warp-uniform): carry the words over
-    if (lane < PW && w0 + lane < p.nwords) vis_next[w0 + lane] = FULL;
+  SweepSmem &w = wsm.u.s;
+  const long long word = w0 + lane;
+  const uint32_t vw = word < p.nwords ? vis[word] : FULL;
+  if (!__any_sync(FULL, vw != FULL)) {  // all visited: carry the words over
+    if (word < p.nwords) vis_next[word] = FULL;
     return;
   }
-  long long js[PW];
-  int rem[PW], deg_in[PW];
+  const int cnt = warp_gather(w, w0, ~vw);
+  w.found[lane] = 0;
+  __syncwarp();
+  if (STATS && lane == 0) ws.swept += cnt;
+  for (int c0 = 0; c0 < cnt; c0 += 32 * PCH) {
+    uint32_t v[PCH], par[PCH];
+    long long js[PCH];
+    int rem[PCH], deg_in[PCH];
 #pragma unroll
-  for (int q = 0; q < PW; q++) {
-    js[q] = 0;
-    rem[q] = 0;
-    if (!((vw[q] >> lane) & 1u)) {
-      const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
-      js[q] = ld_stream64(p.in_off + v);
-      rem[q] = (int)(ld_stream64(p.in_off + v + 1) - js[q]);
-      if (STATS) ws.swept += 1;
-    }
-    deg_in[q] = rem[q];
-  }
-  uint32_t par[PW];
-#pragma unroll
-  for (int q = 0; q < PW; q++) par[q] = INF;
-  for (int step = 0; step < PULL_STEPS; step++) {
-    uint4 g[PW];
-#pragma unroll
-    for (int q = 0; q < PW; q++)
-      if (rem[q] > 0) g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
-    bool live = false;
-#pragma unroll
-    for (int q = 0; q < PW; q++) {
-      if (rem[q] <= 0) continue;
-      const int lo = (int)(js[q] & 3);
-      const int hi = min(4, lo + rem[q]);
-      const uint32_t e[4] = {g[q].x, g[q].y, g[q].z, g[q].w};
-      bool b[4];
-#pragma unroll
-      for (int k = 0; k < 4; k++) b[k] = (k >= lo && k < hi) ? vbit(vis, e[k]) : false;
-      uint32_t hit = INF;
-#pragma unroll
-      for (int k = 3; k >= 0; k--)
-        if (b[k]) hit = e[k];
-      if (STATS) ws.edges += hi - lo;
-      js[q] += hi - lo;
-      rem[q] -= hi - lo;
-      if (hit != INF) {
-        par[q] = hit;
-        rem[q] = 0;
+    for (int q = 0; q < PCH; q++) {
+      const int i = c0 + 32 * q + lane;
+      v[q] = i < cnt ? w.cand[i] : 0;
+      js[q] = 0;
+      rem[q] = 0;
+      par[q] = INF;
+      if (i < cnt) {
+        js[q] = ld_stream64(p.in_off + v[q]);
+        rem[q] = (int)(ld_stream64(p.in_off + v[q] + 1) - js[q]);
       }
-      live |= rem[q] > 0;
+      deg_in[q] = rem[q];
     }
-    if (!__any_sync(FULL, live)) break;
-  }
-  // short remainders: per lane; long remainders: the whole warp, one vertex at a time
+    for (int step = 0; step < PULL_STEPS; step++) {
+      uint4 g[PCH];
 #pragma unroll
-  for (int q = 0; q < PW; q++) {
-    for (;;) {
-      const bool go = rem[q] > 0 && rem[q] <= LONG_IN;
-      if (!__any_sync(FULL, go)) break;
-      if (go) {
-        const uint4 g = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+      for (int q = 0; q < PCH; q++)
+        if (rem[q] > 0) g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+      bool live = false;
+#pragma unroll
+      for (int q = 0; q < PCH; q++) {
+        if (rem[q] <= 0) continue;
         const int lo = (int)(js[q] & 3);
         const int hi = min(4, lo + rem[q]);
-        const uint32_t e[4] = {g.x, g.y, g.z, g.w};
+        const uint32_t e[4] = {g[q].x, g[q].y, g[q].z, g[q].w};
+        bool b[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) b[k] = (k >= lo && k < hi) ? vbit(vis, e[k]) : false;
         uint32_t hit = INF;
 #pragma unroll
         for (int k = 3; k >= 0; k--)
-          if (k >= lo && k < hi && vbit(vis, e[k])) hit = e[k];
+          if (b[k]) hit = e[k];
         if (STATS) ws.edges += hi - lo;
         js[q] += hi - lo;
         rem[q] -= hi - lo;
@@ -807,58 +777,85 @@ __device__ __forceinline__ void pull_words(const Params &p, long long w0, const 
           par[q] = hit;
           rem[q] = 0;
         }
+        live |= rem[q] > 0;
       }
+      if (!__any_sync(FULL, live)) break;
     }
-    unsigned longs = __ballot_sync(FULL, rem[q] > LONG_IN);
-    while (longs) {
-      const int l = __ffs(longs) - 1;
-      longs &= longs - 1;
-      long long a = __shfl_sync(FULL, js[q], l);
-      const long long e_end = a + __shfl_sync(FULL, rem[q], l);
-      uint32_t found = INF;
-      while (a < e_end) {
-        // lane k reads the aligned group a0 + 4k .. a0 + 4k + 3
-        const long long a0 = a & ~3ll;
-        const long long gk = a0 + 4 * lane;
-        uint32_t hit = INF;
-        if (gk < e_end) {
-          const uint4 g = ldg_v4(p.in_tgt + gk);
+    // short remainders: per lane; long remainders: the whole warp, one vertex at a time
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      for (;;) {
+        const bool go = rem[q] > 0 && rem[q] <= LONG_IN;
+        if (!__any_sync(FULL, go)) break;
+        if (go) {
+          const uint4 g = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+          const int lo = (int)(js[q] & 3);
+          const int hi = min(4, lo + rem[q]);
           const uint32_t e[4] = {g.x, g.y, g.z, g.w};
+          uint32_t hit = INF;
 #pragma unroll
           for (int k = 3; k >= 0; k--)
-            if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit = e[k];
+            if (k >= lo && k < hi && vbit(vis, e[k])) hit = e[k];
+          if (STATS) ws.edges += hi - lo;
+          js[q] += hi - lo;
+          rem[q] -= hi - lo;
+          if (hit != INF) {
+            par[q] = hit;
+            rem[q] = 0;
+          }
         }
-        const unsigned hb = __ballot_sync(FULL, hit != INF);
-        if (STATS && lane == 0) ws.edges += min(a0 + 128, e_end) - a;
-        if (hb) {
-          found = __shfl_sync(FULL, hit, __ffs(hb) - 1);
-          break;
-        }
-        a = a0 + 128;
       }
-      if (lane == l) {
-        rem[q] = 0;
-        par[q] = found;
-      }
-    }
-  }
+      unsigned longs = __ballot_sync(FULL, rem[q] > LONG_IN);
+      while (longs) {
+        const int l = __ffs(longs) - 1;
+        longs &= longs - 1;
+        long long a = __shfl_sync(FULL, js[q], l);
+        const long long e_end = a + __shfl_sync(FULL, rem[q], l);
+        uint32_t found = INF;
+        while (a < e_end) {
+          const long long a0 = a & ~3ll;
+          const long long gk = a0 + 4 * lane;
+          uint32_t hit = INF;
+          if (gk < e_end) {
+            const uint4 g = ldg_v4(p.in_tgt + gk);
+            const uint32_t e[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-  for (int q = 0; q < PW; q++) {
-    const bool found = par[q] != INF;
-    const unsigned nbm = __ballot_sync(FULL, found);
-    if (w0 + q < p.nwords && lane == 0) vis_next[w0 + q] = vw[q] | nbm;
-    if (found) {
-      const uint32_t v = (uint32_t)((w0 + q) * 32 + lane);
-      if (STATS) ws.acquired += 1;
-      st_stream(p.dist + v, (uint32_t)(r + 1));
-      if (p.parent) st_stream(p.parent + v, par[q]);
-      const uint32_t dgo = p.symmetric ? (uint32_t)deg_in[q] : __ldg(p.odeg + v);
-      if (dgo > 0) {
-        ws.K += 1;
-        ws.D += dgo;
+            for (int k = 3; k >= 0; k--)
+              if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit = e[k];
+          }
+          const unsigned hb = __ballot_sync(FULL, hit != INF);
+          if (STATS && lane == 0) ws.edges += min(a0 + 128, e_end) - a;
+          if (hb) {
+            found = __shfl_sync(FULL, hit, __ffs(hb) - 1);
+            break;
+          }
+          a = a0 + 128;
+        }
+        if (lane == l) {
+          rem[q] = 0;
+          par[q] = found;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      if (par[q] != INF) {
+        const uint32_t vq = v[q];
+        if (STATS) ws.acquired += 1;
+        st_stream(p.dist + vq, (uint32_t)(r + 1));
+        if (p.parent) st_stream(p.parent + vq, par[q]);
+        atomicOr(&w.found[(vq >> 5) - (uint32_t)w0], 1u << (vq & 31));
+        const uint32_t dgo = p.symmetric ? (uint32_t)deg_in[q] : __ldg(p.odeg + vq);
+        if (dgo > 0) {
+          ws.K += 1;
+          ws.D += dgo;
+        }
       }
     }
   }
+  __syncwarp();
+  if (word < p.nwords) vis_next[word] = vw | w.found[lane];
+  __syncwarp();
 }
 
 // ---- the persistent kernel ---------------------------------------------------
@@ -877,7 +874,7 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
                                               WarpSmem &w, WarpState &ws, uint32_t *fr,
                                               uint32_t *bits, const uint32_t *precheck, int nb,
                                               int r, long long gw, long long nw) {
-  for (long long w0 = gw * PW; w0 < p.nwords; w0 += nw * PW)
+  for (long long w0 = gw * SWEEP_WORDS; w0 < p.nwords; w0 += nw * SWEEP_WORDS)
     forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, fr, bits, precheck, nb, r);
   grid.sync();  // heavy list complete
   if (threadIdx.x == 0) s.hcnt = ld_relaxed64(p.hcnt + (r & 1));
@@ -904,8 +901,6 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
   const long long nw = (long long)gridDim.x * NWARPS;
   const uint32_t src = p.src;
   WarpSmem &wsm = s.w[warp];
-  for (int i = lane; i < TE; i += 32) wsm.head[i] = 0;
-  int tag = 0;
 
   // a1: per-run init
   for (long long i = gtid; i < p.n; i += gstride) {
@@ -975,13 +970,12 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     }
     const int cb = (int)(r & 1), nb = cb ^ 1;
     WarpState ws;
-    ws.tag = tag;
     bool emit_count = false;
     if (kind == 1) {  // dense pull (BFS)
       const uint32_t *vis = p.bm[vc];
       uint32_t *vis_next = p.bm[vc ^ 1];
-      for (long long w0 = gw * PW; w0 < p.nwords; w0 += nw * PW)
-        pull_words<STATS>(p, w0, vis, vis_next, (int)r, ws);
+      for (long long w0 = gw * SWEEP_WORDS; w0 < p.nwords; w0 += nw * SWEEP_WORDS)
+        pull_words<STATS>(p, wsm, w0, vis, vis_next, (int)r, ws);
       vc ^= 1;
       list_valid = false;
       emit_count = true;
@@ -1023,7 +1017,6 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
       const unsigned long long K = warp_sum64((long long)ws.K), D = warp_sum64((long long)ws.D);
       if (lane == 0 && K) atomicAdd(p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
     }
-    tag = ws.tag;
     if (STATS) t_flush = globaltimer_ns();
     if (STATS && p.stats && r < p.stats_cap) {
       // one global atomic per CTA and counter
