@@ -450,29 +450,36 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
 }
 
 // ---- list push: one warp, one tile of TE edges of list `lb` ---------------------
+// Tiles are handed to warps in contiguous blocks, so a warp searches O once per
+// round (warp_upper) and then carries the owner index from tile to tile: a
+// tile's owners are i0, i0+1, ... while O < te, discovered from the owner loads
+// the tile needs anyway.  Returns the first owner of the next tile.
 
 template <int ALGO, bool STATS, int EMIT>
-__device__ __forceinline__ void push_tile(const Params &p, WarpSmem &wsm, WarpState &ws, int lb,
-                                          long long t, long long ntiles, long long f, long long E,
-                                          int nb, int r, uint32_t *bits, const uint32_t *prebits) {
+__device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, WarpState &ws,
+                                               int lb, long long i0, long long t, long long f,
+                                               long long E, int nb, int r, uint32_t *bits,
+                                               const uint32_t *prebits) {
+  constexpr long long BIG = 0x7FFFFFFFFFFFFFFFll;
   const int lane = threadIdx.x & 31;
   const long long ts = t * TE;
   const long long te = min(ts + (long long)TE, E);
   const long long *O = p.fo[lb];
   const long long *B = p.fb[lb];
   const uint32_t *F = p.fv[lb];
-  const long long i0 = warp_upper(O, 0, f, ts);
-  const long long il = warp_upper(O, i0, min(f, i0 + TE + 1), te - 1);
-  const int nown = (int)(il - i0 + 1);
   if (STATS && lane == 0) ws.edges += (unsigned long long)(te - ts);
 
-  if (nown <= 32) {
+  const long long k = i0 + lane;
+  long long Ok = k < f ? __ldcg(O + k) : BIG;
+  const unsigned inb = __ballot_sync(FULL, Ok < te);  // owners with an edge in the tile
+  const int n32 = __popc(inb);
+  if (n32 < 32) {
     // Register path: lane k holds owner i0+k; a chunk's owners come from a
     // ballot (owners starting at or before the chunk) plus an or-reduce of the
     // owners starting inside it.
-    const bool valid = lane < nown;
-    const long long k = i0 + lane;
-    const long long Ok = valid ? __ldcg(O + k) : 0x7FFFFFFFFFFFFFFFll;
+    const long long onext = __shfl_sync(FULL, Ok, n32);
+    const bool valid = lane < n32;
+    if (!valid) Ok = BIG;
     const long long Bk = valid ? __ldcg(B + k) : 0;
     const uint32_t Uk = valid ? __ldcg(F + k) : 0;
     uint32_t Xk = Uk;
@@ -504,91 +511,105 @@ __device__ __forceinline__ void push_tile(const Params &p, WarpSmem &wsm, WarpSt
       }
       apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
     }
-  } else {
-    // Shared-memory path (many low-degree owners): stage every owner of the tile,
-    // mark the slot where each owner's first in-tile edge lies (1 + owner index),
-    // and expand owner ids over the TE slots with a warp max-scan.
-    TileSmem &w = wsm.u.t;
-    {
-      int4 *h4 = reinterpret_cast<int4 *>(w.head);
-#pragma unroll
-      for (int q = 0; q < TE / 128; q++) h4[q * 32 + lane] = make_int4(0, 0, 0, 0);
-    }
-    __syncwarp();
-    for (int kb = 0; kb < nown; kb += 64) {
-      long long o2[2], b2[2];
-      uint32_t u2[2];
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int kk = kb + 32 * h + lane;
-        o2[h] = 0x7FFFFFFFFFFFFFFFll;
-        b2[h] = 0;
-        u2[h] = 0;
-        if (kk < nown) {
-          o2[h] = __ldcg(O + i0 + kk) - ts;
-          b2[h] = __ldcg(B + i0 + kk);
-          u2[h] = __ldcg(F + i0 + kk);
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int kk = kb + 32 * h + lane;
-        if (kk < nown) {
-          w.base[kk] = b2[h];
-          w.own[kk] = (ALGO == ALGO_BF) ? ld_relaxed(p.dist + u2[h]) : u2[h];
-          if (o2[h] < TE) w.head[o2[h] > 0 ? o2[h] : 0] = kk + 1;
-        }
-      }
-    }
-    __syncwarp();
-    {
-      constexpr int PER = TE / 32;
-      int32_t a[PER];
-      const int4 *h4 = reinterpret_cast<const int4 *>(w.head + lane * PER);
-#pragma unroll
-      for (int q = 0; q < PER / 4; q++) {
-        const int4 x = h4[q];
-        a[4 * q] = x.x; a[4 * q + 1] = x.y; a[4 * q + 2] = x.z; a[4 * q + 3] = x.w;
-      }
-#pragma unroll
-      for (int q = 1; q < PER; q++) a[q] = max(a[q], a[q - 1]);
-      int32_t inc = a[PER - 1];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(FULL, inc, o);
-        if (lane >= o) inc = max(inc, y);
-      }
-      int32_t ex = __shfl_up_sync(FULL, inc, 1);
-      if (lane == 0) ex = 0;
-      int4 *o4 = reinterpret_cast<int4 *>(w.head + lane * PER);
-#pragma unroll
-      for (int q = 0; q < PER / 4; q++)
-        o4[q] = make_int4(max(ex, a[4 * q]), max(ex, a[4 * q + 1]), max(ex, a[4 * q + 2]),
-                          max(ex, a[4 * q + 3]));
-    }
-    __syncwarp();
-    for (long long cs = ts; cs < te; cs += 32 * NCH) {
-      uint32_t vv[NCH], ww[NCH], uu[NCH];
-      bool act[NCH];
-#pragma unroll
-      for (int j = 0; j < NCH; j++) {
-        const long long e = cs + 32 * j + lane;
-        act[j] = e < te;
-        vv[j] = 0;
-        ww[j] = 0;
-        uu[j] = 0;
-        if (act[j]) {
-          const int kk = w.head[e - ts] - 1;
-          const long long bb = w.base[kk];
-          uu[j] = w.own[kk];
-          vv[j] = ld_stream(p.tgt + bb + e);
-          if (ALGO == ALGO_BF) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
-        }
-      }
-      apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
-    }
-    __syncwarp();
+    return onext == te ? i0 + n32 : i0 + n32 - 1;
   }
+  // Shared-memory path (many low-degree owners): stage every owner of the tile,
+  // mark the slot where each owner's first in-tile edge lies (1 + owner index),
+  // and expand owner ids over the TE slots with a warp max-scan.
+  TileSmem &w = wsm.u.t;
+  {
+    int4 *h4 = reinterpret_cast<int4 *>(w.head);
+#pragma unroll
+    for (int q = 0; q < TE / 128; q++) h4[q * 32 + lane] = make_int4(0, 0, 0, 0);
+  }
+  __syncwarp();
+  int nown = 0;
+  long long onext = BIG;
+  for (int kb = 0;; kb += 64) {
+    long long o2[2], b2[2];
+    uint32_t u2[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const long long kk = i0 + kb + 32 * h + lane;
+      o2[h] = kk < f ? __ldcg(O + kk) : BIG;
+      b2[h] = 0;
+      u2[h] = 0;
+      if (o2[h] < te) {
+        b2[h] = __ldcg(B + kk);
+        u2[h] = __ldcg(F + kk);
+      }
+    }
+    int cnt_h[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int kk = kb + 32 * h + lane;
+      cnt_h[h] = __popc(__ballot_sync(FULL, o2[h] < te));
+      if (o2[h] < te) {
+        w.base[kk] = b2[h];
+        w.own[kk] = (ALGO == ALGO_BF) ? ld_relaxed(p.dist + u2[h]) : u2[h];
+        const long long o = o2[h] - ts;
+        w.head[o > 0 ? o : 0] = kk + 1;
+      }
+    }
+    nown += cnt_h[0] + cnt_h[1];
+    if (cnt_h[0] < 32) {
+      onext = __shfl_sync(FULL, o2[0], cnt_h[0]);
+      break;
+    }
+    if (cnt_h[1] < 32) {
+      onext = __shfl_sync(FULL, o2[1], cnt_h[1]);
+      break;
+    }
+  }
+  __syncwarp();
+  {
+    constexpr int PER = TE / 32;
+    int32_t a[PER];
+    const int4 *h4 = reinterpret_cast<const int4 *>(w.head + lane * PER);
+#pragma unroll
+    for (int q = 0; q < PER / 4; q++) {
+      const int4 x = h4[q];
+      a[4 * q] = x.x; a[4 * q + 1] = x.y; a[4 * q + 2] = x.z; a[4 * q + 3] = x.w;
+    }
+#pragma unroll
+    for (int q = 1; q < PER; q++) a[q] = max(a[q], a[q - 1]);
+    int32_t inc = a[PER - 1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc = max(inc, y);
+    }
+    int32_t ex = __shfl_up_sync(FULL, inc, 1);
+    if (lane == 0) ex = 0;
+    int4 *o4 = reinterpret_cast<int4 *>(w.head + lane * PER);
+#pragma unroll
+    for (int q = 0; q < PER / 4; q++)
+      o4[q] = make_int4(max(ex, a[4 * q]), max(ex, a[4 * q + 1]), max(ex, a[4 * q + 2]),
+                        max(ex, a[4 * q + 3]));
+  }
+  __syncwarp();
+  for (long long cs = ts; cs < te; cs += 32 * NCH) {
+    uint32_t vv[NCH], ww[NCH], uu[NCH];
+    bool act[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      const long long e = cs + 32 * j + lane;
+      act[j] = e < te;
+      vv[j] = 0;
+      ww[j] = 0;
+      uu[j] = 0;
+      if (act[j]) {
+        const int kk = w.head[e - ts] - 1;
+        const long long bb = w.base[kk];
+        uu[j] = w.own[kk];
+        vv[j] = ld_stream(p.tgt + bb + e);
+        if (ALGO == ALGO_BF) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
+      }
+    }
+    apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+  }
+  __syncwarp();
+  return onext == te ? i0 + nown : i0 + nown - 1;
 }
 
 // ---- bitmap sweeps: gather + compact --------------------------------------------
@@ -864,9 +885,14 @@ template <int ALGO, bool STATS, int EMIT>
 __device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpState &ws, int lb,
                                            long long f, long long E, int nb, int r, uint32_t *bits,
                                            const uint32_t *prebits, long long gw, long long nw) {
+  // contiguous blocks of tiles per warp: one owner search per warp and round
   const long long ntiles = (E + TE - 1) / TE;
-  for (long long t = gw; t < ntiles; t += nw)
-    push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, t, ntiles, f, E, nb, r, bits, prebits);
+  const long long per = (ntiles + nw - 1) / nw;
+  long long t = gw * per;
+  const long long t1 = min(t + per, ntiles);
+  if (t >= t1) return;
+  long long i0 = warp_upper(p.fo[lb], 0, f, t * TE);
+  for (; t < t1; t++) i0 = push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, i0, t, f, E, nb, r, bits, prebits);
 }
 
 template <int ALGO, bool STATS, int EMIT>
