@@ -143,7 +143,7 @@ def algorithmic_bytes(recs, n, m, algo):
     bytes are returned separately)."""
     alg = 0
     wb = (n + 7) // 8
-    per_edge = 8 if algo == "bf" else 4
+    per_edge = 4 if algo == "bfs" else 8
     for r in recs:
         emit = 36 * r["acquired"]
         if r["dense"] == 1:
@@ -216,10 +216,12 @@ def run_ours(args, rank, world, local):
     def one(src, algo, stats=None):
         if algo == "bfs":
             g.bfs(src, dist, par, stream=stream, opts=opts, stats=stats)
-        else:
+        elif algo == "bf":
             g.bellman_ford(src, dist, stream=stream, stats=stats)
+        else:
+            g.widest_path(src, dist, stream=stream, stats=stats)
 
-    algos = [args.algo] + (["bf"] if (want_w and args.algo == "bfs" and not args.profile) else [])
+    algos = [args.algo] + (["bf", "wp"] if (want_w and args.algo == "bfs" and not args.profile) else [])
     # per-source traversed edges (TEPS numerator, reading A20) and algorithmic bytes
     per_src = {}
     for algo in algos:
@@ -228,7 +230,9 @@ def run_ours(args, rank, world, local):
             one(s, algo, stats=st)
             recs = gbbs.round_records(st)
             alg, state = algorithmic_bytes(recs, n, m, algo)
-            per_src[(algo, s)] = dict(m_reach=reached_edges(torch, off, dist), rounds=st.rounds,
+            reach = reached_edges(torch, off, dist) if algo != "wp" else \
+                int((off[1:] - off[:-1])[dist != 0].sum())
+            per_src[(algo, s)] = dict(m_reach=reach, rounds=st.rounds,
                                       dense_rounds=st.dense_rounds, alg_bytes=alg, state_bytes=state,
                                       relax=sum(r["edges_examined"] for r in recs))
 
@@ -336,6 +340,16 @@ def run_ours(args, rank, world, local):
                 "roofline_frac": round(balg / (bkms * 1e-3) / 1e9 / peak, 4),
                 "kernel_ms_per_step": round(bkms, 4), "clocks": bclk,
                 "rounds": [per_src[("bf", s)]["rounds"] for s in sources]}
+        if "wp" in algos and args.algo == "bfs":
+            wt, wclk, wkms = res["wp"]
+            we = sum(per_src[("wp", s)]["m_reach"] for s in sources)
+            walg = sum(per_src[("wp", s)]["alg_bytes"] for s in sources)
+            out["widest_path"] = {
+                "value": round(we / (wt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective)",
+                "ms_per_step": round(wt, 4), "kernel_ms_per_step": round(wkms, 4),
+                "roofline_frac": round(walg / (wkms * 1e-3) / 1e9 / peak, 4),
+                "note": "NEXT-1: Bellman-Ford over the (max, min) semiring, same graph and weights",
+                "rounds": [per_src[("wp", s)]["rounds"] for s in sources]}
         if not args.profile:
             out["cpu_baseline"] = cpu_baseline(args, G["offsets"], G["targets"], sources, cfg)
     g.close()

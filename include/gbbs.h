@@ -140,6 +140,20 @@ int gbbs_bfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
 int gbbs_bellman_ford(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                       void *cuda_stream);
 
+/*
+ * gbbs_widest_path — widest (bottleneck) path from src by Bellman-Ford over
+ * the (max, min) semiring (sec:algs "Widest Path"; output spec
+ * P:1499-1504): width[v] = max over src->v paths of the minimum edge weight
+ * on the path.  Readings W1/W2: width[src] = GBBS_INF (the empty
+ * path has no bottleneck); unreachable vertices get 0 (the max-semiring
+ * identity; the paper's "infinity if unreachable" repeats the SSSP phrasing).
+ * Weights as for gbbs_bellman_ford (NULL = unit).  Same stream, options and
+ * error conventions as gbbs_bellman_ford (no GBBS_ERANGE: widths never exceed
+ * the largest weight).
+ */
+int gbbs_widest_path(const gbbs_graph *g, uint32_t src, uint32_t *width,
+                     void *cuda_stream);
+
 /* ---- extended calls (bench / tests) ------------------------------------ */
 
 /* Representation choice per round (threshold rule reading A10).
@@ -200,6 +214,9 @@ int gbbs_bfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
 int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                          void *cuda_stream, const gbbs_opts *opts,
                          gbbs_stats *stats);
+int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *width,
+                        void *cuda_stream, const gbbs_opts *opts,
+                        gbbs_stats *stats);
 
 /* Launch geometry of the persistent traversal kernel on this device:
  * *ctas = co-resident CTAs used, *threads = threads per CTA. */

@@ -178,3 +178,33 @@ def reached_edges(offsets, dist):
     off = np.ascontiguousarray(offsets, dtype=np.int64)
     dist = np.ascontiguousarray(dist, dtype=np.uint32)
     return int(_load().oracle_reached_edges(off.shape[0] - 1, _ptr(off), _ptr(dist)))
+
+
+def widest_path(offsets, targets, weights, src):
+    """Modified-Dijkstra widest path (readings W1/W2: width[src] = INF32, unreachable 0)."""
+    n, off, tgt, w = _csr(offsets, targets, weights)
+    width = np.empty(n, np.uint32)
+    lib = _load()
+    lib.oracle_widest_path.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]
+    lib.oracle_widest_path.restype = ctypes.c_int
+    _check(lib.oracle_widest_path(n, _ptr(off), _ptr(tgt), _ptr(w), int(src), _ptr(width)),
+           "oracle_widest_path")
+    return width
+
+
+def check_widest(offsets, targets, weights, src, width):
+    """Widest-path certificate (optimality + tight-edge reachability)."""
+    n, off, tgt, w = _csr(offsets, targets, weights)
+    width = np.ascontiguousarray(width, dtype=np.uint32)
+    bad = ctypes.c_int64(-1)
+    lib = _load()
+    lib.oracle_check_widest.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
+                                        ctypes.c_void_p]
+    lib.oracle_check_widest.restype = ctypes.c_int
+    rc = lib.oracle_check_widest(n, _ptr(off), _ptr(tgt), _ptr(w), int(src), _ptr(width),
+                                 ctypes.addressof(bad))
+    if rc not in (OK, EFAIL):
+        raise RuntimeError(f"oracle_check_widest rc={rc}")
+    return rc == OK, bad.value

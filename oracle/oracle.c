@@ -380,3 +380,145 @@ int64_t oracle_reached_edges(int64_t n, const int64_t *off,
     if (dist[v] != INF32) s += off[v + 1] - off[v];
   return s;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Widest (bottleneck) path, PAPER.md:114-136 (sec:algs "Widest Path"),     */
+/* output spec PAPER.md:1499-1504: width[v] = max over src->v paths of the  */
+/* minimum edge weight.  The definition computed by the textbook modified   */
+/* Dijkstra ("Sequentially, the algorithm can be solved as quickly as SSSP  */
+/* using a modified version of Dijkstra's algorithm"):    */
+/* extract the vertex of largest width, relax width[v] = max(width[v],      */
+/* min(width[u], w)).  Readings W1/W2: width[src] = INF32 (empty */
+/* path), unreachable = 0.  weights NULL = unit.                            */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  uint32_t *heap;
+  int64_t *pos;
+  const uint32_t *key;
+  int64_t size;
+} mheap_t; /* max-heap on key */
+
+static void mheap_swap(mheap_t *h, int64_t i, int64_t j) {
+  uint32_t a = h->heap[i], b = h->heap[j];
+  h->heap[i] = b;
+  h->heap[j] = a;
+  h->pos[b] = i;
+  h->pos[a] = j;
+}
+
+static void mheap_up(mheap_t *h, int64_t i) {
+  while (i > 0) {
+    int64_t p = (i - 1) / 2;
+    if (h->key[h->heap[p]] >= h->key[h->heap[i]]) break;
+    mheap_swap(h, i, p);
+    i = p;
+  }
+}
+
+static void mheap_down(mheap_t *h, int64_t i) {
+  for (;;) {
+    int64_t l = 2 * i + 1, r = l + 1, s = i;
+    if (l < h->size && h->key[h->heap[l]] > h->key[h->heap[s]]) s = l;
+    if (r < h->size && h->key[h->heap[r]] > h->key[h->heap[s]]) s = r;
+    if (s == i) break;
+    mheap_swap(h, i, s);
+    i = s;
+  }
+}
+
+int oracle_widest_path(int64_t n, const int64_t *off, const uint32_t *tgt,
+                       const uint32_t *w, uint32_t src, uint32_t *width) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (width == NULL) return ORACLE_EINVAL;
+  mheap_t h;
+  h.heap = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+  h.pos = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+  char *done = (char *)calloc((size_t)n, 1);
+  if (!h.heap || !h.pos || !done) {
+    free(h.heap); free(h.pos); free(done);
+    return ORACLE_ENOMEM;
+  }
+  h.key = width;
+  for (int64_t v = 0; v < n; v++) {
+    width[v] = 0;
+    h.pos[v] = -1;
+  }
+  width[src] = INF32;
+  h.heap[0] = src;
+  h.pos[src] = 0;
+  h.size = 1;
+  while (h.size > 0) {
+    uint32_t u = h.heap[0];
+    mheap_swap(&h, 0, h.size - 1);
+    h.size--;
+    h.pos[u] = -1;
+    if (h.size > 0) mheap_down(&h, 0);
+    done[u] = 1;
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      uint32_t v = tgt[e];
+      if (done[v]) continue;
+      uint32_t we = w ? w[e] : 1u;
+      uint32_t cand = width[u] < we ? width[u] : we;
+      if (cand > width[v]) {
+        width[v] = cand;
+        if (h.pos[v] < 0) {
+          h.heap[h.size] = v;
+          h.pos[v] = h.size;
+          h.size++;
+        }
+        mheap_up(&h, h.pos[v]);
+      }
+    }
+  }
+  free(h.heap); free(h.pos); free(done);
+  return ORACLE_OK;
+}
+
+/* Widest-path certificate, O(n+m): (1) width[src] = INF32; (2) no edge can  */
+/* improve: width[v] >= min(width[u], w) for every edge; (3) a BFS from src  */
+/* over tight edges (min(width[u], w) == width[v] > 0) reaches exactly the   */
+/* vertices with width > 0.  (2) gives width >= true width along an optimal */
+/* path; every vertex reached by (3) has width <= true width by induction;  */
+/* so (2)+(3) imply exact widths.                                           */
+int oracle_check_widest(int64_t n, const int64_t *off, const uint32_t *tgt,
+                        const uint32_t *w, uint32_t src, const uint32_t *width,
+                        int64_t *bad) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (width == NULL) return ORACLE_EINVAL;
+  int64_t dummy;
+  if (!bad) bad = &dummy;
+  *bad = -1;
+  if (width[src] != INF32) { *bad = src; return ORACLE_EFAIL; }
+  for (int64_t u = 0; u < n; u++) {
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      uint32_t we = w ? w[e] : 1u;
+      uint32_t cand = width[u] < we ? width[u] : we;
+      if (width[tgt[e]] < cand) { *bad = tgt[e]; return ORACLE_EFAIL; }
+    }
+  }
+  char *seen = (char *)calloc((size_t)n, 1);
+  uint32_t *queue = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+  if (!seen || !queue) { free(seen); free(queue); return ORACLE_ENOMEM; }
+  int64_t head = 0, tail = 0;
+  seen[src] = 1;
+  queue[tail++] = src;
+  while (head < tail) {
+    uint32_t u = queue[head++];
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      uint32_t v = tgt[e];
+      uint32_t we = w ? w[e] : 1u;
+      uint32_t cand = width[u] < we ? width[u] : we;
+      if (!seen[v] && width[v] > 0 && cand == width[v]) {
+        seen[v] = 1;
+        queue[tail++] = v;
+      }
+    }
+  }
+  for (int64_t v = 0; v < n; v++) {
+    if ((width[v] > 0) != (seen[v] != 0)) { *bad = v; free(seen); free(queue); return ORACLE_EFAIL; }
+  }
+  free(seen); free(queue);
+  return ORACLE_OK;
+}

@@ -66,7 +66,6 @@ struct gbbs_graph {
   long long *fo[3] = {nullptr, nullptr, nullptr};
   long long *fb[3] = {nullptr, nullptr, nullptr};
   uint32_t *iso = nullptr;
-  unsigned long long *part = nullptr;
   unsigned long long *cnt = nullptr;  // [4] + ctrl
   int *status = nullptr;
   long long *rounds = nullptr;
@@ -75,7 +74,7 @@ struct gbbs_graph {
   long long dstats_cap = 0;
   unsigned long long *dcount = nullptr;
   long long nwords = 0;
-  int grid[2][2] = {{0, 0}, {0, 0}};  // [algo][stats]
+  int grid[3][2] = {{0, 0}, {0, 0}, {0, 0}};  // [algo][stats]
   cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
@@ -95,7 +94,6 @@ static void free_graph(gbbs_graph *g) {
   }
   cudaFree(g->cnt);
   cudaFree(g->iso);
-  cudaFree(g->part);
   cudaFree(g->tmp_dist);
   cudaFree(g->tmp_parent);
   cudaFree(g->dstats);
@@ -352,10 +350,8 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
   if ((rc = occupancy_grid<ALGO_BFS, true>(&g->grid[0][1]))) return rc;
   if ((rc = occupancy_grid<ALGO_BF, false>(&g->grid[1][0]))) return rc;
   if ((rc = occupancy_grid<ALGO_BF, true>(&g->grid[1][1]))) return rc;
-  int gmax = 0;
-  for (int a = 0; a < 2; a++)
-    for (int b = 0; b < 2; b++) gmax = gmax > g->grid[a][b] ? gmax : g->grid[a][b];
-  CU(cudaMalloc(&g->part, (size_t)gmax * 16));
+  if ((rc = occupancy_grid<ALGO_WP, false>(&g->grid[2][0]))) return rc;
+  if ((rc = occupancy_grid<ALGO_WP, true>(&g->grid[2][1]))) return rc;
   CU(cudaDeviceSynchronize());
   return GBBS_OK;
 }
@@ -531,8 +527,10 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   int rc;
   if (algo == ALGO_BFS)
     rc = want_rounds ? launch<ALGO_BFS, true>(g, p, st, ev0, ev1) : launch<ALGO_BFS, false>(g, p, st, ev0, ev1);
-  else
+  else if (algo == ALGO_BF)
     rc = want_rounds ? launch<ALGO_BF, true>(g, p, st, ev0, ev1) : launch<ALGO_BF, false>(g, p, st, ev0, ev1);
+  else
+    rc = want_rounds ? launch<ALGO_WP, true>(g, p, st, ev0, ev1) : launch<ALGO_WP, false>(g, p, st, ev0, ev1);
   if (rc) return rc;
   if (!dist_dev) CU(cudaMemcpyAsync(dist, ddist, nb, cudaMemcpyDeviceToHost, st));
   if (parent && !par_dev) CU(cudaMemcpyAsync(parent, dpar, nb, cudaMemcpyDeviceToHost, st));
@@ -601,4 +599,13 @@ extern "C" int gbbs_bfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist, ui
 extern "C" int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                                     void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats) {
   return run(g, ALGO_BF, src, dist, nullptr, cuda_stream, opts, stats);
+}
+
+extern "C" int gbbs_widest_path(const gbbs_graph *g, uint32_t src, uint32_t *width, void *cuda_stream) {
+  return run(g, ALGO_WP, src, width, nullptr, cuda_stream, nullptr, nullptr);
+}
+
+extern "C" int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *width,
+                                   void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats) {
+  return run(g, ALGO_WP, src, width, nullptr, cuda_stream, opts, stats);
 }

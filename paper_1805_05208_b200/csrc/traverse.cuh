@@ -51,7 +51,7 @@ constexpr long long HEAVY = 512;      // bitmap-forward: deferred to heavy tiles
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
-enum Algo { ALGO_BFS = 0, ALGO_BF = 1 };
+enum Algo { ALGO_BFS = 0, ALGO_BF = 1, ALGO_WP = 2 };  // WP: widest path, (max, min) semiring
 enum Emit { EMIT_LIST = 0, EMIT_COUNT = 1 };
 enum { LIST_HEAVY = 2 };
 
@@ -340,7 +340,7 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
         fv[pos] = vv[u];
         fo[pos] = o;
         fb[pos] = lo[u] - o;
-      } else if (ALGO == ALGO_BF && i < cnt) {
+      } else if (ALGO != ALGO_BFS && i < cnt) {
         // out-degree-0 vertex: it never enters a frontier; release its TS bit.
         atomicAnd(bits_next + (vv[u] >> 5), ~(1u << (vv[u] & 31)));
       }
@@ -392,18 +392,27 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       }
     }
   } else {
+    // Bellman-Ford: candidate d(u)+w, priority = smaller (atomicMin).
+    // Widest path: candidate min(width(u), w), priority = larger (atomicMax) —
+    // the (max, min) semiring in place of (min, +).
     unsigned long long nd[NCH];
     uint32_t cur[NCH];
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
-      nd[j] = (unsigned long long)uu[j] + ww[j];
-      cur[j] = act[j] ? p.dist[vv[j]] : 0u;
+      nd[j] = (ALGO == ALGO_WP) ? (unsigned long long)min(uu[j], ww[j])
+                                : (unsigned long long)uu[j] + ww[j];
+      cur[j] = act[j] ? p.dist[vv[j]] : (ALGO == ALGO_WP ? INF : 0u);
     }
     bool cand[NCH];
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       cand[j] = false;
-      if (nd[j] < (unsigned long long)cur[j]) {
+      if (ALGO == ALGO_WP) {
+        if (nd[j] > (unsigned long long)cur[j]) {
+          const uint32_t old = atomicMax(p.dist + vv[j], (uint32_t)nd[j]);  // priority-write
+          cand[j] = nd[j] > (unsigned long long)old;
+        }
+      } else if (nd[j] < (unsigned long long)cur[j]) {
         const uint32_t old = atomicMin(p.dist + vv[j], (uint32_t)nd[j]);  // priority-write
         cand[j] = nd[j] < (unsigned long long)old;
       }
@@ -483,7 +492,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
     const long long Bk = valid ? __ldcg(B + k) : 0;
     const uint32_t Uk = valid ? __ldcg(F + k) : 0;
     uint32_t Xk = Uk;
-    if (ALGO == ALGO_BF) Xk = valid ? ld_relaxed(p.dist + Uk) : 0;
+    if (ALGO != ALGO_BFS) Xk = valid ? ld_relaxed(p.dist + Uk) : 0;
     for (long long cs = ts; cs < te; cs += 32 * NCH) {
       uint32_t vv[NCH], ww[NCH], uu[NCH];
       bool act[NCH];
@@ -505,7 +514,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
           uu[j] = __shfl_sync(FULL, Xk, own);
           if (act[j]) {
             vv[j] = ld_stream(p.tgt + bb + e);
-            if (ALGO == ALGO_BF) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
+            if (ALGO != ALGO_BFS) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
           }
         }
       }
@@ -546,7 +555,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
       cnt_h[h] = __popc(__ballot_sync(FULL, o2[h] < te));
       if (o2[h] < te) {
         w.base[kk] = b2[h];
-        w.own[kk] = (ALGO == ALGO_BF) ? ld_relaxed(p.dist + u2[h]) : u2[h];
+        w.own[kk] = (ALGO != ALGO_BFS) ? ld_relaxed(p.dist + u2[h]) : u2[h];
         const long long o = o2[h] - ts;
         w.head[o > 0 ? o : 0] = kk + 1;
       }
@@ -603,7 +612,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
         const long long bb = w.base[kk];
         uu[j] = w.own[kk];
         vv[j] = ld_stream(p.tgt + bb + e);
-        if (ALGO == ALGO_BF) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
+        if (ALGO != ALGO_BFS) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
       }
     }
     apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
@@ -677,7 +686,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
       dg = (int)(__ldg(p.off + v + 1) - a);
     }
     uint32_t x = v;
-    if (ALGO == ALGO_BF) x = dg > 0 ? ld_relaxed(p.dist + v) : 0u;
+    if (ALGO != ALGO_BFS) x = dg > 0 ? ld_relaxed(p.dist + v) : 0u;
     const bool heavy = dg > (int)HEAVY;
     warp_append(p, LIST_HEAVY, p.hcnt + (r & 1), heavy, v, a, dg);
     unsigned med = __ballot_sync(FULL, dg > 32 && !heavy);
@@ -696,7 +705,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
           const int e = cs + 32 * j + lane;
           act[j] = e < ld;
           vv[j] = act[j] ? ld_stream(p.tgt + la + e) : 0;
-          ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? ld_stream(p.wgt + la + e) : 1u) : 0;
+          ww[j] = (ALGO != ALGO_BFS && act[j]) ? (p.wgt ? ld_stream(p.wgt + la + e) : 1u) : 0;
           uu[j] = lx;
         }
         apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
@@ -714,7 +723,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
       for (int j = 0; j < NCH; j++) {
         act[j] = jj + j < mine;
         vv[j] = act[j] ? ld_stream(p.tgt + a + jj + j) : 0;
-        ww[j] = (ALGO == ALGO_BF && act[j]) ? (p.wgt ? ld_stream(p.wgt + a + jj + j) : 1u) : 0;
+        ww[j] = (ALGO != ALGO_BFS && act[j]) ? (p.wgt ? ld_stream(p.wgt + a + jj + j) : 1u) : 0;
         uu[j] = x;
       }
       apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
@@ -930,7 +939,9 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
 
   // a1: per-run init
   for (long long i = gtid; i < p.n; i += gstride) {
-    st_stream(p.dist + i, (i == src) ? 0u : INF);
+    // BFS/BF: 0 at src, INF elsewhere; widest path: INF (empty path) at src, 0 elsewhere
+    if (ALGO == ALGO_WP) st_stream(p.dist + i, (i == src) ? INF : 0u);
+    else st_stream(p.dist + i, (i == src) ? 0u : INF);
     if (ALGO == ALGO_BFS && p.parent) st_stream(p.parent + i, (i == src) ? src : INF);
   }
   for (long long w = gtid; w < p.nwords; w += gstride) {
@@ -1023,7 +1034,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
       }
     } else {  // list push
       uint32_t *bits = (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nb];
-      if (ALGO == ALGO_BF) {
+      if (ALGO != ALGO_BFS) {
         // a11: release the current frontier's TS bits (buffer cb is idle this round)
         uint32_t *cur_bits = p.bm[cb];
         const uint32_t *F = p.fv[cb];

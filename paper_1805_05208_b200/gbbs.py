@@ -23,8 +23,8 @@ GBBS_SYMMETRIC, GBBS_BORROW, GBBS_NO_VALIDATE = 0x1, 0x2, 0x4
 GBBS_MODE_AUTO, GBBS_MODE_SPARSE, GBBS_MODE_DENSE = 0, 1, 2
 
 EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_bfs",
-           "gbbs_bellman_ford", "gbbs_bfs_ex", "gbbs_bellman_ford_ex", "gbbs_default_opts",
-           "gbbs_launch_info", "gbbs_last_error")
+           "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
+           "gbbs_widest_path_ex", "gbbs_default_opts", "gbbs_launch_info", "gbbs_last_error")
 
 
 class GbbsError(RuntimeError):
@@ -65,13 +65,15 @@ def _load():
     lib.gbbs_bellman_ford.argtypes = [p, u32, p, p]
     lib.gbbs_bfs_ex.argtypes = [p, u32, p, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_bellman_ford_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
+    lib.gbbs_widest_path.argtypes = [p, u32, p, p]
+    lib.gbbs_widest_path_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_default_opts.argtypes = [ctypes.POINTER(gbbs_opts)]
     lib.gbbs_default_opts.restype = None
     lib.gbbs_launch_info.argtypes = [p, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     lib.gbbs_last_error.argtypes = []
     lib.gbbs_last_error.restype = ctypes.c_char_p
     for f in ("gbbs_graph_create", "gbbs_graph_info", "gbbs_bfs", "gbbs_bellman_ford", "gbbs_bfs_ex",
-              "gbbs_bellman_ford_ex", "gbbs_launch_info"):
+              "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_launch_info"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -147,6 +149,16 @@ def gbbs_bellman_ford(handle, src, dist, stream=None, opts=None, stats=None):
         _check(lib.gbbs_bellman_ford_ex(handle, int(src), _ptr(dist), st,
                                         ctypes.byref(opts) if opts is not None else None,
                                         ctypes.byref(stats) if stats is not None else None))
+
+
+def gbbs_widest_path(handle, src, width, stream=None, opts=None, stats=None):
+    st = _stream(stream, width)
+    if opts is None and stats is None:
+        _check(lib.gbbs_widest_path(handle, int(src), _ptr(width), st))
+    else:
+        _check(lib.gbbs_widest_path_ex(handle, int(src), _ptr(width), st,
+                                       ctypes.byref(opts) if opts is not None else None,
+                                       ctypes.byref(stats) if stats is not None else None))
 
 
 def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO):
@@ -225,3 +237,6 @@ class Graph:
 
     def bellman_ford(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_bellman_ford(self.handle, src, dist, stream, opts, stats)
+
+    def widest_path(self, src, width, stream=None, opts=None, stats=None):
+        gbbs_widest_path(self.handle, src, width, stream, opts, stats)

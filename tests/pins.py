@@ -125,3 +125,26 @@ def all_small_graphs(n: int):
     pairs = list(itertools.combinations(range(n), 2))
     for mask in range(1 << len(pairs)):
         yield [p for i, p in enumerate(pairs) if mask >> i & 1]
+
+
+def brute_force_widest(n: int, offsets, targets, weights, src: int):
+    """Max over ALL simple src->v paths of the minimum edge weight (n <= 9);
+    width[src] = INF (empty path), unreachable 0 (readings W1/W2)."""
+    adj = {u: [(int(targets[e]), 1 if weights is None else int(weights[e]))
+               for e in range(offsets[u], offsets[u + 1])] for u in range(n)}
+    best = [0] * n
+    best[src] = INF
+
+    def dfs(u, bottleneck, seen):
+        for v, w in adj[u]:
+            if v in seen:
+                continue
+            b = min(bottleneck, w)
+            if b > best[v]:
+                best[v] = b
+            seen.add(v)
+            dfs(v, b, seen)
+            seen.remove(v)
+
+    dfs(src, INF, {src})
+    return np.array(best, np.uint64)

@@ -303,3 +303,55 @@ def test_c1_generator_bit_identical_and_parity(G):
     toff, ttgt = graphgen.torus3d(L)
     o2, t2 = device.torus_csr(L)
     assert (o2.cpu().numpy() == toff).all() and (t2.cpu().numpy().view(np.uint32) == ttgt).all()
+
+
+# ---- NEXT-1 widest path -------------------------------------------------------------
+
+def run_wp(G, g, src, host=False, mode=None):
+    d = np.empty(g.n, np.uint32) if host else torch.empty(g.n, dtype=torch.int32, device="cuda")
+    opts = None if mode is None else G.make_opts(20, {"auto": 0, "sparse": 1, "dense": 2}[mode])
+    g.widest_path(src, d, opts=opts)
+    return d if host else d.cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_widest_random(G, seed):
+    for sym in (True, False):
+        off, tgt = graphgen.random_graph(600, 0.005 * (1 + seed), 40 + seed, symmetric=sym)
+        w = graphgen.pair_weights(off, tgt, seed, 1000)
+        g = G.Graph(off, tgt, w, symmetric=sym)
+        for src in (0, 5, 599):
+            ref = oracle.widest_path(off, tgt, w, src)
+            for mode in ("auto", "dense"):
+                assert (run_wp(G, g, src, mode=mode) == ref).all(), (sym, src, mode)
+        assert (run_wp(G, g, 0, host=True) == oracle.widest_path(off, tgt, w, 0)).all()
+        g.close()
+
+
+def test_widest_spec_examples_and_unit(G):
+    off, tgt, w = graphgen.from_edge_list(3, [(0, 1), (1, 2), (0, 2)], True, [3, 5, 2])
+    g = G.Graph(off, tgt, w, symmetric=True)
+    assert list(run_wp(G, g, 0)) == [0xFFFFFFFF, 3, 3]
+    g.close()
+    off, tgt = graphgen.rmat_graph(14, 1 << 17, 2, 0.57, 0.19, 0.19)
+    g = G.Graph(off, tgt, symmetric=True)            # NULL weights = unit: reached -> 1
+    d = run_wp(G, g, 0)
+    bfs, _ = oracle.bfs(off, tgt, 0)
+    assert ((d == 1) == ((bfs != 0xFFFFFFFF) & (bfs > 0))).all() and d[0] == 0xFFFFFFFF
+    g.close()
+
+
+def test_widest_c1_and_torus(G):
+    cfg = graphgen.CONFIGS["c1"]
+    off, tgt = graphgen.rmat_graph(cfg.levels, 1 << cfg.log_edges, cfg.graph_seed, *cfg.abc)
+    w = graphgen.pair_weights(off, tgt, cfg.weight_seed, 1 << 20)
+    g = G.Graph(off, tgt, w, symmetric=True)
+    assert (run_wp(G, g, 0) == oracle.widest_path(off, tgt, w, 0)).all()
+    g.close()
+    off, tgt = graphgen.torus3d(20)
+    w = graphgen.pair_weights(off, tgt, 7, 24)
+    g = G.Graph(off, tgt, w, symmetric=True)
+    d = run_wp(G, g, 0)
+    assert (d == oracle.widest_path(off, tgt, w, 0)).all()
+    assert oracle.check_widest(off, tgt, w, 0, d)[0]
+    g.close()

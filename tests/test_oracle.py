@@ -279,3 +279,64 @@ def test_c1_oracle_self_consistent():
     f, _ = oracle.frontier_bellman_ford64(off, tgt, w, 0)
     assert (oracle.narrow(f) == dd).all()
     assert oracle.check_sssp(off, tgt, w, 0, dd)[0]
+
+
+# ---- NEXT-1 widest path -----------------------------
+
+from pins import brute_force_widest  # noqa: E402
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_widest_brute_force(seed):
+    n = 8
+    off, tgt = graphgen.random_graph(n, 0.35, 300 + seed, symmetric=seed % 2 == 0)
+    w = graphgen.pair_weights(off, tgt, seed, 20) if seed % 3 else \
+        (np.arange(tgt.shape[0]) % 9 + 1).astype(np.uint32)
+    for src in range(n):
+        ref = brute_force_widest(n, off, tgt, w, src)
+        got = oracle.widest_path(off, tgt, w, src)
+        assert (got.astype(np.uint64) == ref).all()
+        assert oracle.check_widest(off, tgt, w, src, got)[0]
+
+
+def test_widest_closed_forms_and_spec_examples():
+    # SPEC.md:344  path 0-1 (3), 1-2 (5) plus edge 0-2 (2), src=0 -> D[2]=3
+    off, tgt, w = graphgen.from_edge_list(3, [(0, 1), (1, 2), (0, 2)], True, [3, 5, 2])
+    assert list(oracle.widest_path(off, tgt, w, 0)) == [INF, 3, 3]
+    # SPEC.md:345  single edge 0-1 (7) -> D[1]=7
+    off, tgt, w = graphgen.from_edge_list(2, [(0, 1)], True, [7])
+    assert list(oracle.widest_path(off, tgt, w, 0)) == [INF, 7]
+    # weighted path: width = running minimum of the prefix weights
+    n = 60
+    ws = np.random.default_rng(1).integers(1, 100, n - 1)
+    off, tgt, w = graphgen.from_edge_list(n, path_graph(n), True, list(ws))
+    assert (oracle.widest_path(off, tgt, w, 0)[1:] == np.minimum.accumulate(ws)).all()
+    # tree: unique path -> minimum weight along it
+    edges, par, _ = recursive_tree(200, 4)
+    wt = np.random.default_rng(2).integers(1, 50, len(edges))
+    off, tgt, w = graphgen.from_edge_list(200, edges, True, list(wt))
+    exp = np.zeros(200, np.int64)
+    exp[0] = INF
+    for i, (p, c) in enumerate(edges):       # edges are in child order 1..199, parents first
+        exp[c] = min(exp[p], wt[i])
+    assert (oracle.widest_path(off, tgt, w, 0) == exp).all()
+    # constant weight c on a connected graph: every vertex c, src INF; unreachable 0
+    off, tgt = graphgen.from_edge_list(5, [(0, 1), (1, 2), (3, 4)])
+    got = oracle.widest_path(off, tgt, np.full(tgt.shape, 6, np.uint32), 0)
+    assert list(got) == [INF, 6, 6, 0, 0]
+
+
+def test_widest_certificate_rejects_mutations():
+    off, tgt = graphgen.rmat_graph(10, 1 << 13, 8, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 8, 30)
+    wd = oracle.widest_path(off, tgt, w, 0)
+    assert oracle.check_widest(off, tgt, w, 0, wd)[0]
+    reached = np.nonzero((wd > 0) & (wd != INF))[0]
+    for v in reached[:: max(1, reached.size // 12)]:
+        for delta in (-1, 1):
+            w2 = wd.copy(); w2[v] = int(wd[v]) + delta
+            assert not oracle.check_widest(off, tgt, w, 0, w2)[0]
+    # an unreachable pair claiming a width between themselves
+    off, tgt, ww = graphgen.from_edge_list(4, [(0, 1), (2, 3)], True, [5, 9])
+    bad = np.array([INF, 5, 4, 4], np.uint32)
+    assert not oracle.check_widest(off, tgt, ww, 0, bad)[0]
