@@ -168,7 +168,11 @@ int gbbs_widest_path(const gbbs_graph *g, uint32_t src, uint32_t *width,
 typedef struct {
   uint32_t threshold_den; /* T; 0 selects the default 20                  */
   int32_t mode;           /* GBBS_MODE_*                                   */
-  uint32_t reserved[6];   /* must be zero                                  */
+  uint32_t ctas_per_sm;   /* persistent-kernel CTAs per SM; 0 = as many as
+                             are co-resident (default).  Fewer CTAs make
+                             the per-round grid barrier cheaper (many small
+                             rounds) at the cost of latency hiding.        */
+  uint32_t reserved[5];   /* must be zero                                  */
 } gbbs_opts;
 
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */

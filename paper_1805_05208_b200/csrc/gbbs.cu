@@ -58,6 +58,7 @@ struct gbbs_graph {
   uint32_t *wgt = nullptr;
   bool own_off = true, own_tgt = true, own_wgt = true;
   uint32_t *odeg = nullptr;  // out-degrees, directed graphs only
+  uint16_t *shadow = nullptr;  // 16-bit distance shadow (BF / widest path)
   long long *in_off = nullptr;  // alias of off when symmetric
   uint32_t *in_tgt = nullptr;
   // scratch
@@ -84,6 +85,7 @@ static void free_graph(gbbs_graph *g) {
   if (g->own_tgt) cudaFree(g->tgt);
   if (g->own_wgt) cudaFree(g->wgt);
   cudaFree(g->odeg);
+  cudaFree(g->shadow);
   if (g->in_off && g->in_off != g->off) cudaFree(g->in_off);
   if (g->in_tgt && g->in_tgt != g->tgt) cudaFree(g->in_tgt);
   for (int i = 0; i < 3; i++) {
@@ -338,6 +340,7 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
     k_out_degree<<<(unsigned)((n + 255) / 256), 256>>>(g->off, n, g->odeg);
     CU(cudaGetLastError());
   }
+  CU(cudaMalloc(&g->shadow, (size_t)n * 2));
   CU(cudaMalloc(&g->iso, (size_t)g->nwords * 4));
   k_isolated<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->in_off, n, g->nwords, g->iso);
   CU(cudaGetLastError());
@@ -415,11 +418,19 @@ __global__ void k_count_reached(const uint32_t *dist, long long n, unsigned long
 }
 
 template <int ALGO, bool STATS>
-static int launch(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+static int launch(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1,
+                  unsigned ctas_per_sm) {
   void *args[] = {&p};
+  int grid = g->grid[ALGO][STATS];
+  if (ctas_per_sm) {
+    int nsm = 0;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    const long long want = (long long)ctas_per_sm * nsm;
+    if (want < grid) grid = (int)want;
+  }
   if (ev0) CU(cudaEventRecord(ev0, st));
-  CU(cudaLaunchCooperativeKernel((const void *)traverse_kernel<ALGO, STATS>, g->grid[ALGO][STATS],
-                                 BLOCK, args, 0, st));
+  CU(cudaLaunchCooperativeKernel((const void *)traverse_kernel<ALGO, STATS>, grid, BLOCK, args, 0,
+                                 st));
   if (ev1) CU(cudaEventRecord(ev1, st));
   return GBBS_OK;
 }
@@ -436,7 +447,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   if (opts) {
     o = *opts;
     if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 6; i++)
+    for (int i = 0; i < 5; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.mode < 0 || o.mode > 2) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
   }
@@ -505,6 +516,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   p.ebits = g->ebits;
   p.iso = g->iso;
   p.odeg = g->odeg;
+  p.shadow = g->shadow;
   p.symmetric = (g->flags & GBBS_SYMMETRIC) ? 1 : 0;
   p.mode = o.mode;
   p.src = src;
@@ -526,11 +538,11 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   }
   int rc;
   if (algo == ALGO_BFS)
-    rc = want_rounds ? launch<ALGO_BFS, true>(g, p, st, ev0, ev1) : launch<ALGO_BFS, false>(g, p, st, ev0, ev1);
+    rc = want_rounds ? launch<ALGO_BFS, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_BFS, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
   else if (algo == ALGO_BF)
-    rc = want_rounds ? launch<ALGO_BF, true>(g, p, st, ev0, ev1) : launch<ALGO_BF, false>(g, p, st, ev0, ev1);
+    rc = want_rounds ? launch<ALGO_BF, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_BF, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
   else
-    rc = want_rounds ? launch<ALGO_WP, true>(g, p, st, ev0, ev1) : launch<ALGO_WP, false>(g, p, st, ev0, ev1);
+    rc = want_rounds ? launch<ALGO_WP, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_WP, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
   if (rc) return rc;
   if (!dist_dev) CU(cudaMemcpyAsync(dist, ddist, nb, cudaMemcpyDeviceToHost, st));
   if (parent && !par_dev) CU(cudaMemcpyAsync(parent, dpar, nb, cudaMemcpyDeviceToHost, st));

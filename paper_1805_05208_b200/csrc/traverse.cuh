@@ -78,6 +78,7 @@ struct Params {
   const uint32_t *iso;       // [nwords] isolated-vertex (+padding) mask
   const uint32_t *odeg;      // out-degrees (directed graphs; nullptr if symmetric)
   uint32_t *dist;            // [n]
+  uint16_t *shadow;          // [n] BF/WP: 16-bit conservative copy of dist
   uint32_t *parent;          // [n] or nullptr
   uint32_t *bm[2];           // BFS: visited (double-buffered); BF: frontier TS bits
   uint32_t *fv[3];           // lists 0/1 (rounds) and 2 (heavy): vertex
@@ -396,27 +397,36 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     // Widest path: candidate min(width(u), w), priority = larger (atomicMax) —
     // the (max, min) semiring in place of (min, +).
     unsigned long long nd[NCH];
+    // Pre-check against the 16-bit shadow of dist (half the bytes of dist, meant
+    // to stay in L2): BF keeps shadow >= min(dist, 0xFFFF) because distances only
+    // fall and the shadow only ever receives values dist held; WP keeps
+    // shadow <= width.  A relaxation the shadow proves useless is skipped; the
+    // others go straight to the priority-write, whose returned old value decides.
     uint32_t cur[NCH];
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       nd[j] = (ALGO == ALGO_WP) ? (unsigned long long)min(uu[j], ww[j])
                                 : (unsigned long long)uu[j] + ww[j];
-      cur[j] = act[j] ? p.dist[vv[j]] : (ALGO == ALGO_WP ? INF : 0u);
+      cur[j] = act[j] ? (uint32_t)p.shadow[vv[j]] : (ALGO == ALGO_WP ? 0xFFFFu : 0u);
     }
     bool cand[NCH];
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       cand[j] = false;
+      if (!act[j]) continue;
       if (ALGO == ALGO_WP) {
         if (nd[j] > (unsigned long long)cur[j]) {
           const uint32_t old = atomicMax(p.dist + vv[j], (uint32_t)nd[j]);  // priority-write
           cand[j] = nd[j] > (unsigned long long)old;
         }
-      } else if (nd[j] < (unsigned long long)cur[j]) {
+      } else if (nd[j] < (unsigned long long)cur[j] || cur[j] == 0xFFFFu) {
         const uint32_t old = atomicMin(p.dist + vv[j], (uint32_t)nd[j]);  // priority-write
         cand[j] = nd[j] < (unsigned long long)old;
       }
     }
+#pragma unroll
+    for (int j = 0; j < NCH; j++)
+      if (cand[j]) p.shadow[vv[j]] = (uint16_t)min(nd[j], 0xFFFFull);
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       win[j] = false;
@@ -468,18 +478,26 @@ template <int ALGO, bool STATS, int EMIT>
 __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, WarpState &ws,
                                                int lb, long long i0, long long t, long long f,
                                                long long E, int nb, int r, uint32_t *bits,
-                                               const uint32_t *prebits) {
+                                               const uint32_t *prebits, int TR) {
   constexpr long long BIG = 0x7FFFFFFFFFFFFFFFll;
   const int lane = threadIdx.x & 31;
-  const long long ts = t * TE;
-  const long long te = min(ts + (long long)TE, E);
+  const long long ts = t * TR;
+  const long long te = min(ts + (long long)TR, E);
   const long long *O = p.fo[lb];
   const long long *B = p.fb[lb];
   const uint32_t *F = p.fv[lb];
   if (STATS && lane == 0) ws.edges += (unsigned long long)(te - ts);
 
   const long long k = i0 + lane;
-  long long Ok = k < f ? __ldcg(O + k) : BIG;
+  // O, base and vertex of the next 32 entries are loaded together (the base and
+  // vertex speculatively), so the owner set costs one round trip
+  long long Ok = BIG, Bk = 0;
+  uint32_t Uk = 0;
+  if (k < f) {
+    Ok = __ldcg(O + k);
+    Bk = __ldcg(B + k);
+    Uk = __ldcg(F + k);
+  }
   const unsigned inb = __ballot_sync(FULL, Ok < te);  // owners with an edge in the tile
   const int n32 = __popc(inb);
   if (n32 < 32) {
@@ -489,8 +507,6 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
     const long long onext = __shfl_sync(FULL, Ok, n32);
     const bool valid = lane < n32;
     if (!valid) Ok = BIG;
-    const long long Bk = valid ? __ldcg(B + k) : 0;
-    const uint32_t Uk = valid ? __ldcg(F + k) : 0;
     uint32_t Xk = Uk;
     if (ALGO != ALGO_BFS) Xk = valid ? ld_relaxed(p.dist + Uk) : 0;
     for (long long cs = ts; cs < te; cs += 32 * NCH) {
@@ -540,10 +556,11 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const long long kk = i0 + kb + 32 * h + lane;
-      o2[h] = kk < f ? __ldcg(O + kk) : BIG;
+      o2[h] = BIG;
       b2[h] = 0;
       u2[h] = 0;
-      if (o2[h] < te) {
+      if (kk < f) {
+        o2[h] = __ldcg(O + kk);
         b2[h] = __ldcg(B + kk);
         u2[h] = __ldcg(F + kk);
       }
@@ -894,14 +911,19 @@ template <int ALGO, bool STATS, int EMIT>
 __device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpState &ws, int lb,
                                            long long f, long long E, int nb, int r, uint32_t *bits,
                                            const uint32_t *prebits, long long gw, long long nw) {
+  // Tile size: TE, or smaller (power of two >= 32) when the round has fewer than
+  // TE edges per warp, so a small round costs each warp a single batch.
+  int TR = TE;
+  while (TR > 32 && (E + TR / 2 - 1) / (TR / 2) <= nw) TR >>= 1;
   // contiguous blocks of tiles per warp: one owner search per warp and round
-  const long long ntiles = (E + TE - 1) / TE;
+  const long long ntiles = (E + TR - 1) / TR;
   const long long per = (ntiles + nw - 1) / nw;
   long long t = gw * per;
   const long long t1 = min(t + per, ntiles);
   if (t >= t1) return;
-  long long i0 = warp_upper(p.fo[lb], 0, f, t * TE);
-  for (; t < t1; t++) i0 = push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, i0, t, f, E, nb, r, bits, prebits);
+  long long i0 = warp_upper(p.fo[lb], 0, f, t * TR);
+  for (; t < t1; t++)
+    i0 = push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, i0, t, f, E, nb, r, bits, prebits, TR);
 }
 
 template <int ALGO, bool STATS, int EMIT>
@@ -940,8 +962,13 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
   // a1: per-run init
   for (long long i = gtid; i < p.n; i += gstride) {
     // BFS/BF: 0 at src, INF elsewhere; widest path: INF (empty path) at src, 0 elsewhere
-    if (ALGO == ALGO_WP) st_stream(p.dist + i, (i == src) ? INF : 0u);
-    else st_stream(p.dist + i, (i == src) ? 0u : INF);
+    if (ALGO == ALGO_WP) {
+      st_stream(p.dist + i, (i == src) ? INF : 0u);
+      p.shadow[i] = (i == src) ? 0xFFFFu : 0u;
+    } else {
+      st_stream(p.dist + i, (i == src) ? 0u : INF);
+      if (ALGO == ALGO_BF) p.shadow[i] = (i == src) ? 0u : 0xFFFFu;
+    }
     if (ALGO == ALGO_BFS && p.parent) st_stream(p.parent + i, (i == src) ? src : INF);
   }
   for (long long w = gtid; w < p.nwords; w += gstride) {

@@ -35,7 +35,7 @@ class GbbsError(RuntimeError):
 
 class gbbs_opts(ctypes.Structure):
     _fields_ = [("threshold_den", ctypes.c_uint32), ("mode", ctypes.c_int32),
-                ("reserved", ctypes.c_uint32 * 6)]
+                ("ctas_per_sm", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 5)]
 
 
 class gbbs_round_stat(ctypes.Structure):
@@ -161,11 +161,12 @@ def gbbs_widest_path(handle, src, width, stream=None, opts=None, stats=None):
                                        ctypes.byref(stats) if stats is not None else None))
 
 
-def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO):
+def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0):
     o = gbbs_opts()
     lib.gbbs_default_opts(ctypes.byref(o))
     o.threshold_den = threshold_den
     o.mode = mode
+    o.ctas_per_sm = ctas_per_sm
     return o
 
 

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--mode", default="auto")
     ap.add_argument("--T", type=int, default=20)
     ap.add_argument("--src", type=int, default=0, help="index into the config's sources")
+    ap.add_argument("--ctas", type=int, default=0, help="CTAs per SM (0 = max)")
     a = ap.parse_args()
     import torch
     from graphgen import device as gdev
@@ -26,7 +27,7 @@ def main():
     g = gbbs.Graph(G["offsets"], G["targets"], G["weights"], symmetric=G["symmetric"])
     d = torch.empty(G["n"], dtype=torch.int32, device="cuda")
     p = torch.empty_like(d)
-    opts = gbbs.make_opts(a.T, {"auto": 0, "sparse": 1, "dense": 2}[a.mode])
+    opts = gbbs.make_opts(a.T, {"auto": 0, "sparse": 1, "dense": 2}[a.mode], a.ctas)
     s = G["sources"][a.src]
     for _ in range(a.reps):
         st = gbbs.make_stats(0)
