@@ -350,6 +350,25 @@ def run_ours(args, rank, world, local):
                 "roofline_frac": round(walg / (wkms * 1e-3) / 1e9 / peak, 4),
                 "note": "NEXT-1: Bellman-Ford over the (max, min) semiring, same graph and weights",
                 "rounds": [per_src[("wp", s)]["rounds"] for s in sources]}
+        if want_w and args.algo == "bfs" and not args.profile:
+            # NEXT-3: single-source betweenness on the same graph (8 sources per step)
+            delta = torch.empty(n, dtype=torch.float64, device=dev)
+            for s in sources[:2]:
+                g.betweenness(s, delta)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush_buf.fill_(1)
+            e0.record(stream)
+            for s in sources:
+                g.betweenness(s, delta, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            bt = e0.elapsed_time(e1)
+            out["betweenness"] = {
+                "value": round(edges_step / (bt * 1e-3) / 1e9, 3),
+                "unit": "GTEPS (m_reach of the BFS per source / time)",
+                "ms_per_step": round(bt, 4),
+                "note": "NEXT-3: Brandes dependencies, forward CAS + fp64 fetch-and-add, backward per level"}
         if not args.profile:
             out["cpu_baseline"] = cpu_baseline(args, G["offsets"], G["targets"], sources, cfg)
     g.close()

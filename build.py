@@ -22,6 +22,7 @@ PRODUCT = dict(
     out=os.path.join(ROOT, "paper_1805_05208_b200", "libgbbs.so"),
     srcs=[os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "gbbs.cu")],
     deps=[os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "traverse.cuh"),
+          os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "bc.cuh"),
           os.path.join(ROOT, "include", "gbbs.h")],
 )
 GEN = dict(

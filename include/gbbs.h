@@ -154,6 +154,26 @@ int gbbs_bellman_ford(const gbbs_graph *g, uint32_t src, uint32_t *dist,
 int gbbs_widest_path(const gbbs_graph *g, uint32_t src, uint32_t *width,
                      void *cuda_stream);
 
+/*
+ * gbbs_betweenness — single-source betweenness contributions (P:98-101,
+ * sec:algs; output spec P:1493-1496): delta[v] = sum over t != src, v of
+ * sigma_st(v) / sigma_st, Brandes' dependency of src on v, following
+ * out-edges (the paper's input is undirected; pass a symmetric CSR).  The
+ * forward pass counts shortest paths with an atomicCAS test-and-set on the
+ * level and an fp64 fetch-and-add on sigma; the backward pass accumulates
+ * delta level by level.  delta[src] = 0 and unreached vertices get 0
+ * (reading B1).
+ *
+ * delta   double[n], caller-owned, host or device.  fp64 accumulation in a
+ *         nondeterministic order: results agree with a sequential Brandes to
+ *         rounding (DESIGN.md tolerance), not bit for bit.
+ * Errors: GBBS_EINVAL (g or delta NULL, src >= n), GBBS_ENOMEM (scratch:
+ *         12n + 24*levels bytes on first use), GBBS_ECUDA, GBBS_EINTERNAL
+ *         (more than 2^22 BFS levels).
+ */
+int gbbs_betweenness(const gbbs_graph *g, uint32_t src, double *delta,
+                     void *cuda_stream);
+
 /* ---- extended calls (bench / tests) ------------------------------------ */
 
 /* Representation choice per round (threshold rule reading A10).
@@ -218,6 +238,9 @@ int gbbs_bfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
 int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                          void *cuda_stream, const gbbs_opts *opts,
                          gbbs_stats *stats);
+int gbbs_betweenness_ex(const gbbs_graph *g, uint32_t src, double *delta,
+                        void *cuda_stream, const gbbs_opts *opts,
+                        gbbs_stats *stats);
 int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *width,
                         void *cuda_stream, const gbbs_opts *opts,
                         gbbs_stats *stats);

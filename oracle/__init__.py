@@ -208,3 +208,17 @@ def check_widest(offsets, targets, weights, src, width):
     if rc not in (OK, EFAIL):
         raise RuntimeError(f"oracle_check_widest rc={rc}")
     return rc == OK, bad.value
+
+
+def betweenness(offsets, targets, src, want_sigma=False):
+    """Brandes single-source dependencies delta_src (float64); reading B1:
+    delta[src] = 0, unreached 0.  Returns (delta, sigma or None)."""
+    n, off, tgt, _ = _csr(offsets, targets)
+    delta = np.empty(n, np.float64)
+    sigma = np.empty(n, np.float64) if want_sigma else None
+    lib = _load()
+    lib.oracle_bc.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
+                              ctypes.c_void_p, ctypes.c_void_p]
+    lib.oracle_bc.restype = ctypes.c_int
+    _check(lib.oracle_bc(n, _ptr(off), _ptr(tgt), int(src), _ptr(delta), _ptr(sigma)), "oracle_bc")
+    return delta, sigma

@@ -522,3 +522,61 @@ int oracle_check_widest(int64_t n, const int64_t *off, const uint32_t *tgt,
   free(seen); free(queue);
   return ORACLE_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Single-source betweenness contributions, PAPER.md:98-101 (sec:algs) and   */
+/* the output spec PAPER.md:1493-1496: S[v] = contribution to v's centrality */
+/* from all (src, t) shortest paths through v = Brandes' dependency          */
+/* delta_src(v) = sum_{t != src, v} sigma_st(v) / sigma_st.  Textbook        */
+/* Brandes: BFS from src counting shortest paths sigma (double), then        */
+/* vertices in reverse BFS order accumulate                                  */
+/* delta[v] = sum_{v->w, d[w] = d[v]+1} sigma[v]/sigma[w] * (1 + delta[w]).   */
+/* Reading B1: endpoints are excluded, so delta[src] = 0 and     */
+/* unreached vertices get 0.  sigma may be NULL.                             */
+/* ------------------------------------------------------------------------ */
+int oracle_bc(int64_t n, const int64_t *off, const uint32_t *tgt, uint32_t src,
+              double *delta, double *sigma_out) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (delta == NULL) return ORACLE_EINVAL;
+  uint32_t *order = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+  uint32_t *d = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+  double *sigma = (double *)calloc((size_t)n, sizeof(double));
+  if (!order || !d || !sigma) {
+    free(order); free(d); free(sigma);
+    return ORACLE_ENOMEM;
+  }
+  for (int64_t v = 0; v < n; v++) {
+    d[v] = INF32;
+    delta[v] = 0.0;
+  }
+  int64_t head = 0, tail = 0;
+  d[src] = 0;
+  sigma[src] = 1.0;
+  order[tail++] = src;
+  while (head < tail) {
+    uint32_t u = order[head++];
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      uint32_t v = tgt[e];
+      if (d[v] == INF32) {
+        d[v] = d[u] + 1;
+        order[tail++] = v;
+      }
+      if (d[v] == d[u] + 1) sigma[v] += sigma[u];
+    }
+  }
+  for (int64_t i = tail - 1; i >= 0; i--) {
+    uint32_t v = order[i];
+    double acc = 0.0;
+    for (int64_t e = off[v]; e < off[v + 1]; e++) {
+      uint32_t w = tgt[e];
+      if (d[w] == d[v] + 1) acc += sigma[v] / sigma[w] * (1.0 + delta[w]);
+    }
+    delta[v] = acc;
+  }
+  delta[src] = 0.0;
+  if (sigma_out)
+    for (int64_t v = 0; v < n; v++) sigma_out[v] = sigma[v];
+  free(order); free(d); free(sigma);
+  return ORACLE_OK;
+}

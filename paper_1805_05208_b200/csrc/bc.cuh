@@ -1,0 +1,313 @@
+// bc.cuh — single-source betweenness contributions (NEXT-3), one persistent
+// cooperative kernel per call.
+//
+// PAPER.md:98-101 (sec:algs): "It uses fetch-and-add to compute the total number
+// of shortest-paths through vertices"; output spec PAPER.md:1493-1496: for every
+// v, the contribution to v's centrality from all (src, t) shortest paths through
+// v — Brandes' dependency delta_src(v).
+//
+//  forward  level r -> r+1 over the level-r vertex list (edge tiles as in the
+//           list push of traverse.cuh): for edge (u, v) the test-and-set is an
+//           atomicCAS(dist[v], INF, r+1) whose returned value also says whether
+//           v lies on level r+1 (won or lost to a same-level writer), and the
+//           fetch-and-add is atomicAdd(sigma[v], sigma[u]) in fp64.  Winners are
+//           appended to a cumulative level queue (all levels kept, in order).
+//  backward levels L-1 .. 1: for every edge (u, v) of a level-l vertex u with
+//           dist[v] = l+1, delta[u] += sigma[u] / sigma[v] * (1 + delta[v])
+//           (Brandes' recurrence), a grid barrier between levels.
+// delta[src] = 0 and unreached vertices keep 0 (reading B1).
+#pragma once
+
+#include "traverse.cuh"
+
+namespace gbbs_dev {
+
+struct BcParams {
+  long long n, m;
+  const long long *off;
+  const uint32_t *tgt;
+  uint32_t *dist;            // [n] level of each vertex (INF = unreached)
+  double *sigma;             // [n] shortest-path counts
+  double *delta;             // [n] output
+  uint32_t *qv;              // cumulative level queue: vertex
+  long long *qo;             //   exclusive edge prefix O within its level
+  long long *qb;             //   base = offset(v) - O
+  long long *lvl;            // [3 * lvl_cap]: start, count, edges per level
+  long long lvl_cap;
+  unsigned long long *cnt;   // packed (count << ebits | edges) ring [4]
+  int *status;
+  long long *rounds_out;
+  int ebits;
+  uint32_t src;
+};
+
+struct BcWarpSmem {
+  alignas(16) int32_t head[TE];
+  long long base[TE + 1];
+  uint32_t own[TE + 1];
+  uint32_t stage[WCAP];
+};
+
+struct BcSmem {
+  BcWarpSmem w[NWARPS];
+  unsigned long long cnt;
+};
+
+// Append staged vertices (all with out-degree > 0 are kept) to the next level.
+__device__ __forceinline__ void bc_flush(const BcParams &p, const uint32_t *st, int cnt,
+                                         long long qbase, unsigned long long *ctr) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  long long Kl = 0, Dl = 0;
+  for (int i = lane; i < cnt; i += 32) {
+    const uint32_t v = st[i];
+    const long long dg = __ldg(p.off + v + 1) - __ldg(p.off + v);
+    Kl += dg > 0;
+    Dl += dg;
+  }
+  const unsigned long long K = warp_sum64(Kl), D = warp_sum64(Dl);
+  unsigned long long old = 0;
+  if (lane == 0 && K) old = atomicAdd(ctr, (K << p.ebits) | D);
+  old = __shfl_sync(FULL, old, 0);
+  unsigned long long k = old >> p.ebits, d = old & ((1ull << p.ebits) - 1);
+  for (int b0 = 0; b0 < cnt; b0 += 32) {
+    const int i = b0 + lane;
+    uint32_t v = 0;
+    long long a = 0, deg = 0;
+    if (i < cnt) {
+      v = st[i];
+      a = __ldg(p.off + v);
+      deg = __ldg(p.off + v + 1) - a;
+    }
+    const bool keep = deg > 0;
+    const unsigned bal = __ballot_sync(FULL, keep);
+    const long long dex = warp_excl_sum64(deg, lane);
+    if (keep) {
+      const unsigned long long pos = qbase + k + __popc(bal & lanemask_lt());
+      const long long o = (long long)d + dex;
+      p.qv[pos] = v;
+      p.qo[pos] = o;
+      p.qb[pos] = a - o;
+    }
+    k += __popc(bal);
+    d += (unsigned long long)__shfl_sync(FULL, dex + deg, 31);
+  }
+  __syncwarp();
+}
+
+// One warp tile of level-l edges: owners staged in shared memory (1 + index at
+// the slot of each owner's first in-tile edge, expanded by a warp max-scan).
+// BACK = false: forward (CAS + sigma fetch-and-add, stage winners);
+// BACK = true : backward (accumulate delta of the owners).
+template <bool BACK>
+__device__ __forceinline__ long long bc_tile(const BcParams &p, BcWarpSmem &w, int &scnt,
+                                             const uint32_t *F, const long long *O,
+                                             const long long *B, long long f, long long E,
+                                             long long i0, long long t, int l, long long qnext,
+                                             unsigned long long *ctr) {
+  constexpr long long BIG = 0x7FFFFFFFFFFFFFFFll;
+  const int lane = threadIdx.x & 31;
+  const long long ts = t * TE;
+  const long long te = min(ts + (long long)TE, E);
+  {
+    int4 *h4 = reinterpret_cast<int4 *>(w.head);
+#pragma unroll
+    for (int q = 0; q < TE / 128; q++) h4[q * 32 + lane] = make_int4(0, 0, 0, 0);
+  }
+  __syncwarp();
+  int nown = 0;
+  long long onext = BIG;
+  for (int kb = 0;; kb += 32) {
+    const long long kk = i0 + kb + lane;
+    long long o = BIG, b = 0;
+    uint32_t u = 0;
+    if (kk < f) {
+      o = __ldcg(O + kk);
+      b = __ldcg(B + kk);
+      u = __ldcg(F + kk);
+    }
+    const int c = __popc(__ballot_sync(FULL, o < te));
+    if (o < te) {
+      w.base[kb + lane] = b;
+      w.own[kb + lane] = u;
+      const long long r = o - ts;
+      w.head[r > 0 ? r : 0] = kb + lane + 1;
+    }
+    nown += c;
+    if (c < 32) {
+      onext = __shfl_sync(FULL, o, c);
+      break;
+    }
+  }
+  __syncwarp();
+  {
+    constexpr int PER = TE / 32;
+    int32_t a[PER];
+    const int4 *h4 = reinterpret_cast<const int4 *>(w.head + lane * PER);
+#pragma unroll
+    for (int q = 0; q < PER / 4; q++) {
+      const int4 x = h4[q];
+      a[4 * q] = x.x; a[4 * q + 1] = x.y; a[4 * q + 2] = x.z; a[4 * q + 3] = x.w;
+    }
+#pragma unroll
+    for (int q = 1; q < PER; q++) a[q] = max(a[q], a[q - 1]);
+    int32_t inc = a[PER - 1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc = max(inc, y);
+    }
+    int32_t ex = __shfl_up_sync(FULL, inc, 1);
+    if (lane == 0) ex = 0;
+    int4 *o4 = reinterpret_cast<int4 *>(w.head + lane * PER);
+#pragma unroll
+    for (int q = 0; q < PER / 4; q++)
+      o4[q] = make_int4(max(ex, a[4 * q]), max(ex, a[4 * q + 1]), max(ex, a[4 * q + 2]),
+                        max(ex, a[4 * q + 3]));
+  }
+  __syncwarp();
+  const uint32_t nl = (uint32_t)(l + 1);
+  for (long long cs = ts; cs < te; cs += 32 * NCH) {
+    uint32_t vv[NCH], uu[NCH];
+    bool act[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      const long long e = cs + 32 * j + lane;
+      act[j] = e < te;
+      vv[j] = 0;
+      uu[j] = 0;
+      if (act[j]) {
+        const int kk = w.head[e - ts] - 1;
+        uu[j] = w.own[kk];
+        vv[j] = ld_stream(p.tgt + w.base[kk] + e);
+      }
+    }
+    if (!BACK) {
+      bool win[NCH];
+#pragma unroll
+      for (int j = 0; j < NCH; j++) {
+        win[j] = false;
+        if (!act[j]) continue;
+        uint32_t cur = p.dist[vv[j]];
+        bool same = cur == nl;
+        if (cur == INF) {
+          const uint32_t old = atomicCAS(p.dist + vv[j], INF, nl);  // test-and-set
+          win[j] = old == INF;
+          same = win[j] || old == nl;
+        }
+        if (same) atomicAdd(p.sigma + vv[j], p.sigma[uu[j]]);  // fetch-and-add
+      }
+#pragma unroll
+      for (int j = 0; j < NCH; j++) {
+        const unsigned b = __ballot_sync(FULL, win[j]);
+        if (win[j]) w.stage[scnt + __popc(b & lanemask_lt())] = vv[j];
+        scnt += __popc(b);
+      }
+      if (scnt > WCAP - 32 * NCH) {
+        bc_flush(p, w.stage, scnt, qnext, ctr);
+        scnt = 0;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NCH; j++) {
+        double c = 0.0;
+        if (act[j] && p.dist[vv[j]] == nl)
+          c = p.sigma[uu[j]] / p.sigma[vv[j]] * (1.0 + p.delta[vv[j]]);
+        const unsigned same = __match_any_sync(FULL, act[j] ? uu[j] : INF);
+        if (same == FULL) {  // one owner for the whole chunk (a hub): reduce first
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+          if (lane == 0 && c != 0.0) atomicAdd(p.delta + uu[j], c);
+        } else if (c != 0.0) {
+          atomicAdd(p.delta + uu[j], c);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  return onext == te ? i0 + nown : i0 + nown - 1;
+}
+
+template <bool BACK>
+__device__ __forceinline__ void bc_level(const BcParams &p, BcWarpSmem &w, int &scnt,
+                                         long long start, long long f, long long E, int l,
+                                         long long qnext, unsigned long long *ctr, long long gw,
+                                         long long nw) {
+  const uint32_t *F = p.qv + start;
+  const long long *O = p.qo + start;
+  const long long *B = p.qb + start;
+  const long long ntiles = (E + TE - 1) / TE;
+  const long long per = (ntiles + nw - 1) / nw;
+  long long t = gw * per;
+  const long long t1 = min(t + per, ntiles);
+  if (t >= t1) return;
+  long long i0 = warp_upper(O, 0, f, t * TE);
+  for (; t < t1; t++) i0 = bc_tile<BACK>(p, w, scnt, F, O, B, f, E, i0, t, l, qnext, ctr);
+}
+
+__global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
+  __shared__ BcSmem s;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const long long gtid = (long long)blockIdx.x * BLOCK + tid;
+  const long long gstride = (long long)gridDim.x * BLOCK;
+  const long long gw = (long long)blockIdx.x * NWARPS + warp;
+  const long long nw = (long long)gridDim.x * NWARPS;
+  const uint32_t src = p.src;
+  BcWarpSmem &w = s.w[warp];
+
+  for (long long i = gtid; i < p.n; i += gstride) {
+    p.dist[i] = (i == src) ? 0u : INF;
+    p.sigma[i] = (i == src) ? 1.0 : 0.0;
+    p.delta[i] = 0.0;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    const long long a = p.off[src], d0 = p.off[src + 1] - a;
+    p.cnt[1] = p.cnt[2] = p.cnt[3] = 0;
+    if (d0 > 0) {
+      p.qv[0] = src;
+      p.qo[0] = 0;
+      p.qb[0] = a;
+      p.cnt[0] = (1ull << p.ebits) | (unsigned long long)d0;
+    } else {
+      p.cnt[0] = 0;
+    }
+    *p.status = 0;
+  }
+  grid.sync();
+
+  const unsigned long long emask = (1ull << p.ebits) - 1;
+  long long start = 0;  // queue position of the current level
+  int l = 0;
+  for (;; l++) {
+    if (tid == 0) s.cnt = ld_relaxed64(p.cnt + (l & 3));
+    __syncthreads();
+    const long long f = (long long)(s.cnt >> p.ebits), E = (long long)(s.cnt & emask);
+    if (f == 0) break;
+    if (l >= p.lvl_cap) {
+      if (blockIdx.x == 0 && tid == 0) *p.status = 1;
+      break;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      p.cnt[(l + 2) & 3] = 0;
+      p.lvl[3 * l] = start;
+      p.lvl[3 * l + 1] = f;
+      p.lvl[3 * l + 2] = E;
+    }
+    int scnt = 0;
+    bc_level<false>(p, w, scnt, start, f, E, l, start + f, p.cnt + ((l + 1) & 3), gw, nw);
+    if (scnt > 0) bc_flush(p, w.stage, scnt, start + f, p.cnt + ((l + 1) & 3));
+    start += f;
+    grid.sync();
+  }
+  const int L = l;  // levels with a non-empty list: 0 .. L-1
+  for (int b = L - 1; b >= 1; b--) {
+    const long long st0 = p.lvl[3 * b], f = p.lvl[3 * b + 1], E = p.lvl[3 * b + 2];
+    int scnt = 0;
+    bc_level<true>(p, w, scnt, st0, f, E, b, 0, nullptr, gw, nw);
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && tid == 0) *p.rounds_out = L;
+}
+
+}  // namespace gbbs_dev

@@ -10,6 +10,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdarg>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <string>
 
@@ -77,7 +78,10 @@ struct gbbs_graph {
   long long nwords = 0;
   int grid[3][2] = {{0, 0}, {0, 0}, {0, 0}};  // [algo][stats]
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  struct BcScratch *bc = nullptr;  // betweenness scratch (lazy)
 };
+
+static void free_bc(gbbs_graph *g);
 
 static void free_graph(gbbs_graph *g) {
   if (!g) return;
@@ -101,6 +105,7 @@ static void free_graph(gbbs_graph *g) {
   cudaFree(g->dstats);
   if (g->ev[0]) cudaEventDestroy(g->ev[0]);
   if (g->ev[1]) cudaEventDestroy(g->ev[1]);
+  free_bc(g);
   delete g;
 }
 
@@ -620,4 +625,121 @@ extern "C" int gbbs_widest_path(const gbbs_graph *g, uint32_t src, uint32_t *wid
 extern "C" int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *width,
                                    void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats) {
   return run(g, ALGO_WP, src, width, nullptr, cuda_stream, opts, stats);
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-3: single-source betweenness contributions (bc.cuh)
+// ---------------------------------------------------------------------------
+#include "bc.cuh"
+
+struct BcScratch {
+  uint32_t *dist = nullptr;
+  double *sigma = nullptr, *delta = nullptr;
+  long long *lvl = nullptr;
+  long long lvl_cap = 0;
+  int grid = 0;
+};
+
+static BcScratch *bc_scratch(gbbs_graph *g, int *rc) {
+  static thread_local std::string dummy;
+  if (g->bc) return g->bc;
+  BcScratch *b = new (std::nothrow) BcScratch();
+  *rc = GBBS_ENOMEM;
+  if (!b) return nullptr;
+  b->lvl_cap = g->n + 1 < (1ll << 22) ? g->n + 1 : (1ll << 22);
+  bool ok = cudaMalloc(&b->dist, (size_t)g->n * 4) == cudaSuccess &&
+            cudaMalloc(&b->sigma, (size_t)g->n * 8) == cudaSuccess &&
+            cudaMalloc(&b->delta, (size_t)g->n * 8) == cudaSuccess &&
+            cudaMalloc(&b->lvl, (size_t)b->lvl_cap * 24) == cudaSuccess;
+  int dev = 0, nsm = 0, per = 0;
+  ok = ok && cudaGetDevice(&dev) == cudaSuccess &&
+       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bc_kernel, BLOCK, 0) == cudaSuccess &&
+       per > 0;
+  if (!ok) {
+    cudaFree(b->dist); cudaFree(b->sigma); cudaFree(b->delta); cudaFree(b->lvl);
+    delete b;
+    cudaGetLastError();
+    fail(GBBS_ENOMEM, "betweenness scratch allocation failed");
+    return nullptr;
+  }
+  b->grid = per * nsm;
+  g->bc = b;
+  *rc = GBBS_OK;
+  return b;
+}
+
+static void free_bc(gbbs_graph *g) {
+  if (!g->bc) return;
+  cudaFree(g->bc->dist); cudaFree(g->bc->sigma); cudaFree(g->bc->delta); cudaFree(g->bc->lvl);
+  delete g->bc;
+  g->bc = nullptr;
+}
+
+extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *delta,
+                                   void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats) {
+  g_last_error.clear();
+  if (!cg_) return fail(GBBS_EINVAL, "g is NULL");
+  gbbs_graph *g = const_cast<gbbs_graph *>(cg_);
+  if (!delta) return fail(GBBS_EINVAL, "delta is NULL");
+  if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
+  if (opts)
+    for (int i = 0; i < 5; i++)
+      if (opts->reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
+  int rc = GBBS_OK;
+  BcScratch *b = bc_scratch(g, &rc);
+  if (!b) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const bool dev_out = is_device_ptr(delta);
+  BcParams p;
+  memset(&p, 0, sizeof p);
+  p.n = g->n;
+  p.m = g->m;
+  p.off = g->off;
+  p.tgt = g->tgt;
+  p.dist = b->dist;
+  p.sigma = b->sigma;
+  p.delta = dev_out ? delta : b->delta;
+  p.qv = g->fv[0];
+  p.qo = g->fo[0];
+  p.qb = g->fb[0];
+  p.lvl = b->lvl;
+  p.lvl_cap = b->lvl_cap;
+  p.cnt = g->cnt;
+  p.status = g->status;
+  p.rounds_out = g->rounds;
+  p.ebits = g->ebits;
+  p.src = src;
+  void *args[] = {&p};
+  if (stats) {
+    if (!g->ev[0]) {
+      CU(cudaEventCreate(&g->ev[0]));
+      CU(cudaEventCreate(&g->ev[1]));
+    }
+    CU(cudaEventRecord(g->ev[0], st));
+  }
+  CU(cudaLaunchCooperativeKernel((const void *)bc_kernel, b->grid, BLOCK, args, 0, st));
+  if (stats) CU(cudaEventRecord(g->ev[1], st));
+  if (!dev_out) CU(cudaMemcpyAsync(delta, b->delta, (size_t)g->n * 8, cudaMemcpyDeviceToHost, st));
+  struct {
+    int status;
+    int pad;
+    long long rounds;
+  } ctrl;
+  CU(cudaMemcpyAsync(&ctrl, g->status, 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (stats) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
+    memset(stats, 0, offsetof(gbbs_stats, rounds_out));
+    stats->kernel_ms = ms;
+    stats->rounds = ctrl.rounds;
+  }
+  if (ctrl.status != 0) return fail(GBBS_EINTERNAL, "more than %lld BFS levels", b->lvl_cap);
+  return GBBS_OK;
+}
+
+extern "C" int gbbs_betweenness(const gbbs_graph *g, uint32_t src, double *delta,
+                                void *cuda_stream) {
+  return gbbs_betweenness_ex(g, src, delta, cuda_stream, nullptr, nullptr);
 }

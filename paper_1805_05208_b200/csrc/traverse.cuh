@@ -45,7 +45,10 @@ namespace cg = cooperative_groups;
 constexpr int BLOCK = 256;            // threads per CTA
 constexpr int NWARPS = BLOCK / 32;
 constexpr int TE = 256;               // edges per warp tile (edgeMapBlocked bsize)
-constexpr int NCH = 4;                // 32-edge chunks in flight per batch
+#ifndef GBBS_NCH
+#define GBBS_NCH 4
+#endif
+constexpr int NCH = GBBS_NCH;         // 32-edge chunks in flight per batch
 constexpr int WCAP = 384;             // per-warp staging capacity (vertices)
 constexpr long long HEAVY = 512;      // bitmap-forward: deferred to heavy tiles above this
 constexpr uint32_t INF = 0xFFFFFFFFu;
@@ -260,8 +263,6 @@ __device__ __forceinline__ void warp_append(const Params &p, int nb, unsigned lo
     p.fo[nb][pos] = o;
     p.fb[nb][pos] = a - o;
   }
-  const unsigned long long pos = (old >> p.ebits) + __popc(bal & lanemask_lt());
-  const long long o = (long long)(old & ((1ull << p.ebits) - 1)) + dex;
 }
 
 // Write `cnt` staged vertices of this warp into the next frontier list (a7).

@@ -24,7 +24,8 @@ GBBS_MODE_AUTO, GBBS_MODE_SPARSE, GBBS_MODE_DENSE = 0, 1, 2
 
 EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_bfs",
            "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
-           "gbbs_widest_path_ex", "gbbs_default_opts", "gbbs_launch_info", "gbbs_last_error")
+           "gbbs_widest_path_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
+           "gbbs_launch_info", "gbbs_last_error")
 
 
 class GbbsError(RuntimeError):
@@ -66,6 +67,8 @@ def _load():
     lib.gbbs_bfs_ex.argtypes = [p, u32, p, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_bellman_ford_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_widest_path.argtypes = [p, u32, p, p]
+    lib.gbbs_betweenness.argtypes = [p, u32, p, p]
+    lib.gbbs_betweenness_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_widest_path_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_default_opts.argtypes = [ctypes.POINTER(gbbs_opts)]
     lib.gbbs_default_opts.restype = None
@@ -73,7 +76,8 @@ def _load():
     lib.gbbs_last_error.argtypes = []
     lib.gbbs_last_error.restype = ctypes.c_char_p
     for f in ("gbbs_graph_create", "gbbs_graph_info", "gbbs_bfs", "gbbs_bellman_ford", "gbbs_bfs_ex",
-              "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_launch_info"):
+              "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_betweenness",
+              "gbbs_betweenness_ex", "gbbs_launch_info"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -161,6 +165,14 @@ def gbbs_widest_path(handle, src, width, stream=None, opts=None, stats=None):
                                        ctypes.byref(stats) if stats is not None else None))
 
 
+def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
+    st = _stream(stream, delta)
+    if stats is None:
+        _check(lib.gbbs_betweenness(handle, int(src), _ptr(delta), st))
+    else:
+        _check(lib.gbbs_betweenness_ex(handle, int(src), _ptr(delta), st, None, ctypes.byref(stats)))
+
+
 def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0):
     o = gbbs_opts()
     lib.gbbs_default_opts(ctypes.byref(o))
@@ -241,3 +253,6 @@ class Graph:
 
     def widest_path(self, src, width, stream=None, opts=None, stats=None):
         gbbs_widest_path(self.handle, src, width, stream, opts, stats)
+
+    def betweenness(self, src, delta, stream=None, stats=None):
+        gbbs_betweenness(self.handle, src, delta, stream, stats)

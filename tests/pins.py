@@ -148,3 +148,40 @@ def brute_force_widest(n: int, offsets, targets, weights, src: int):
 
     dfs(src, INF, {src})
     return np.array(best, np.uint64)
+
+
+def brute_force_dependencies(n: int, offsets, targets, src: int):
+    """delta_src(v) = sum_{t != src, v} sigma_st(v) / sigma_st straight from the
+    definition (pair dependencies; no Brandes recurrence): shortest-path counts
+    between every pair by a BFS from every vertex, sigma_st(v) = sigma_sv *
+    sigma_vt when d(s,v) + d(v,t) = d(s,t)."""
+    adj = [[int(targets[e]) for e in range(offsets[u], offsets[u + 1])] for u in range(n)]
+
+    def bfs_counts(s):
+        d = [None] * n
+        c = [0] * n
+        d[s], c[s] = 0, 1
+        frontier = [s]
+        while frontier:
+            nxt = []
+            for u in frontier:
+                for v in adj[u]:
+                    if d[v] is None:
+                        d[v] = d[u] + 1
+                        nxt.append(v)
+                    if d[v] == d[u] + 1:
+                        c[v] += c[u]
+            frontier = nxt
+        return d, c
+
+    D, C = zip(*[bfs_counts(s) for s in range(n)])
+    out = np.zeros(n)
+    for v in range(n):
+        if v == src or D[src][v] is None:
+            continue
+        for t in range(n):
+            if t in (src, v) or D[src][t] is None or D[v][t] is None:
+                continue
+            if D[src][v] + D[v][t] == D[src][t]:
+                out[v] += C[src][v] * C[v][t] / C[src][t]
+    return out

@@ -118,3 +118,15 @@ def test_c5_full(G):
         for T in (10, 40):
             assert (gpu_bfs(G, g, n, s, T)[0] == base).all()
     g.close()
+
+
+def test_c2_betweenness_full(G):
+    D, H = build("c2", False)
+    g = G.Graph(D["offsets"], D["targets"], None, symmetric=True)
+    s = D["sources"][0]
+    d = torch.empty(D["n"], dtype=torch.float64, device="cuda")
+    g.betweenness(s, d)
+    ref, _ = oracle.betweenness(H["off"], H["tgt"], s)
+    got = d.cpu().numpy()
+    assert np.allclose(got, ref, rtol=1e-9, atol=1e-9 * float(np.abs(ref).max()))
+    g.close()

@@ -355,3 +355,67 @@ def test_widest_c1_and_torus(G):
     assert (d == oracle.widest_path(off, tgt, w, 0)).all()
     assert oracle.check_widest(off, tgt, w, 0, d)[0]
     g.close()
+
+
+# ---- NEXT-3 single-source betweenness -----------------------------------------------
+
+def run_bc(G, g, src, host=False):
+    if host:
+        d = np.empty(g.n, np.float64)
+        g.betweenness(src, d)
+        return d
+    d = torch.empty(g.n, dtype=torch.float64, device="cuda")
+    g.betweenness(src, d)
+    return d.cpu().numpy()
+
+
+def assert_bc_close(got, ref):
+    # fp64 sums of positive terms in a nondeterministic order (DESIGN.md tolerance)
+    assert np.allclose(got, ref, rtol=1e-9, atol=1e-9 * max(1.0, float(np.abs(ref).max())))
+
+
+def test_bc_spec_examples_and_closed_forms(G):
+    off, tgt = graphgen.from_edge_list(3, [(0, 1), (1, 2)])
+    g = G.Graph(off, tgt, symmetric=True)
+    assert list(run_bc(G, g, 0)) == [0.0, 1.0, 0.0]
+    g.close()
+    off, tgt = graphgen.from_edge_list(4, [(0, 1), (0, 2), (1, 3), (2, 3)])
+    g = G.Graph(off, tgt, symmetric=True)
+    assert list(run_bc(G, g, 0)) == [0.0, 0.5, 0.5, 0.0]
+    g.close()
+    n = 3000
+    off, tgt = graphgen.from_edge_list(n, path_graph(n))
+    g = G.Graph(off, tgt, symmetric=True)
+    d = run_bc(G, g, 0)
+    assert (d[1:] == np.arange(n - 2, -1, -1)).all()
+    g.close()
+    off, tgt = graphgen.from_edge_list(500, [(0, i) for i in range(1, 500)])
+    g = G.Graph(off, tgt, symmetric=True)
+    assert (run_bc(G, g, 0) == 0).all()
+    d = run_bc(G, g, 7, host=True)
+    assert d[0] == 498 and (np.delete(d, 0) == 0).all()
+    g.close()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_bc_random_and_rmat(G, seed):
+    off, tgt = graphgen.random_graph(800, 0.004 * (1 + seed), 70 + seed, symmetric=True)
+    g = G.Graph(off, tgt, symmetric=True)
+    for src in (0, 11, 799):
+        assert_bc_close(run_bc(G, g, src), oracle.betweenness(off, tgt, src)[0])
+    g.close()
+    off, tgt = graphgen.rmat_graph(15, 1 << 19, 80 + seed, 0.57, 0.19, 0.19)
+    g = G.Graph(off, tgt, symmetric=True)
+    assert_bc_close(run_bc(G, g, 0), oracle.betweenness(off, tgt, 0)[0])
+    g.close()
+
+
+def test_bc_torus_and_grid(G):
+    off, tgt = graphgen.torus3d(12)
+    g = G.Graph(off, tgt, symmetric=True)
+    assert_bc_close(run_bc(G, g, 0), oracle.betweenness(off, tgt, 0)[0])
+    g.close()
+    off, tgt = graphgen.from_edge_list(40 * 30, grid_edges(40, 30))
+    g = G.Graph(off, tgt, symmetric=True)
+    assert_bc_close(run_bc(G, g, 0), oracle.betweenness(off, tgt, 0)[0])
+    g.close()

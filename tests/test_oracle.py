@@ -340,3 +340,46 @@ def test_widest_certificate_rejects_mutations():
     off, tgt, ww = graphgen.from_edge_list(4, [(0, 1), (2, 3)], True, [5, 9])
     bad = np.array([INF, 5, 4, 4], np.uint32)
     assert not oracle.check_widest(off, tgt, ww, 0, bad)[0]
+
+
+# ---- NEXT-3 single-source betweenness ----------------
+
+from pins import brute_force_dependencies  # noqa: E402
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_bc_brute_force(seed):
+    n = 8
+    off, tgt = graphgen.random_graph(n, 0.3 + 0.05 * (seed % 3), 500 + seed, symmetric=seed % 2 == 0)
+    for src in range(n):
+        got, _ = oracle.betweenness(off, tgt, src)
+        assert np.allclose(got, brute_force_dependencies(n, off, tgt, src), rtol=1e-12, atol=1e-12)
+
+
+def test_bc_closed_forms_and_spec_examples():
+    # SPEC.md:350 P3 src=0 -> [0, 1, 0]
+    off, tgt = graphgen.from_edge_list(3, [(0, 1), (1, 2)])
+    assert list(oracle.betweenness(off, tgt, 0)[0]) == [0.0, 1.0, 0.0]
+    # SPEC.md:351 diamond 0-1,0-2,1-3,2-3 src=0 -> d(1)=d(2)=0.5, d(3)=0
+    off, tgt = graphgen.from_edge_list(4, [(0, 1), (0, 2), (1, 3), (2, 3)])
+    assert list(oracle.betweenness(off, tgt, 0)[0]) == [0.0, 0.5, 0.5, 0.0]
+    # SPEC.md:352 star with centre src -> all leaves 0; leaf src -> centre n-2
+    n = 9
+    off, tgt = graphgen.from_edge_list(n, [(0, i) for i in range(1, n)])
+    assert (oracle.betweenness(off, tgt, 0)[0] == 0).all()
+    d, _ = oracle.betweenness(off, tgt, 3)
+    assert d[0] == n - 2 and (np.delete(d, 0) == 0).all()
+    # path from an end: delta(v) = number of vertices beyond v
+    n = 40
+    off, tgt = graphgen.from_edge_list(n, path_graph(n))
+    d, s = oracle.betweenness(off, tgt, 0, want_sigma=True)
+    assert (d[1:] == np.arange(n - 2, -1, -1)).all() and (s == 1).all()
+    # complete graph: every pair adjacent, no interior vertices
+    off, tgt = graphgen.from_edge_list(7, [(i, j) for i in range(7) for j in range(i + 1, 7)])
+    assert (oracle.betweenness(off, tgt, 2)[0] == 0).all()
+    # 2D grid from a corner: sigma = binomial path counts
+    a, b = 6, 5
+    off, tgt = graphgen.from_edge_list(a * b, grid_edges(a, b))
+    _, s = oracle.betweenness(off, tgt, 0, want_sigma=True)
+    from math import comb
+    assert all(s[x + a * y] == comb(x + y, x) for y in range(b) for x in range(a))
