@@ -138,7 +138,9 @@ def algorithmic_bytes(recs, n, m, algo):
       dense pull  : in-offsets 8 B per swept vertex + 8, in-edges 4 B per edge loaded,
                     visited bitmap n/8 read + n/8 written;
       bitmap fwd  : frontier bitmap(s) swept (n/8, x2 for BFS), offsets 16 B per
-                    frontier vertex, targets (+weights) per edge, emitted entries.
+                    frontier vertex, targets (+weights) per edge, emitted entries;
+      wBFS bucket : 24 B per bucket entry swept (id, dist, two offsets), 8 B per
+                    edge (target + weight), 4 B per insertion.
     Probes of the L2-resident bitmaps and dist/parent state are not counted (state
     bytes are returned separately)."""
     alg = 0
@@ -148,6 +150,8 @@ def algorithmic_bytes(recs, n, m, algo):
         emit = 36 * r["acquired"]
         if r["dense"] == 1:
             alg += 8 * r["vertices_swept"] + 8 + 4 * r["edges_examined"] + 2 * wb
+        elif r["dense"] in (3, 4):  # wBFS bucket round: entry id + dist + offsets, edges, inserts
+            alg += 24 * r["vertices_swept"] + 8 * r["edges_examined"] + 4 * r["acquired"]
         elif r["dense"] == 2:
             alg += (2 if algo == "bfs" else 1) * wb + 16 * r["vertices_swept"] + per_edge * r["edges_examined"] + emit
         else:
@@ -218,10 +222,13 @@ def run_ours(args, rank, world, local):
             g.bfs(src, dist, par, stream=stream, opts=opts, stats=stats)
         elif algo == "bf":
             g.bellman_ford(src, dist, stream=stream, stats=stats)
+        elif algo == "wbfs":
+            g.wbfs(src, dist, stream=stream, stats=stats)
         else:
             g.widest_path(src, dist, stream=stream, stats=stats)
 
-    algos = [args.algo] + (["bf", "wp"] if (want_w and args.algo == "bfs" and not args.profile) else [])
+    algos = [args.algo] + (["bf", "wbfs", "wp"] if (want_w and args.algo == "bfs" and not args.profile)
+                           else [])
     # per-source traversed edges (TEPS numerator, reading A20) and algorithmic bytes
     per_src = {}
     for algo in algos:
@@ -340,6 +347,15 @@ def run_ours(args, rank, world, local):
                 "roofline_frac": round(balg / (bkms * 1e-3) / 1e9 / peak, 4),
                 "kernel_ms_per_step": round(bkms, 4), "clocks": bclk,
                 "rounds": [per_src[("bf", s)]["rounds"] for s in sources]}
+        if "wbfs" in algos and args.algo == "bfs":
+            wt, wclk, wkms = res["wbfs"]
+            we = sum(per_src[("wbfs", s)]["m_reach"] for s in sources)
+            out["wbfs"] = {
+                "value": round(we / (wt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective)",
+                "ms_per_step": round(wt, 4), "kernel_ms_per_step": round(wkms, 4),
+                "note": "NEXT-2: integral-weight SSSP over distance buckets (bucket width 1), "
+                        "same graph and weights as the Bellman-Ford leg",
+                "rounds": [per_src[("wbfs", s)]["rounds"] for s in sources]}
         if "wp" in algos and args.algo == "bfs":
             wt, wclk, wkms = res["wp"]
             we = sum(per_src[("wp", s)]["m_reach"] for s in sources)

@@ -174,6 +174,26 @@ int gbbs_widest_path(const gbbs_graph *g, uint32_t src, uint32_t *width,
 int gbbs_betweenness(const gbbs_graph *g, uint32_t src, double *delta,
                      void *cuda_stream);
 
+/*
+ * gbbs_wbfs — integral-weight SSSP ("weighted BFS", output spec P:1481-1484,
+ * sec:benchmark; algorithm, sec:algs, after Julienne): dist[v] = the
+ * shortest weighted distance from src, GBBS_INF if unreachable — the same
+ * result as gbbs_bellman_ford, reached by extracting distance buckets in
+ * increasing order, each bucket one edgeMap round with the priority-write min
+ * (PAPER.md:1826-1831), vertices whose distance dropped moved to their new
+ * bucket.  With the default bucket width 1 and weights >= 1 every reached
+ * vertex is expanded exactly once (O(m) work; rounds = number of distinct
+ * finite distances).  gbbs_opts.delta > 1 selects Delta-stepping buckets.
+ *
+ * Weights, dist, stream and error conventions as gbbs_bellman_ford (including
+ * GBBS_ERANGE), plus GBBS_EINVAL if floor((delta - 1 + maxw) / delta) >= 64
+ * (the bucket ring holds 64 lists).  The bucket structure is allocated on the
+ * first call and kept with the handle: 4 * nbq * 2^ceil(log2 n) bytes for the
+ * bucket lists (nbq = the power of two above that span, <= 64) plus 16n bytes.
+ */
+int gbbs_wbfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
+              void *cuda_stream);
+
 /* ---- extended calls (bench / tests) ------------------------------------ */
 
 /* Representation choice per round (threshold rule reading A10).
@@ -192,14 +212,19 @@ typedef struct {
                              are co-resident (default).  Fewer CTAs make
                              the per-round grid barrier cheaper (many small
                              rounds) at the cost of latency hiding.        */
-  uint32_t reserved[5];   /* must be zero                                  */
+  uint32_t delta;         /* gbbs_wbfs bucket width; 0 = default: 1 (the
+                             paper's one bucket per distance) while
+                             maxw <= 32, else ceil(maxw / 32).  Other
+                             calls ignore it.                              */
+  uint32_t reserved[4];   /* must be zero                                  */
 } gbbs_opts;
 
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */
 typedef struct {
   int32_t dense;          /* round kind: 0 = list push, 1 = dense pull,
-                             2 = bitmap-forward push                      */
-  int32_t reserved;
+                             2 = bitmap-forward push, 3 = wBFS bucket
+                             list, 4 = wBFS near list (same bucket)       */
+  int32_t bucket;         /* wBFS: the bucket the round processed; else 0 */
   int64_t frontier;       /* |U|: frontier vertices with out-degree > 0   */
   int64_t frontier_edges; /* sum of out-degrees of U                       */
   int64_t acquired;       /* vertices won this round (incl. out-degree 0) */
@@ -241,6 +266,8 @@ int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
 int gbbs_betweenness_ex(const gbbs_graph *g, uint32_t src, double *delta,
                         void *cuda_stream, const gbbs_opts *opts,
                         gbbs_stats *stats);
+int gbbs_wbfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
+                 void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats);
 int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *width,
                         void *cuda_stream, const gbbs_opts *opts,
                         gbbs_stats *stats);

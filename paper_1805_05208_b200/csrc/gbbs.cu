@@ -53,7 +53,7 @@ struct gbbs_graph {
   long long n = 0, m = 0;
   uint32_t flags = 0;
   int ebits = 1;
-  uint32_t maxw = 1;
+  uint32_t maxw = 1, minw = 1;
   long long *off = nullptr;
   uint32_t *tgt = nullptr;
   uint32_t *wgt = nullptr;
@@ -79,9 +79,11 @@ struct gbbs_graph {
   int grid[3][2] = {{0, 0}, {0, 0}, {0, 0}};  // [algo][stats]
   cudaEvent_t ev[2] = {nullptr, nullptr};
   struct BcScratch *bc = nullptr;  // betweenness scratch (lazy)
+  struct WbfsScratch *wb = nullptr;  // wBFS bucket structure (lazy)
 };
 
 static void free_bc(gbbs_graph *g);
+static void free_wbfs(gbbs_graph *g);
 
 static void free_graph(gbbs_graph *g) {
   if (!g) return;
@@ -106,6 +108,7 @@ static void free_graph(gbbs_graph *g) {
   if (g->ev[0]) cudaEventDestroy(g->ev[0]);
   if (g->ev[1]) cudaEventDestroy(g->ev[1]);
   free_bc(g);
+  free_wbfs(g);
   delete g;
 }
 
@@ -122,13 +125,32 @@ __global__ void k_validate(const long long *off, const uint32_t *tgt, long long 
     if (tgt[e] >= (unsigned long long)n) atomicOr(bad, 2ull);
 }
 
+// out[0] = max weight, out[1] = min weight (out[1] preset to 0xFFFFFFFF)
 __global__ void k_maxw(const uint32_t *w, long long m, unsigned int *out) {
   long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long gs = (long long)gridDim.x * blockDim.x;
-  uint32_t mx = 0;
-  for (long long e = gt; e < m; e += gs) mx = max(mx, w[e]);
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+  uint32_t mx = 0, mn = 0xFFFFFFFFu;
+  for (long long e = gt; e < m; e += gs) {
+    mx = max(mx, w[e]);
+    mn = min(mn, w[e]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, mx);
+    atomicMin(out + 1, mn);
+  }
+}
+
+// bit v set iff out-degree(v) > HEAVY (wBFS: insertions count the hubs of a bucket)
+__global__ void k_heavy_bits(const long long *off, long long n, long long nwords, uint32_t *hv) {
+  long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((v >> 5) >= nwords) return;
+  const bool h = v < n && off[v + 1] - off[v] > HEAVY;
+  const unsigned b = __ballot_sync(0xffffffffu, h);
+  if ((threadIdx.x & 31) == 0) hv[v >> 5] = b;
 }
 
 // key = target << 32 | source for every edge; one warp per source vertex.
@@ -279,12 +301,14 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
                   (bad & 2) ? " target >= n" : "");
     }
   }
-  g->maxw = 1;
+  g->maxw = g->minw = 1;
   if (g->wgt && m > 0) {
     unsigned int *mx = (unsigned int *)(dscratch + 1);
+    CU(cudaMemset(mx + 1, 0xFF, 4));
     k_maxw<<<1184, 256>>>(g->wgt, m, mx);
     CU(cudaGetLastError());
     CU(cudaMemcpy(&g->maxw, mx, 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&g->minw, mx + 1, 4, cudaMemcpyDeviceToHost));
   }
   cudaFree(dscratch);
 
@@ -440,6 +464,118 @@ static int launch(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev0, cu
   return GBBS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// NEXT-2: wBFS bucket structure (lazy, per handle; sized for the bucket span)
+// ---------------------------------------------------------------------------
+struct WbfsScratch {
+  uint32_t *bq = nullptr;  // nbq lists x qcap ids
+  unsigned long long qcap = 0;
+  int nbq = 0;
+  uint32_t *xq[3] = {nullptr, nullptr, nullptr};
+  uint32_t *tag = nullptr, *hv = nullptr;
+  unsigned long long *ctr = nullptr;  // btail[64] bheavy[64] xcnt[6] pub[3]
+  int grid[2] = {0, 0};
+};
+
+static void free_wbfs(gbbs_graph *g) {
+  WbfsScratch *w = g->wb;
+  if (!w) return;
+  cudaFree(w->bq);
+  for (int i = 0; i < 3; i++) cudaFree(w->xq[i]);
+  cudaFree(w->tag);
+  cudaFree(w->hv);
+  cudaFree(w->ctr);
+  delete w;
+  g->wb = nullptr;
+}
+
+constexpr size_t WBFS_DYN_SMEM = sizeof(WbfsWarpSmem) * NWARPS;
+
+template <bool STATS>
+static int wbfs_grid(int *grid) {
+  int dev = 0, nsm = 0, per = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaFuncSetAttribute(wbfs_kernel<STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)WBFS_DYN_SMEM));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, wbfs_kernel<STATS>, BLOCK, WBFS_DYN_SMEM));
+  if (per < 1) return fail(GBBS_ECUDA, "wbfs kernel cannot be resident");
+  *grid = per * nsm;
+  return GBBS_OK;
+}
+
+// Bucket width and list count: delta = opts.delta, or by default 1 (the paper's
+// wBFS) while the span fits 64 lists, else ceil(maxw / 32).  span = floor((delta -
+// 1 + maxw) / delta) buckets above the current one can receive entries, so nbq =
+// the smallest power of two > span.
+static int wbfs_setup(gbbs_graph *g, uint32_t delta, Params &p) {
+  const unsigned long long W = g->maxw ? g->maxw : 1;
+  unsigned long long D = delta ? delta : (W <= 32 ? 1 : (W + 31) / 32);
+  const unsigned long long span = (D - 1 + W) / D;
+  if (span >= 64)
+    return fail(GBBS_EINVAL, "wbfs: delta %llu too small for max weight %llu (needs (delta-1+maxw)/delta < 64)",
+                D, W);
+  int nbq = 1;
+  while ((unsigned long long)nbq <= span) nbq <<= 1;
+  unsigned long long qcap = 1;
+  while (qcap < (unsigned long long)g->n) qcap <<= 1;
+  WbfsScratch *w = g->wb;
+  if (w && w->nbq < nbq) {
+    free_wbfs(g);
+    w = nullptr;
+  }
+  if (!w) {
+    w = new (std::nothrow) WbfsScratch();
+    if (!w) return fail(GBBS_ENOMEM, "host allocation");
+    g->wb = w;
+    w->nbq = nbq;
+    w->qcap = qcap;
+    CU(cudaMalloc(&w->bq, (size_t)nbq * qcap * 4));
+    for (int i = 0; i < 3; i++) CU(cudaMalloc(&w->xq[i], (size_t)g->n * 4));
+    CU(cudaMalloc(&w->tag, (size_t)g->n * 4));
+    CU(cudaMalloc(&w->hv, (size_t)g->nwords * 4));
+    CU(cudaMalloc(&w->ctr, (64 + 64 + 6 + 3) * 8));
+    k_heavy_bits<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->n, g->nwords, w->hv);
+    CU(cudaGetLastError());
+    int rc;
+    if ((rc = wbfs_grid<false>(&w->grid[0]))) return rc;
+    if ((rc = wbfs_grid<true>(&w->grid[1]))) return rc;
+  }
+  const bool need_near = D > 1 || g->minw == 0;
+  p.bq = w->bq;
+  p.qcap = w->qcap;
+  p.nbq = w->nbq;
+  p.btail = w->ctr;
+  p.bheavy = w->ctr + 64;
+  p.xcnt = w->ctr + 128;
+  p.pub = w->ctr + 134;
+  for (int i = 0; i < 3; i++) p.xq[i] = w->xq[i];
+  p.tag = need_near ? w->tag : nullptr;
+  p.hv = w->hv;
+  p.delta = (uint32_t)D;
+  const long long n1 = g->n + 1;
+  p.max_rounds = need_near ? (n1 < (1ll << 31) ? n1 * n1 : (1ll << 62)) : n1;
+  return GBBS_OK;
+}
+
+template <bool STATS>
+static int launch_wbfs(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1,
+                       unsigned ctas_per_sm) {
+  void *args[] = {&p};
+  int grid = g->wb->grid[STATS];
+  if (ctas_per_sm) {
+    int nsm = 0;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    const long long want = (long long)ctas_per_sm * nsm;
+    if (want < grid) grid = (int)want;
+  }
+  if (ev0) CU(cudaEventRecord(ev0, st));
+  CU(cudaLaunchCooperativeKernel((const void *)wbfs_kernel<STATS>, grid, BLOCK, args, WBFS_DYN_SMEM,
+                                 st));
+  if (ev1) CU(cudaEventRecord(ev1, st));
+  return GBBS_OK;
+}
+
 static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, uint32_t *parent,
                void *stream, const gbbs_opts *opts, gbbs_stats *stats) {
   g_last_error.clear();
@@ -452,11 +588,11 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   if (opts) {
     o = *opts;
     if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 5; i++)
+    for (int i = 0; i < 4; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.mode < 0 || o.mode > 2) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
   }
-  if (algo == ALGO_BF) {
+  if (algo == ALGO_BF || algo == ALGO_WBFS) {
     // uint32 distances: every finite distance is a simple-path length <= maxw*(n-1)
     unsigned long long bound = (unsigned long long)g->maxw * (unsigned long long)(g->n - 1);
     if (g->maxw != 0 && bound / g->maxw != (unsigned long long)(g->n - 1)) bound = ~0ull;
@@ -526,6 +662,10 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   p.mode = o.mode;
   p.src = src;
 
+  if (algo == ALGO_WBFS) {
+    int rc2 = wbfs_setup(g, o.delta, p);
+    if (rc2) return rc2;
+  }
 #ifdef GBBS_DBG_PHASE
   static unsigned long long *dbg = nullptr;
   if (!dbg) cudaMalloc(&dbg, 64 * 4 * 8);
@@ -546,8 +686,10 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
     rc = want_rounds ? launch<ALGO_BFS, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_BFS, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
   else if (algo == ALGO_BF)
     rc = want_rounds ? launch<ALGO_BF, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_BF, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
-  else
+  else if (algo == ALGO_WP)
     rc = want_rounds ? launch<ALGO_WP, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_WP, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
+  else
+    rc = want_rounds ? launch_wbfs<true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch_wbfs<false>(g, p, st, ev0, ev1, o.ctas_per_sm);
   if (rc) return rc;
   if (!dist_dev) CU(cudaMemcpyAsync(dist, ddist, nb, cudaMemcpyDeviceToHost, st));
   if (parent && !par_dev) CU(cudaMemcpyAsync(parent, dpar, nb, cudaMemcpyDeviceToHost, st));
@@ -618,6 +760,15 @@ extern "C" int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t 
   return run(g, ALGO_BF, src, dist, nullptr, cuda_stream, opts, stats);
 }
 
+extern "C" int gbbs_wbfs(const gbbs_graph *g, uint32_t src, uint32_t *dist, void *cuda_stream) {
+  return run(g, ALGO_WBFS, src, dist, nullptr, cuda_stream, nullptr, nullptr);
+}
+
+extern "C" int gbbs_wbfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist, void *cuda_stream,
+                            const gbbs_opts *opts, gbbs_stats *stats) {
+  return run(g, ALGO_WBFS, src, dist, nullptr, cuda_stream, opts, stats);
+}
+
 extern "C" int gbbs_widest_path(const gbbs_graph *g, uint32_t src, uint32_t *width, void *cuda_stream) {
   return run(g, ALGO_WP, src, width, nullptr, cuda_stream, nullptr, nullptr);
 }
@@ -684,7 +835,7 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   if (!delta) return fail(GBBS_EINVAL, "delta is NULL");
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   if (opts)
-    for (int i = 0; i < 5; i++)
+      for (int i = 0; i < 4; i++)
       if (opts->reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
   int rc = GBBS_OK;
   BcScratch *b = bc_scratch(g, &rc);

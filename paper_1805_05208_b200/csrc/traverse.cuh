@@ -34,6 +34,9 @@
 // Winners are packed per warp (ballot -> shared staging -> one packed 64-bit
 // atomicAdd per flush), i.e. at most LN(U) writes.
 #pragma once
+// apply_batch returns early for wBFS (insertions instead of staging); the
+// staging loops after it are then unreachable by design
+#pragma nv_diag_suppress 128
 
 #include <cooperative_groups.h>
 #include <cstdint>
@@ -54,13 +57,14 @@ constexpr long long HEAVY = 512;      // bitmap-forward: deferred to heavy tiles
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
-enum Algo { ALGO_BFS = 0, ALGO_BF = 1, ALGO_WP = 2 };  // WP: widest path, (max, min) semiring
+// WP: widest path, (max, min) semiring; WBFS: integral-weight SSSP with buckets
+enum Algo { ALGO_BFS = 0, ALGO_BF = 1, ALGO_WP = 2, ALGO_WBFS = 3 };
 enum Emit { EMIT_LIST = 0, EMIT_COUNT = 1 };
 enum { LIST_HEAVY = 2 };
 
 struct RoundStat {           // mirrors gbbs_round_stat
   int32_t dense;
-  int32_t reserved;
+  int32_t bucket;
   long long frontier;
   long long frontier_edges;
   long long acquired;
@@ -100,6 +104,18 @@ struct Params {
   int mode;                  // 0 auto, 1 sparse, 2 dense
   int symmetric;
   uint32_t src;
+  // wBFS (ALGO_WBFS) bucket structure, wbfs_kernel
+  uint32_t *bq;              // [nb][qcap] ring of bucket lists (vertex ids, circular)
+  unsigned long long *btail; // [nb] monotone append counters of the bucket lists
+  unsigned long long *bheavy;// [nb] monotone counters of heavy (deg > HEAVY) entries
+  uint32_t *xq[3];           // near lists: re-insertions into the current bucket
+  unsigned long long *xcnt;  // [3] their counters, [3] heavy counters after them
+  unsigned long long *pub;   // [3] per-round masks of bucket lists that got entries
+  uint32_t *tag;             // [n] round tag deduplicating near-list insertions
+  const uint32_t *hv;        // [nwords] out-degree > HEAVY
+  unsigned long long qcap;   // per-list capacity (power of two >= n)
+  uint32_t delta;            // bucket width
+  int nbq;                   // number of bucket lists (power of two)
 #ifdef GBBS_DBG_PHASE
   unsigned long long *dbg;   // [64][4] per-round max phase durations (ns)
 #endif
@@ -136,6 +152,8 @@ struct Smem {
 // EMIT_COUNT rounds, and gbbs_round_stat counters (STATS builds only).
 struct WarpState {
   int scnt = 0;
+  unsigned long long bk = 0;     // wBFS: bucket being processed
+  unsigned long long pmask = 0;  // wBFS: bucket lists this lane appended to
   unsigned long long K = 0, D = 0;
   unsigned long long edges = 0, swept = 0, acquired = 0;
 };
@@ -273,7 +291,8 @@ __device__ __forceinline__ void warp_append(const Params &p, int nb, unsigned lo
 template <int ALGO>
 __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, int cnt, int nb,
                                            int r, uint32_t *bits_next,
-                                           unsigned long long *tmark = nullptr) {
+                                           unsigned long long *tmark = nullptr,
+                                           unsigned long long *ctr = nullptr) {
   constexpr int FL = 4;
   const int lane = threadIdx.x & 31;
 #ifdef GBBS_DBG_PHASE
@@ -304,7 +323,7 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
   const unsigned long long tB = globaltimer_ns();
 #endif
   unsigned long long old = 0;
-  if (lane == 0 && K) old = atomicAdd(p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
+  if (lane == 0 && K) old = atomicAdd(ctr ? ctr : p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
   old = __shfl_sync(FULL, old, 0);
 #ifdef GBBS_DBG_PHASE
   const unsigned long long tC = globaltimer_ns();
@@ -342,7 +361,7 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
         fv[pos] = vv[u];
         fo[pos] = o;
         fb[pos] = lo[u] - o;
-      } else if (ALGO != ALGO_BFS && i < cnt) {
+      } else if ((ALGO == ALGO_BF || ALGO == ALGO_WP) && i < cnt) {
         // out-degree-0 vertex: it never enters a frontier; release its TS bit.
         atomicAnd(bits_next + (vv[u] >> 5), ~(1u << (vv[u] & 31)));
       }
@@ -360,6 +379,111 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
     atomicMax(p.dbg + 4 * r + 3, (unsigned long long)cnt);
   }
 #endif
+}
+
+// ---- wBFS bucket insertion ------------------------------------------------------------
+// A vertex whose distance the priority-write lowered from `old` to `nd` moves to
+// bucket nd / delta (Julienne's bucket update after edgeMapData).
+// Into the bucket being processed it goes to the near list of this round (once
+// per round: round tag); into a later bucket it is appended to that bucket's list
+// unless it already sits there (old in the same bucket: the list holds it
+// unprocessed, since distances only fall).  Lanes aiming at the same list are
+// grouped with match.any and reserve their slots with ONE atomicAdd.
+constexpr uint32_t XKEY = 64;    // near list
+constexpr uint32_t NOKEY = 0xFFFFFFFFu;
+
+// Per-warp wBFS staging metadata in dynamic shared memory (wbfs_kernel only):
+// the list key of every staged vertex and a 65-bin histogram over the keys.
+struct WbfsWarpSmem {
+  uint32_t hist[XKEY + 1];
+  uint8_t key[WCAP];
+};
+extern __shared__ __align__(16) unsigned char gbbs_dyn_smem[];
+__device__ __forceinline__ WbfsWarpSmem &wbfs_smem() {
+  return reinterpret_cast<WbfsWarpSmem *>(gbbs_dyn_smem)[threadIdx.x >> 5];
+}
+
+// Flush the warp's staged insertions: one shared-memory histogram over the list
+// keys, then ONE atomicAdd per (list, flush) reserves the slots — the bucket
+// tails are the hottest addresses of the run, so per-lane reservations would
+// serialise on them — and every vertex is written at base + its rank in its
+// list.  Warp-uniform call.
+template <bool STATS>
+__device__ __forceinline__ void wbfs_flush(const Params &p, WarpState &ws, const uint32_t *st, int cnt,
+                                        int r) {
+  const int lane = threadIdx.x & 31;
+  const int xr = r % 3;
+  WbfsWarpSmem &w = wbfs_smem();
+  __syncwarp();
+  for (int i = lane; i < cnt; i += 32) atomicAdd(&w.hist[w.key[i]], 1u);
+  __syncwarp();
+  const uint32_t hA = w.hist[lane], hB = w.hist[lane + 32], hX = w.hist[XKEY];
+  unsigned long long bA = 0, bB = 0, bX = 0;
+  if (hA) bA = atomicAdd(p.btail + lane, (unsigned long long)hA);
+  if (hB) bB = atomicAdd(p.btail + lane + 32, (unsigned long long)hB);
+  if (lane == 0 && hX) bX = atomicAdd(p.xcnt + xr, (unsigned long long)hX);
+  ws.pmask |= (hA ? 1ull << lane : 0ull) | (hB ? 1ull << (lane + 32) : 0ull);
+  __syncwarp();
+  w.hist[lane] = 0;
+  w.hist[lane + 32] = 0;
+  if (lane == 0) w.hist[XKEY] = 0;
+  __syncwarp();
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t key = i < cnt ? w.key[i] : 0u;
+    const unsigned long long x0 = __shfl_sync(FULL, bA, key & 31);
+    const unsigned long long x1 = __shfl_sync(FULL, bB, key & 31);
+    const unsigned long long x2 = __shfl_sync(FULL, bX, 0);
+    if (i < cnt) {
+      const uint32_t v = st[i];
+      const unsigned long long pos =
+          (key == XKEY ? x2 : (key >= 32 ? x1 : x0)) + atomicAdd(&w.hist[key], 1u);
+      if (key == XKEY)
+        p.xq[xr][pos] = v;
+      else
+        p.bq[(unsigned long long)key * p.qcap + (pos & (p.qcap - 1))] = v;
+      if ((__ldg(p.hv + (v >> 5)) >> (v & 31)) & 1u)
+        atomicAdd(key == XKEY ? p.xcnt + 3 + xr : p.bheavy + key, 1ull);
+    }
+  }
+  __syncwarp();
+  w.hist[lane] = 0;
+  w.hist[lane + 32] = 0;
+  if (lane == 0) w.hist[XKEY] = 0;
+  if (STATS && lane == 0) ws.acquired += cnt;
+  __syncwarp();
+}
+
+// Stage the vertices whose distance the priority-write lowered (bucket update).
+template <bool STATS, int NB>
+__device__ __forceinline__ void wbfs_stage(const Params &p, WarpState &ws, uint32_t *st,
+                                           const bool (&cand)[NB], const uint32_t (&v)[NB],
+                                           const unsigned long long (&nd)[NB],
+                                           const uint32_t (&old)[NB], int r) {
+  WbfsWarpSmem &w = wbfs_smem();
+#pragma unroll
+  for (int j = 0; j < NB; j++) {
+    uint32_t key = NOKEY;
+    if (cand[j]) {
+      const unsigned long long b = nd[j] / p.delta;
+      if (b == ws.bk) {
+        if (atomicExch(p.tag + v[j], (uint32_t)(r + 1)) != (uint32_t)(r + 1)) key = XKEY;
+      } else if (old[j] == INF || old[j] / p.delta != b) {
+        key = (uint32_t)(b & (unsigned long long)(p.nbq - 1));
+      }
+    }
+    const unsigned bal = __ballot_sync(FULL, key != NOKEY);
+    if (key != NOKEY) {
+      const int idx = ws.scnt + __popc(bal & lanemask_lt());
+      st[idx] = v[j];
+      w.key[idx] = (uint8_t)key;
+    }
+    ws.scnt += __popc(bal);
+  }
+  if (ws.scnt > WCAP - 32 * NB) {
+    wbfs_flush<STATS>(p, ws, st, ws.scnt, r);
+    ws.scnt = 0;
+  }
 }
 
 // ---- F: apply one batch of NCH 32-edge chunks -------------------------------------
@@ -411,9 +535,11 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       cur[j] = act[j] ? (uint32_t)p.shadow[vv[j]] : (ALGO == ALGO_WP ? 0xFFFFu : 0u);
     }
     bool cand[NCH];
+    uint32_t oldv[NCH];
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       cand[j] = false;
+      oldv[j] = 0;
       if (!act[j]) continue;
       if (ALGO == ALGO_WP) {
         if (nd[j] > (unsigned long long)cur[j]) {
@@ -423,11 +549,16 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       } else if (nd[j] < (unsigned long long)cur[j] || cur[j] == 0xFFFFu) {
         const uint32_t old = atomicMin(p.dist + vv[j], (uint32_t)nd[j]);  // priority-write
         cand[j] = nd[j] < (unsigned long long)old;
+        oldv[j] = old;
       }
     }
 #pragma unroll
     for (int j = 0; j < NCH; j++)
       if (cand[j]) p.shadow[vv[j]] = (uint16_t)min(nd[j], 0xFFFFull);
+    if constexpr (ALGO == ALGO_WBFS) {
+      wbfs_stage<STATS, NCH>(p, ws, st, cand, vv, nd, oldv, r);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       win[j] = false;
@@ -666,13 +797,67 @@ __device__ __forceinline__ int warp_gather(SweepSmem &w, long long w0, uint32_t 
   return __shfl_sync(FULL, inc, 31);
 }
 
+// ---- vertex push (bitmap-forward and bucket sweeps) --------------------------------
+// One vertex per lane: v with out-edges [a, a+dg) and the value F propagates (x:
+// BFS the parent id v, BF/WP/wBFS dist[v]).  Lane-owned when <= 32 edges (NCH
+// edges per batch), warp-owned when <= HEAVY edges, appended to the heavy list
+// (counter *hctr) above that — heavy vertices are pushed with list tiles after a
+// grid barrier, so a hub is spread over many warps (edgeMapBlocked).
+// dg = 0 marks an idle lane.
+template <int ALGO, bool STATS, int EMIT>
+__device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, WarpState &ws,
+                                              uint32_t v, long long a, int dg, uint32_t x,
+                                              unsigned long long *hctr, int nb, int r,
+                                              uint32_t *bits, const uint32_t *prebits) {
+  const int lane = threadIdx.x & 31;
+  const bool heavy = dg > (int)HEAVY;
+  warp_append(p, LIST_HEAVY, hctr, heavy, v, a, dg);
+  unsigned med = __ballot_sync(FULL, dg > 32 && !heavy);
+  while (med) {
+    const int l = __ffs(med) - 1;
+    med &= med - 1;
+    const long long la = __shfl_sync(FULL, a, l);
+    const int ld = __shfl_sync(FULL, dg, l);
+    const uint32_t lx = __shfl_sync(FULL, x, l);
+    if (STATS && lane == 0) ws.edges += ld;
+    for (int cs = 0; cs < ld; cs += 32 * NCH) {
+      uint32_t vv[NCH], ww[NCH], uu[NCH];
+      bool act[NCH];
+#pragma unroll
+      for (int j = 0; j < NCH; j++) {
+        const int e = cs + 32 * j + lane;
+        act[j] = e < ld;
+        vv[j] = act[j] ? ld_stream(p.tgt + la + e) : 0;
+        ww[j] = (ALGO != ALGO_BFS && act[j]) ? (p.wgt ? ld_stream(p.wgt + la + e) : 1u) : 0;
+        uu[j] = lx;
+      }
+      apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+    }
+  }
+  const int mine = dg <= 32 ? dg : 0;
+  if (STATS) ws.edges += mine;
+  int mx = mine;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+  for (int jj = 0; jj < mx; jj += NCH) {
+    uint32_t vv[NCH], ww[NCH], uu[NCH];
+    bool act[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      act[j] = jj + j < mine;
+      vv[j] = act[j] ? ld_stream(p.tgt + a + jj + j) : 0;
+      ww[j] = (ALGO != ALGO_BFS && act[j]) ? (p.wgt ? ld_stream(p.wgt + a + jj + j) : 1u) : 0;
+      uu[j] = x;
+    }
+    apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
+  }
+}
+
 // ---- bitmap-forward push ----------------------------------------------------------
 // BFS: frontier = precheck (vis_cur) & ~bits (vis_old): what the last dense round
 // added; the TS target is vis_old, which also absorbs the frontier bits (atomicOr)
 // so that it becomes the next visited set; vis_cur is read-only and is the
 // pre-check.  BF: frontier = fr (this round's TS bits), cleared as swept.
-// Each frontier vertex: lane-owned when <= 32 edges (NCH edges per batch),
-// warp-owned when <= HEAVY edges, appended to the heavy list above that.
 template <int ALGO, bool STATS, int EMIT>
 __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, WarpState &ws,
                                               long long w0, uint32_t *fr, uint32_t *bits,
@@ -705,47 +890,8 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
     }
     uint32_t x = v;
     if (ALGO != ALGO_BFS) x = dg > 0 ? ld_relaxed(p.dist + v) : 0u;
-    const bool heavy = dg > (int)HEAVY;
-    warp_append(p, LIST_HEAVY, p.hcnt + (r & 1), heavy, v, a, dg);
-    unsigned med = __ballot_sync(FULL, dg > 32 && !heavy);
-    while (med) {
-      const int l = __ffs(med) - 1;
-      med &= med - 1;
-      const long long la = __shfl_sync(FULL, a, l);
-      const int ld = __shfl_sync(FULL, dg, l);
-      const uint32_t lx = __shfl_sync(FULL, x, l);
-      if (STATS && lane == 0) ws.edges += ld;
-      for (int cs = 0; cs < ld; cs += 32 * NCH) {
-        uint32_t vv[NCH], ww[NCH], uu[NCH];
-        bool act[NCH];
-#pragma unroll
-        for (int j = 0; j < NCH; j++) {
-          const int e = cs + 32 * j + lane;
-          act[j] = e < ld;
-          vv[j] = act[j] ? ld_stream(p.tgt + la + e) : 0;
-          ww[j] = (ALGO != ALGO_BFS && act[j]) ? (p.wgt ? ld_stream(p.wgt + la + e) : 1u) : 0;
-          uu[j] = lx;
-        }
-        apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
-      }
-    }
-    const int mine = dg <= 32 ? dg : 0;
-    if (STATS) ws.edges += mine;
-    int mx = mine;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
-    for (int jj = 0; jj < mx; jj += NCH) {
-      uint32_t vv[NCH], ww[NCH], uu[NCH];
-      bool act[NCH];
-#pragma unroll
-      for (int j = 0; j < NCH; j++) {
-        act[j] = jj + j < mine;
-        vv[j] = act[j] ? ld_stream(p.tgt + a + jj + j) : 0;
-        ww[j] = (ALGO != ALGO_BFS && act[j]) ? (p.wgt ? ld_stream(p.wgt + a + jj + j) : 1u) : 0;
-        uu[j] = x;
-      }
-      apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
-    }
+    push_vertices<ALGO, STATS, EMIT>(p, wsm, ws, v, a, dg, x, p.hcnt + (r & 1), nb, r, bits,
+                                     prebits);
   }
   __syncwarp();
 }
@@ -1108,6 +1254,216 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     }
     grid.sync();
   }
+  if (blockIdx.x == 0 && tid == 0) *p.rounds_out = r;
+}
+
+// ---- wBFS: integral-weight SSSP over buckets (NEXT-2) ---------------------------------
+// Julienne's weighted BFS (sec:algs; output spec P:1481-1484): buckets
+// of distance width delta are extracted in increasing order; each extracted
+// bucket is one edgeMapData round whose F is the priority-write min of
+// dist[u] + w (a6), and every vertex whose distance dropped moves to its new
+// bucket (wbfs_insert).  delta = 1 is the paper's algorithm (one bucket per
+// distance value; with weights >= 1 each vertex is expanded exactly once, O(m)
+// work); delta > 1 is Delta-stepping, re-expanding vertices that improve inside
+// the current bucket from a near list.
+//
+// Bucket structure, all on the device: nbq (a power of two > the bucket span
+// floor((delta - 1 + maxw) / delta)) circular lists of capacity qcap >= n; bucket
+// j lives in list j mod nbq, which is unambiguous because every pending entry lies
+// within one span above the bucket being processed.  Append counters are
+// monotone; each CTA keeps the list heads in shared memory and the set of lists
+// with pending entries in a register mask (`pend`), fed by per-round masks that
+// appending warps publish (`pub`).  All CTAs therefore take the same decision
+// without a host round trip: every round reads only counters that no warp
+// updates during that round.  Entries whose vertex has since moved to an
+// earlier bucket are skipped when swept (lazy deletion).
+template <bool STATS>
+__global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) wbfs_kernel(Params p) {
+  __shared__ Smem s;
+  __shared__ unsigned long long s_head[64], s_hhead[64], s_ctl[3 + 2 * 64];
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long gtid = (long long)blockIdx.x * BLOCK + tid;
+  const long long gstride = (long long)gridDim.x * BLOCK;
+  const long long gw = (long long)blockIdx.x * NWARPS + warp;
+  const long long nw = (long long)gridDim.x * NWARPS;
+  const uint32_t src = p.src;
+  const int nbq = p.nbq;
+  const unsigned long long qmask = p.qcap - 1;
+  WarpSmem &wsm = s.w[warp];
+
+  // a1: per-run init
+  for (long long i = gtid; i < p.n; i += gstride) {
+    st_stream(p.dist + i, (i == src) ? 0u : INF);
+    p.shadow[i] = (i == src) ? 0u : 0xFFFFu;
+    if (p.tag) p.tag[i] = 0;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    for (int q = 0; q < nbq; q++) p.btail[q] = p.bheavy[q] = 0;
+    for (int q = 0; q < 6; q++) p.xcnt[q] = 0;
+    for (int q = 0; q < 3; q++) p.pub[q] = 0;
+    p.hcnt[0] = p.hcnt[1] = 0;
+    p.cnt[0] = p.cnt[1] = p.cnt[2] = 0;
+    p.bq[0] = src;  // bucket 0 = {src}
+    p.btail[0] = 1;
+    p.bheavy[0] = (p.hv[src >> 5] >> (src & 31)) & 1u;
+    *p.status = 0;
+  }
+  if (tid < 64) s_head[tid] = s_hhead[tid] = 0;
+  {
+    WbfsWarpSmem &w = wbfs_smem();
+    w.hist[lane] = w.hist[lane + 32] = 0;
+    if (lane == 0) w.hist[XKEY] = 0;
+  }
+  grid.sync();
+
+  unsigned long long pend = 1;  // lists with pending entries: bucket 0's
+  unsigned long long k = 0;     // bucket being processed
+  bool taken = false;           // has bucket k's list been taken
+  long long r = 0;
+  for (;; r++) {
+    const int pr = (int)((r + 2) % 3), xr = (int)(r % 3);
+    if (tid == 0) {
+      s_ctl[0] = r ? ld_relaxed64(p.xcnt + pr) : 0;
+      s_ctl[1] = r ? ld_relaxed64(p.xcnt + 3 + pr) : 0;
+      s_ctl[2] = r ? ld_relaxed64(p.pub + pr) : 0;
+    }
+    if (tid < nbq) {  // only the chosen list's counters are used: no warp appends to it this round
+      s_ctl[3 + tid] = ld_relaxed64(p.btail + tid);
+      s_ctl[3 + 64 + tid] = ld_relaxed64(p.bheavy + tid);
+    }
+    __syncthreads();
+    pend |= s_ctl[2];
+    const uint32_t *Q;
+    unsigned long long qm, h, t;
+    bool heavy_any;
+    int slot = -1;
+    if (s_ctl[0] > 0) {  // near list of bucket k (delta > 1 or zero weights)
+      Q = p.xq[pr];
+      qm = ~0ull;
+      h = 0;
+      t = s_ctl[0];
+      heavy_any = s_ctl[1] > 0;
+    } else {  // next bucket: the smallest j >= k (+1 once taken) with a pending list
+      const unsigned long long j0 = taken ? k + 1 : k;
+      const int sh = (int)(j0 & (unsigned long long)(nbq - 1));
+      const unsigned long long all = (nbq == 64) ? ~0ull : ((1ull << nbq) - 1);
+      const unsigned long long rot = ((pend >> sh) | (sh ? (pend << (nbq - sh)) : 0ull)) & all;
+      if (rot == 0) break;  // every bucket list is empty: done
+      k = j0 + (unsigned long long)(__ffsll((long long)rot) - 1);
+      taken = true;
+      slot = (int)(k & (unsigned long long)(nbq - 1));
+      pend &= ~(1ull << slot);
+      Q = p.bq + (unsigned long long)slot * p.qcap;
+      qm = qmask;
+      h = s_head[slot];
+      t = s_ctl[3 + slot];
+      heavy_any = s_ctl[3 + 64 + slot] > s_hhead[slot];
+    }
+    if (r >= p.max_rounds) {
+      if (blockIdx.x == 0 && tid == 0) *p.status = 1;
+      break;
+    }
+    __syncthreads();
+    if (tid == 0 && slot >= 0) {
+      s_head[slot] = t;
+      s_hhead[slot] = s_ctl[3 + 64 + slot];
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      const int nr = (int)((r + 1) % 3);  // idle this round; appended to next round
+      p.xcnt[nr] = p.xcnt[3 + nr] = 0;
+      p.pub[nr] = 0;
+      p.cnt[nr] = 0;
+      p.hcnt[(r + 1) & 1] = 0;
+      if (STATS && p.stats && r < p.stats_cap) {
+        p.stats[r].dense = slot >= 0 ? 3 : 4;
+        p.stats[r].bucket = (int32_t)k;
+        p.stats[r].frontier = (long long)(t - h);
+        p.stats[r].t_start_ns = (long long)globaltimer_ns();
+      }
+    }
+    WarpState ws;
+    ws.bk = k;
+    // A large bucket (more entries than lanes in the grid) is first compacted into
+    // a frontier list carrying edge prefixes (one packed atomicAdd per warp, as
+    // warp_flush) and then pushed in fixed-size edge tiles — edgeMapBlocked's
+    // load balance for the rounds that carry most of the edges.  A
+    // small one is swept directly, one vertex per lane, saving a grid barrier.
+    const bool big = (t - h) > 32ull * (unsigned long long)nw;
+    for (unsigned long long i0 = h + 32ull * (unsigned long long)gw; i0 < t;
+         i0 += 32ull * (unsigned long long)nw) {
+      const unsigned long long i = i0 + lane;
+      uint32_t v = 0, x = 0;
+      long long a = 0;
+      int dg = 0;
+      if (i < t) {
+        v = __ldcg(Q + (i & qm));
+        x = ld_relaxed(p.dist + v);
+        a = __ldg(p.off + v);
+        dg = (int)(__ldg(p.off + v + 1) - a);
+        if (x / p.delta != k) dg = 0;  // lazy deletion: v has moved to an earlier bucket
+        if (STATS) ws.swept += 1;
+      }
+      if (big) {  // stage the live entries; one packed atomicAdd per full stage
+        const unsigned bal = __ballot_sync(FULL, dg > 0);
+        if (dg > 0) wsm.stage[ws.scnt + __popc(bal & lanemask_lt())] = v;
+        ws.scnt += __popc(bal);
+        if (ws.scnt > WCAP - 32) {
+          warp_flush<ALGO_WBFS>(p, wsm.stage, ws.scnt, 0, (int)r, nullptr, nullptr, p.cnt + xr);
+          ws.scnt = 0;
+        }
+      } else {
+        push_vertices<ALGO_WBFS, STATS, EMIT_LIST>(p, wsm, ws, v, a, dg, x, p.hcnt + (r & 1), 0,
+                                                   (int)r, nullptr, nullptr);
+      }
+    }
+    if (big) {
+      if (ws.scnt > 0) {
+        warp_flush<ALGO_WBFS>(p, wsm.stage, ws.scnt, 0, (int)r, nullptr, nullptr, p.cnt + xr);
+        ws.scnt = 0;
+      }
+      grid.sync();
+      if (tid == 0) s.cnt = ld_relaxed64(p.cnt + xr);
+      __syncthreads();
+      const unsigned long long c = s.cnt;
+      const long long f = (long long)(c >> p.ebits);
+      const long long E = (long long)(c & ((1ull << p.ebits) - 1));
+      if (STATS && p.stats && r < p.stats_cap && blockIdx.x == 0 && tid == 0)
+        p.stats[r].frontier_edges = E;
+      if (f > 0)
+        list_round<ALGO_WBFS, STATS, EMIT_LIST>(p, wsm, ws, 0, f, E, 0, (int)r, nullptr, nullptr,
+                                                gw, nw);
+    } else if (heavy_any) {  // hubs of this bucket, spread over all warps in list tiles
+      grid.sync();
+      if (tid == 0) s.hcnt = ld_relaxed64(p.hcnt + (r & 1));
+      __syncthreads();
+      const unsigned long long hc = s.hcnt;
+      const long long hf = (long long)(hc >> p.ebits);
+      const long long hE = (long long)(hc & ((1ull << p.ebits) - 1));
+      if (hf > 0)
+        list_round<ALGO_WBFS, STATS, EMIT_LIST>(p, wsm, ws, LIST_HEAVY, hf, hE, 0, (int)r, nullptr,
+                                                nullptr, gw, nw);
+    }
+    if (ws.scnt > 0) wbfs_flush<STATS>(p, ws, wsm.stage, ws.scnt, (int)r);
+    // publish the lists this warp appended to
+    unsigned long long pm = ws.pmask;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pm |= __shfl_xor_sync(FULL, pm, o);
+    if (lane == 0 && pm) atomicOr(p.pub + xr, pm);
+    if (STATS && p.stats && r < p.stats_cap) {
+      const unsigned long long e = warp_sum64((long long)ws.edges);
+      const unsigned long long sw = warp_sum64((long long)ws.swept);
+      const unsigned long long aq = warp_sum64((long long)ws.acquired);
+      if (lane == 0) {
+        if (e) atomicAdd((unsigned long long *)&p.stats[r].edges_examined, e);
+        if (sw) atomicAdd((unsigned long long *)&p.stats[r].vertices_swept, sw);
+        if (aq) atomicAdd((unsigned long long *)&p.stats[r].acquired, aq);
+      }
+    }
+    grid.sync();
+  }
+  if (STATS && blockIdx.x == 0 && tid == 0 && p.stats && r < p.stats_cap)
+    p.stats[r].t_start_ns = (long long)globaltimer_ns();
   if (blockIdx.x == 0 && tid == 0) *p.rounds_out = r;
 }
 

@@ -24,7 +24,7 @@ GBBS_MODE_AUTO, GBBS_MODE_SPARSE, GBBS_MODE_DENSE = 0, 1, 2
 
 EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_bfs",
            "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
-           "gbbs_widest_path_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
+           "gbbs_widest_path_ex", "gbbs_wbfs", "gbbs_wbfs_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
            "gbbs_launch_info", "gbbs_last_error")
 
 
@@ -36,11 +36,12 @@ class GbbsError(RuntimeError):
 
 class gbbs_opts(ctypes.Structure):
     _fields_ = [("threshold_den", ctypes.c_uint32), ("mode", ctypes.c_int32),
-                ("ctas_per_sm", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 5)]
+                ("ctas_per_sm", ctypes.c_uint32), ("delta", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 4)]
 
 
 class gbbs_round_stat(ctypes.Structure):
-    _fields_ = [("dense", ctypes.c_int32), ("reserved", ctypes.c_int32),
+    _fields_ = [("dense", ctypes.c_int32), ("bucket", ctypes.c_int32),
                 ("frontier", ctypes.c_int64), ("frontier_edges", ctypes.c_int64),
                 ("acquired", ctypes.c_int64), ("edges_examined", ctypes.c_int64),
                 ("vertices_swept", ctypes.c_int64), ("t_start_ns", ctypes.c_int64),
@@ -67,6 +68,8 @@ def _load():
     lib.gbbs_bfs_ex.argtypes = [p, u32, p, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_bellman_ford_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_widest_path.argtypes = [p, u32, p, p]
+    lib.gbbs_wbfs.argtypes = [p, u32, p, p]
+    lib.gbbs_wbfs_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_betweenness.argtypes = [p, u32, p, p]
     lib.gbbs_betweenness_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_widest_path_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
@@ -76,8 +79,8 @@ def _load():
     lib.gbbs_last_error.argtypes = []
     lib.gbbs_last_error.restype = ctypes.c_char_p
     for f in ("gbbs_graph_create", "gbbs_graph_info", "gbbs_bfs", "gbbs_bellman_ford", "gbbs_bfs_ex",
-              "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_betweenness",
-              "gbbs_betweenness_ex", "gbbs_launch_info"):
+              "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_wbfs",
+              "gbbs_wbfs_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -165,6 +168,16 @@ def gbbs_widest_path(handle, src, width, stream=None, opts=None, stats=None):
                                        ctypes.byref(stats) if stats is not None else None))
 
 
+def gbbs_wbfs(handle, src, dist, stream=None, opts=None, stats=None):
+    st = _stream(stream, dist)
+    if opts is None and stats is None:
+        _check(lib.gbbs_wbfs(handle, int(src), _ptr(dist), st))
+    else:
+        _check(lib.gbbs_wbfs_ex(handle, int(src), _ptr(dist), st,
+                                ctypes.byref(opts) if opts is not None else None,
+                                ctypes.byref(stats) if stats is not None else None))
+
+
 def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
     st = _stream(stream, delta)
     if stats is None:
@@ -173,12 +186,13 @@ def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
         _check(lib.gbbs_betweenness_ex(handle, int(src), _ptr(delta), st, None, ctypes.byref(stats)))
 
 
-def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0):
+def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0):
     o = gbbs_opts()
     lib.gbbs_default_opts(ctypes.byref(o))
     o.threshold_den = threshold_den
     o.mode = mode
     o.ctas_per_sm = ctas_per_sm
+    o.delta = delta
     return o
 
 
@@ -203,7 +217,7 @@ def round_records(stats):
     out = []
     for i, r in enumerate(raw[:n]):
         us = (raw[i + 1].t_start_ns - r.t_start_ns) / 1e3 if i + 1 < len(raw) else None
-        out.append(dict(dense=r.dense, frontier=r.frontier, frontier_edges=r.frontier_edges,
+        out.append(dict(dense=r.dense, bucket=r.bucket, frontier=r.frontier, frontier_edges=r.frontier_edges,
                         acquired=r.acquired, edges_examined=r.edges_examined,
                         vertices_swept=r.vertices_swept, us=us,
                         work_us=(r.t_work_ns - r.t_start_ns) / 1e3,
@@ -253,6 +267,9 @@ class Graph:
 
     def widest_path(self, src, width, stream=None, opts=None, stats=None):
         gbbs_widest_path(self.handle, src, width, stream, opts, stats)
+
+    def wbfs(self, src, dist, stream=None, opts=None, stats=None):
+        gbbs_wbfs(self.handle, src, dist, stream, opts, stats)
 
     def betweenness(self, src, delta, stream=None, stats=None):
         gbbs_betweenness(self.handle, src, delta, stream, stats)

@@ -48,6 +48,13 @@ def gpu_bf(G, g, n, s):
     return d.cpu().numpy().view(np.uint32)
 
 
+def gpu_wbfs(G, g, n, s, delta=0):
+    d = torch.empty(n, dtype=torch.int32, device="cuda")
+    st = G.make_stats(1 << 16)
+    g.wbfs(s, d, opts=G.make_opts(delta=delta), stats=st)
+    return d.cpu().numpy().view(np.uint32), st
+
+
 def test_c1_full(G):
     D, H = build("c1", True)
     g = G.Graph(D["offsets"], D["targets"], D["weights"], symmetric=True)
@@ -86,8 +93,13 @@ def test_c3_full(G):
     lv = torus_level_counts(L)
     assert st.rounds == len(lv) == 385
     assert [r["frontier"] for r in G.round_records(st)] == list(lv)
+    ref = oracle.dijkstra(H["off"], H["tgt"], H["w"], 0)[0]
     bf = gpu_bf(G, g, n, 0)
-    assert (bf == oracle.dijkstra(H["off"], H["tgt"], H["w"], 0)[0]).all()
+    assert (bf == ref).all()
+    # NEXT-2 wBFS, bucket width 1: one round per distinct distance
+    wb, st = gpu_wbfs(G, g, n, 0)
+    assert (wb == ref).all()
+    assert st.rounds == np.unique(ref).size
     g.close()
 
 
@@ -98,6 +110,9 @@ def test_c4_full(G):
     for s in D["sources"][:2]:
         bf = gpu_bf(G, g, n, s)
         assert oracle.check_sssp(H["off"], H["tgt"], H["w"], s, bf)[0], s
+        wb, st = gpu_wbfs(G, g, n, s)                     # NEXT-2: same distances
+        assert (wb == bf).all(), s
+        assert st.rounds == np.unique(bf[bf != 0xFFFFFFFF]).size
     s = D["sources"][0]
     d, p, _ = gpu_bfs(G, g, n, s)
     assert oracle.check_bfs(H["off"], H["tgt"], s, d, p)[0]

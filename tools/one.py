@@ -19,22 +19,27 @@ def main():
     ap.add_argument("--T", type=int, default=20)
     ap.add_argument("--src", type=int, default=0, help="index into the config's sources")
     ap.add_argument("--ctas", type=int, default=0, help="CTAs per SM (0 = max)")
+    ap.add_argument("--delta", type=int, default=0, help="wbfs bucket width (0 = default)")
     a = ap.parse_args()
     import torch
     from graphgen import device as gdev
     from paper_1805_05208_b200 import gbbs
-    G = gdev.build_config(a.config, weights=a.algo == "bf")
+    G = gdev.build_config(a.config, weights=a.algo != "bfs")
     g = gbbs.Graph(G["offsets"], G["targets"], G["weights"], symmetric=G["symmetric"])
     d = torch.empty(G["n"], dtype=torch.int32, device="cuda")
     p = torch.empty_like(d)
-    opts = gbbs.make_opts(a.T, {"auto": 0, "sparse": 1, "dense": 2}[a.mode], a.ctas)
+    opts = gbbs.make_opts(a.T, {"auto": 0, "sparse": 1, "dense": 2}[a.mode], a.ctas, a.delta)
     s = G["sources"][a.src]
     for _ in range(a.reps):
         st = gbbs.make_stats(0)
         if a.algo == "bfs":
             g.bfs(s, d, p, opts=opts, stats=st)
-        else:
+        elif a.algo == "bf":
             g.bellman_ford(s, d, opts=opts, stats=st)
+        elif a.algo == "wbfs":
+            g.wbfs(s, d, opts=opts, stats=st)
+        else:
+            g.widest_path(s, d, opts=opts, stats=st)
         print(f"{a.config} {a.algo} src={s} kernel {st.kernel_ms * 1e3:.1f} us", flush=True)
     torch.cuda.synchronize()
 

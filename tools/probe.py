@@ -15,6 +15,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def run_algo(g, algo, s, d, p, opts, st):
+    if algo == "bfs":
+        g.bfs(s, d, p, opts=opts, stats=st)
+    elif algo == "bf":
+        g.bellman_ford(s, d, opts=opts, stats=st)
+    elif algo == "wbfs":
+        g.wbfs(s, d, opts=opts, stats=st)
+    else:
+        g.widest_path(s, d, opts=opts, stats=st)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c2")
@@ -22,6 +33,7 @@ def main():
     ap.add_argument("--nsrc", type=int, default=1)
     ap.add_argument("--mode", default="auto")
     ap.add_argument("--T", type=int, default=20)
+    ap.add_argument("--delta", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--rounds", action="store_true", help="print every round")
     ap.add_argument("--check", action="store_true", help="certify against the oracle certificate")
@@ -43,20 +55,14 @@ def main():
         for algo in a.algos.split(","):
             for s in G["sources"][: a.nsrc]:
                 st = gbbs.make_stats(1 << 17)
-                opts = gbbs.make_opts(a.T, mode)
-                if algo == "bfs":
-                    g.bfs(s, d, p, opts=opts, stats=st)
-                else:
-                    g.bellman_ford(s, d, opts=opts, stats=st)
+                opts = gbbs.make_opts(a.T, mode, delta=a.delta)
+                run_algo(g, algo, s, d, p, opts, st)
                 recs = gbbs.round_records(st)
                 mreach = int((off[1:] - off[:-1])[d != -1].sum())
                 kms = []
                 for _ in range(a.reps):
                     s2 = gbbs.make_stats(0)
-                    if algo == "bfs":
-                        g.bfs(s, d, p, opts=opts, stats=s2)
-                    else:
-                        g.bellman_ford(s, d, opts=opts, stats=s2)
+                    run_algo(g, algo, s, d, p, opts, s2)
                     kms.append(s2.kernel_ms)
                 km = float(np.median(kms))
                 tot_us = sum(r["us"] or 0 for r in recs)
@@ -65,7 +71,7 @@ def main():
                       f"GTEPS={mreach / km / 1e6:.1f}", flush=True)
                 if a.rounds or st.rounds <= 40:
                     for i, r in enumerate(recs):
-                        print(f"   r{i:<4d} {'D' if r['dense'] else 'S'} U={r['frontier']:>10d} "
+                        print(f"   r{i:<4d} {'SDFBN'[r['dense']]} k={r['bucket']:<6d} U={r['frontier']:>10d} "
                               f"E={r['frontier_edges']:>11d} acq={r['acquired']:>9d} "
                               f"ex={r['edges_examined']:>11d} sw={r['vertices_swept']:>9d} "
                               f"{(r['us'] or 0):9.1f}us  work<{r['work_us']:.1f} flush<{r['flush_us']:.1f}")
@@ -74,6 +80,8 @@ def main():
                     fr = np.array([r["frontier"] for r in recs])
                     wk = np.array([r["work_us"] for r in recs])
                     fl = np.array([r["flush_us"] for r in recs])
+                    print(f"   totals: entries {sum(r['frontier'] for r in recs)} edges "
+                          f"{sum(r['edges_examined'] for r in recs)} acquired {sum(r['acquired'] for r in recs)}")
                     print(f"   per-round us: median {np.median(us):.2f} p90 {np.percentile(us, 90):.2f} "
                           f"max {us.max():.1f}; work-end median {np.median(wk):.2f} flush-end median "
                           f"{np.median(fl):.2f}; frontier median {np.median(fr):.0f} max {fr.max()}")
