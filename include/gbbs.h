@@ -194,6 +194,32 @@ int gbbs_betweenness(const gbbs_graph *g, uint32_t src, double *delta,
 int gbbs_wbfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
               void *cuda_stream);
 
+/*
+ * gbbs_bellman_ford_signed — general-weight SSSP by frontier Bellman-Ford
+ * (output spec P:1487-1490, sec:benchmark; algorithm, sec:algs) with the
+ * graph's weights read as int32 (two's complement of the uint32 weights given
+ * at create; NULL weights = 1).
+ *
+ * dist    int64[n], caller-owned, host or device: the shortest-path distance
+ *         from src; GBBS_DIST_INF if unreachable.  If a negative-weight cycle
+ *         is reachable from src, "all distances must be -infinity":
+ *         with gbbs_opts.neg_scope = 0 (default) every entry is
+ *         GBBS_DIST_NEGINF; with neg_scope = 1 exactly the vertices reachable
+ *         from such a cycle are GBBS_DIST_NEGINF and the others keep their
+ *         finite distance or GBBS_DIST_INF.
+ * Cost: O(diam) rounds without a reachable negative cycle; with one, n rounds
+ * (the cycle is proven by a frontier that is still non-empty after round
+ * n - 1) plus, for neg_scope = 1, one edge pass and a reachability sweep.
+ * Same stream/synchronization conventions as gbbs_bfs.
+ * Errors: GBBS_EINVAL (g or dist NULL, src >= n, bad options), GBBS_ERANGE
+ *         if (n - 1) * max|w| >= 2^62, GBBS_ENOMEM (8n bytes of staging for
+ *         a host dist), GBBS_ECUDA.
+ */
+#define GBBS_DIST_INF INT64_MAX
+#define GBBS_DIST_NEGINF INT64_MIN
+int gbbs_bellman_ford_signed(const gbbs_graph *g, uint32_t src, int64_t *dist,
+                             void *cuda_stream);
+
 /* ---- extended calls (bench / tests) ------------------------------------ */
 
 /* Representation choice per round (threshold rule reading A10).
@@ -216,7 +242,13 @@ typedef struct {
                              paper's one bucket per distance) while
                              maxw <= 32, else ceil(maxw / 32).  Other
                              calls ignore it.                              */
-  uint32_t reserved[4];   /* must be zero                                  */
+  uint32_t neg_scope;     /* gbbs_bellman_ford_signed, when a negative cycle
+                             is reachable from src: 0 (default) = every
+                             distance is GBBS_DIST_NEGINF (PAPER.md:1489
+                             read literally, reading N1); 1 = exactly the
+                             vertices reachable from such a cycle
+                             (reading N2).  Other calls ignore it.         */
+  uint32_t reserved[3];   /* must be zero                                  */
 } gbbs_opts;
 
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */
@@ -266,6 +298,9 @@ int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
 int gbbs_betweenness_ex(const gbbs_graph *g, uint32_t src, double *delta,
                         void *cuda_stream, const gbbs_opts *opts,
                         gbbs_stats *stats);
+int gbbs_bellman_ford_signed_ex(const gbbs_graph *g, uint32_t src, int64_t *dist,
+                                void *cuda_stream, const gbbs_opts *opts,
+                                gbbs_stats *stats);
 int gbbs_wbfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                  void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats);
 int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *width,

@@ -222,3 +222,26 @@ def betweenness(offsets, targets, src, want_sigma=False):
     lib.oracle_bc.restype = ctypes.c_int
     _check(lib.oracle_bc(n, _ptr(off), _ptr(tgt), int(src), _ptr(delta), _ptr(sigma)), "oracle_bc")
     return delta, sigma
+
+
+DIST_INF = np.int64(np.iinfo(np.int64).max)
+DIST_NEGINF = np.int64(np.iinfo(np.int64).min)
+
+
+def bellman_ford_signed(offsets, targets, weights, src, scope=0):
+    """NEXT-4 general-weight SSSP, weights read as int32.
+    Returns (dist int64 with DIST_INF / DIST_NEGINF, negative_cycle_reachable).
+    scope 0: every distance -inf on a reachable negative cycle (reading N1);
+    scope 1: only the cycle's forward closure (reading N2)."""
+    n, off, tgt, w = _csr(offsets, targets, weights)
+    dist = np.empty(n, np.int64)
+    neg = ctypes.c_int(0)
+    lib = _load()
+    lib.oracle_bellman_ford_signed.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int,
+                                               ctypes.c_void_p, ctypes.c_void_p]
+    lib.oracle_bellman_ford_signed.restype = ctypes.c_int
+    _check(lib.oracle_bellman_ford_signed(n, _ptr(off), _ptr(tgt), _ptr(w), int(src), int(scope),
+                                          _ptr(dist), ctypes.addressof(neg)),
+           "oracle_bellman_ford_signed")
+    return dist, bool(neg.value)

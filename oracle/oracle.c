@@ -580,3 +580,95 @@ int oracle_bc(int64_t n, const int64_t *off, const uint32_t *tgt, uint32_t src,
   free(order); free(d); free(sigma);
   return ORACLE_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: general-weight SSSP (sec:benchmark "General- */
+/* Weight SSSP (Bellman-Ford)"): D[v] = shortest-path distance from src,    */
+/* infinity if unreachable; "All distances must be -infinity if G contains  */
+/* a negative-weight cycle reachable from src".  Weights are int32 (w[e]    */
+/* read as two's complement; NULL = unit weights), distances int64 with     */
+/* INT64_MAX = infinity and INT64_MIN = -infinity.                          */
+/*                                                                          */
+/* Textbook Bellman-Ford: n-1 passes relaxing every edge (u,v) with D[u]    */
+/* finite.  Afterwards an edge that still relaxes proves a negative cycle   */
+/* reachable from src (a walk beating every simple path), and every         */
+/* reachable negative cycle has such an edge.  scope 0 (reading N1, the     */
+/* sentence read literally): then every D[v] = -infinity.  scope 1 (reading */
+/* N2): D[v] = -infinity exactly for v reachable from the target of a still */
+/* relaxing edge (depth-first search over out-edges).  *negcycle = 1 if a   */
+/* reachable negative cycle exists.  Distances of simple paths fit int64    */
+/* when (n-1) * max|w| < 2^62; larger inputs return ORACLE_ERANGE.          */
+/* ------------------------------------------------------------------------ */
+int oracle_bellman_ford_signed(int64_t n, const int64_t *off, const uint32_t *tgt,
+                               const uint32_t *w, uint32_t src, int scope,
+                               int64_t *dist, int *negcycle) {
+  int rc = check_args(n, off, tgt, src);
+  if (rc) return rc;
+  if (dist == NULL || (scope != 0 && scope != 1)) return ORACLE_EINVAL;
+  const int64_t m = off[n];
+  int64_t maxabs = 1;
+  for (int64_t e = 0; w && e < m; e++) {
+    int64_t x = (int32_t)w[e];
+    if (x < 0) x = -x;
+    if (x > maxabs) maxabs = x;
+  }
+  if ((n - 1) > ((INT64_C(1) << 62) - 1) / maxabs) return ORACLE_ERANGE;
+  for (int64_t v = 0; v < n; v++) dist[v] = INT64_MAX;
+  dist[src] = 0;
+  for (int64_t pass = 0; pass < n - 1; pass++) {
+    int changed = 0;
+    for (int64_t u = 0; u < n; u++) {
+      if (dist[u] == INT64_MAX) continue;
+      for (int64_t e = off[u]; e < off[u + 1]; e++) {
+        int64_t nd = dist[u] + (w ? (int64_t)(int32_t)w[e] : 1);
+        if (nd < dist[tgt[e]]) {
+          dist[tgt[e]] = nd;
+          changed = 1;
+        }
+      }
+    }
+    if (!changed) break;
+  }
+  /* pass n: edges that still relax */
+  unsigned char *mark = (unsigned char *)calloc((size_t)n, 1);
+  int64_t *stack = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+  if (!mark || !stack) {
+    free(mark);
+    free(stack);
+    return ORACLE_ENOMEM;
+  }
+  int64_t sp = 0;
+  int found = 0;
+  for (int64_t u = 0; u < n; u++) {
+    if (dist[u] == INT64_MAX) continue;
+    for (int64_t e = off[u]; e < off[u + 1]; e++) {
+      int64_t nd = dist[u] + (w ? (int64_t)(int32_t)w[e] : 1);
+      if (nd < dist[tgt[e]]) {
+        found = 1;
+        if (!mark[tgt[e]]) {
+          mark[tgt[e]] = 1;
+          stack[sp++] = tgt[e];
+        }
+      }
+    }
+  }
+  if (negcycle) *negcycle = found;
+  if (found && scope == 0) {
+    for (int64_t v = 0; v < n; v++) dist[v] = INT64_MIN;
+  } else if (found) {
+    while (sp > 0) { /* forward closure of the seeds */
+      int64_t u = stack[--sp];
+      for (int64_t e = off[u]; e < off[u + 1]; e++) {
+        if (!mark[tgt[e]]) {
+          mark[tgt[e]] = 1;
+          stack[sp++] = tgt[e];
+        }
+      }
+    }
+    for (int64_t v = 0; v < n; v++)
+      if (mark[v]) dist[v] = INT64_MIN;
+  }
+  free(mark);
+  free(stack);
+  return ORACLE_OK;
+}

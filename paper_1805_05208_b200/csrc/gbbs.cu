@@ -16,6 +16,7 @@
 
 #include "../../include/gbbs.h"
 #include "traverse.cuh"
+#include "sbf.cuh"
 
 using namespace gbbs_dev;
 
@@ -80,6 +81,9 @@ struct gbbs_graph {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   struct BcScratch *bc = nullptr;  // betweenness scratch (lazy)
   struct WbfsScratch *wb = nullptr;  // wBFS bucket structure (lazy)
+  long long *tmp_sdist = nullptr;    // signed BF: int64 staging for host outputs
+  long long smaxabs = -1;            // signed BF: max |w| of the weights read as int32
+  int sgrid[2] = {0, 0};
 };
 
 static void free_bc(gbbs_graph *g);
@@ -109,6 +113,7 @@ static void free_graph(gbbs_graph *g) {
   if (g->ev[1]) cudaEventDestroy(g->ev[1]);
   free_bc(g);
   free_wbfs(g);
+  cudaFree(g->tmp_sdist);
   delete g;
 }
 
@@ -142,6 +147,19 @@ __global__ void k_maxw(const uint32_t *w, long long m, unsigned int *out) {
     atomicMax(out, mx);
     atomicMin(out + 1, mn);
   }
+}
+
+// max |w| over the weights read as int32 (signed Bellman-Ford range check)
+__global__ void k_absmax_i32(const uint32_t *w, long long m, unsigned long long *out) {
+  long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long gs = (long long)gridDim.x * blockDim.x;
+  unsigned long long mx = 0;
+  for (long long e = gt; e < m; e += gs) {
+    const long long x = (long long)(int32_t)w[e];
+    mx = max(mx, (unsigned long long)(x < 0 ? -x : x));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
 // bit v set iff out-degree(v) > HEAVY (wBFS: insertions count the hubs of a bucket)
@@ -588,7 +606,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   if (opts) {
     o = *opts;
     if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < 3; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.mode < 0 || o.mode > 2) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
   }
@@ -760,6 +778,148 @@ extern "C" int gbbs_bellman_ford_ex(const gbbs_graph *g, uint32_t src, uint32_t 
   return run(g, ALGO_BF, src, dist, nullptr, cuda_stream, opts, stats);
 }
 
+// ---------------------------------------------------------------------------
+// NEXT-4: general-weight (signed) Bellman-Ford (sbf.cuh)
+// ---------------------------------------------------------------------------
+template <bool STATS>
+static int sbf_launch(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+  if (!g->sgrid[STATS]) {
+    int nsm = 0, per = 0;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sbf_kernel<STATS>, BLOCK, 0));
+    if (per < 1) return fail(GBBS_ECUDA, "signed Bellman-Ford kernel cannot be resident");
+    g->sgrid[STATS] = per * nsm;
+  }
+  void *args[] = {&p};
+  if (ev0) CU(cudaEventRecord(ev0, st));
+  CU(cudaLaunchCooperativeKernel((const void *)sbf_kernel<STATS>, g->sgrid[STATS], BLOCK, args, 0, st));
+  if (ev1) CU(cudaEventRecord(ev1, st));
+  return GBBS_OK;
+}
+
+extern "C" int gbbs_bellman_ford_signed_ex(const gbbs_graph *cg_, uint32_t src, int64_t *dist,
+                                           void *cuda_stream, const gbbs_opts *opts,
+                                           gbbs_stats *stats) {
+  g_last_error.clear();
+  if (!cg_) return fail(GBBS_EINVAL, "g is NULL");
+  gbbs_graph *g = const_cast<gbbs_graph *>(cg_);
+  if (!dist) return fail(GBBS_EINVAL, "dist is NULL");
+  if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
+  gbbs_opts o;
+  gbbs_default_opts(&o);
+  if (opts) {
+    o = *opts;
+    for (int i = 0; i < 3; i++)
+      if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
+    if (o.neg_scope > 1) return fail(GBBS_EINVAL, "bad neg_scope %u", o.neg_scope);
+  }
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  if (dev != g->device) CU(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (g->smaxabs < 0) {
+    g->smaxabs = 1;
+    if (g->wgt && g->m > 0) {
+      unsigned long long *d = nullptr;
+      CU(cudaMalloc(&d, 8));
+      CU(cudaMemset(d, 0, 8));
+      k_absmax_i32<<<1184, 256>>>(g->wgt, g->m, d);
+      cudaError_t e = cudaGetLastError();
+      unsigned long long h = 0;
+      if (e == cudaSuccess) e = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+      cudaFree(d);
+      if (e != cudaSuccess) return fail(GBBS_ECUDA, "max |w|: %s", cudaGetErrorString(e));
+      g->smaxabs = (long long)h;
+    }
+  }
+  // every simple path stays above FLOOR = -2^62 and below +2^62
+  if (g->smaxabs > 0 && (unsigned long long)(g->n - 1) > ((1ull << 62) - 1) / (unsigned long long)g->smaxabs)
+    return fail(GBBS_ERANGE, "(n-1) * max|w| = %lld * %lld does not fit in 2^62", g->n - 1, g->smaxabs);
+  const bool dev_out = is_device_ptr(dist);
+  if (!dev_out && !g->tmp_sdist) CU(cudaMalloc(&g->tmp_sdist, (size_t)g->n * 8));
+  long long *dd = dev_out ? (long long *)dist : g->tmp_sdist;
+
+  const bool want_rounds = stats && stats->rounds_out && stats->rounds_cap > 0;
+  long long cap = 0;
+  if (want_rounds) {
+    cap = stats->rounds_cap;
+    if (g->dstats_cap < cap) {
+      cudaFree(g->dstats);
+      g->dstats = nullptr;
+      g->dstats_cap = 0;
+      CU(cudaMalloc(&g->dstats, (size_t)cap * sizeof(RoundStat)));
+      g->dstats_cap = cap;
+    }
+    CU(cudaMemsetAsync(g->dstats, 0, (size_t)cap * sizeof(RoundStat), st));
+  }
+  Params p;
+  memset(&p, 0, sizeof p);
+  p.n = g->n;
+  p.m = g->m;
+  p.off = g->off;
+  p.tgt = g->tgt;
+  p.wgt = g->wgt;
+  p.sdist = dd;
+  p.bm[0] = g->bm[0];
+  p.bm[1] = g->bm[1];
+  for (int i = 0; i < 3; i++) {
+    p.fv[i] = g->fv[i];
+    p.fo[i] = g->fo[i];
+    p.fb[i] = g->fb[i];
+  }
+  p.cnt = g->cnt;
+  p.status = g->status;
+  p.rounds_out = g->rounds;
+  p.stats = want_rounds ? g->dstats : nullptr;
+  p.stats_cap = cap;
+  p.nwords = g->nwords;
+  p.max_rounds = g->n;  // n rounds: a frontier left after them proves a negative cycle
+  p.ebits = g->ebits;
+  p.neg_scope = (int)o.neg_scope;
+  p.src = src;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (stats) {
+    if (!g->ev[0]) {
+      CU(cudaEventCreate(&g->ev[0]));
+      CU(cudaEventCreate(&g->ev[1]));
+    }
+    ev0 = g->ev[0];
+    ev1 = g->ev[1];
+  }
+  int rc = want_rounds ? sbf_launch<true>(g, p, st, ev0, ev1) : sbf_launch<false>(g, p, st, ev0, ev1);
+  if (rc) return rc;
+  if (!dev_out) CU(cudaMemcpyAsync(dist, dd, (size_t)g->n * 8, cudaMemcpyDeviceToHost, st));
+  struct {
+    int status;
+    int pad;
+    long long rounds;
+  } ctrl;
+  CU(cudaMemcpyAsync(&ctrl, g->status, 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (stats) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ev0, ev1));
+    stats->kernel_ms = ms;
+    stats->rounds = ctrl.rounds;
+    stats->dense_rounds = 0;
+    stats->edges_examined = 0;
+    stats->reached = -1;
+    if (want_rounds) {
+      long long nr = ctrl.rounds + 1 < cap ? ctrl.rounds + 1 : cap;
+      CU(cudaMemcpy(stats->rounds_out, g->dstats, (size_t)nr * sizeof(RoundStat),
+                    cudaMemcpyDeviceToHost));
+      for (long long i = 0; i < nr && i < ctrl.rounds; i++)
+        stats->edges_examined += stats->rounds_out[i].edges_examined;
+    }
+  }
+  return GBBS_OK;
+}
+
+extern "C" int gbbs_bellman_ford_signed(const gbbs_graph *g, uint32_t src, int64_t *dist,
+                                        void *cuda_stream) {
+  return gbbs_bellman_ford_signed_ex(g, src, dist, cuda_stream, nullptr, nullptr);
+}
+
 extern "C" int gbbs_wbfs(const gbbs_graph *g, uint32_t src, uint32_t *dist, void *cuda_stream) {
   return run(g, ALGO_WBFS, src, dist, nullptr, cuda_stream, nullptr, nullptr);
 }
@@ -835,7 +995,7 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   if (!delta) return fail(GBBS_EINVAL, "delta is NULL");
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   if (opts)
-      for (int i = 0; i < 4; i++)
+      for (int i = 0; i < 3; i++)
       if (opts->reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
   int rc = GBBS_OK;
   BcScratch *b = bc_scratch(g, &rc);

@@ -116,6 +116,9 @@ struct Params {
   unsigned long long qcap;   // per-list capacity (power of two >= n)
   uint32_t delta;            // bucket width
   int nbq;                   // number of bucket lists (power of two)
+  // signed Bellman-Ford (sbf_kernel)
+  long long *sdist;          // [n] int64 distances
+  int neg_scope;             // 0: all -inf on a negative cycle, 1: its forward closure
 #ifdef GBBS_DBG_PHASE
   unsigned long long *dbg;   // [64][4] per-round max phase durations (ns)
 #endif

@@ -19,12 +19,15 @@ LIB_PATH = os.environ.get("GBBS_LIB") or os.path.join(_HERE, "libgbbs.so")
 
 GBBS_OK, GBBS_EINVAL, GBBS_ERANGE, GBBS_ENOMEM, GBBS_ECUDA, GBBS_EINTERNAL = 0, -1, -2, -3, -4, -5
 GBBS_INF = 0xFFFFFFFF
+GBBS_DIST_INF = np.iinfo(np.int64).max
+GBBS_DIST_NEGINF = np.iinfo(np.int64).min
 GBBS_SYMMETRIC, GBBS_BORROW, GBBS_NO_VALIDATE = 0x1, 0x2, 0x4
 GBBS_MODE_AUTO, GBBS_MODE_SPARSE, GBBS_MODE_DENSE = 0, 1, 2
 
 EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_bfs",
            "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
-           "gbbs_widest_path_ex", "gbbs_wbfs", "gbbs_wbfs_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
+           "gbbs_widest_path_ex", "gbbs_wbfs", "gbbs_wbfs_ex", "gbbs_bellman_ford_signed",
+           "gbbs_bellman_ford_signed_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
            "gbbs_launch_info", "gbbs_last_error")
 
 
@@ -37,7 +40,7 @@ class GbbsError(RuntimeError):
 class gbbs_opts(ctypes.Structure):
     _fields_ = [("threshold_den", ctypes.c_uint32), ("mode", ctypes.c_int32),
                 ("ctas_per_sm", ctypes.c_uint32), ("delta", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32 * 4)]
+                ("neg_scope", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 3)]
 
 
 class gbbs_round_stat(ctypes.Structure):
@@ -69,6 +72,9 @@ def _load():
     lib.gbbs_bellman_ford_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_widest_path.argtypes = [p, u32, p, p]
     lib.gbbs_wbfs.argtypes = [p, u32, p, p]
+    lib.gbbs_bellman_ford_signed.argtypes = [p, u32, p, p]
+    lib.gbbs_bellman_ford_signed_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts),
+                                                ctypes.POINTER(gbbs_stats)]
     lib.gbbs_wbfs_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_betweenness.argtypes = [p, u32, p, p]
     lib.gbbs_betweenness_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
@@ -80,7 +86,7 @@ def _load():
     lib.gbbs_last_error.restype = ctypes.c_char_p
     for f in ("gbbs_graph_create", "gbbs_graph_info", "gbbs_bfs", "gbbs_bellman_ford", "gbbs_bfs_ex",
               "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_wbfs",
-              "gbbs_wbfs_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
+              "gbbs_wbfs_ex", "gbbs_bellman_ford_signed", "gbbs_bellman_ford_signed_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -178,6 +184,17 @@ def gbbs_wbfs(handle, src, dist, stream=None, opts=None, stats=None):
                                 ctypes.byref(stats) if stats is not None else None))
 
 
+def gbbs_bellman_ford_signed(handle, src, dist, stream=None, opts=None, stats=None):
+    """dist: int64[n] (numpy or torch, host or device)."""
+    st = _stream(stream, dist)
+    if opts is None and stats is None:
+        _check(lib.gbbs_bellman_ford_signed(handle, int(src), _ptr(dist), st))
+    else:
+        _check(lib.gbbs_bellman_ford_signed_ex(handle, int(src), _ptr(dist), st,
+                                               ctypes.byref(opts) if opts is not None else None,
+                                               ctypes.byref(stats) if stats is not None else None))
+
+
 def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
     st = _stream(stream, delta)
     if stats is None:
@@ -186,13 +203,14 @@ def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
         _check(lib.gbbs_betweenness_ex(handle, int(src), _ptr(delta), st, None, ctypes.byref(stats)))
 
 
-def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0):
+def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0, neg_scope=0):
     o = gbbs_opts()
     lib.gbbs_default_opts(ctypes.byref(o))
     o.threshold_den = threshold_den
     o.mode = mode
     o.ctas_per_sm = ctas_per_sm
     o.delta = delta
+    o.neg_scope = neg_scope
     return o
 
 
@@ -270,6 +288,9 @@ class Graph:
 
     def wbfs(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_wbfs(self.handle, src, dist, stream, opts, stats)
+
+    def bellman_ford_signed(self, src, dist, stream=None, opts=None, stats=None):
+        gbbs_bellman_ford_signed(self.handle, src, dist, stream, opts, stats)
 
     def betweenness(self, src, delta, stream=None, stats=None):
         gbbs_betweenness(self.handle, src, delta, stream, stats)

@@ -185,3 +185,58 @@ def brute_force_dependencies(n: int, offsets, targets, src: int):
             if D[src][v] + D[v][t] == D[src][t]:
                 out[v] += C[src][v] * C[v][t] / C[src][t]
     return out
+
+
+# ---- NEXT-4 signed weights ----------------------------------------------------------
+
+def signed_csr(n: int, edges, weights):
+    """Directed CSR (sorted, duplicates keep the last weight) with int32 weights
+    returned as their uint32 two's-complement bit patterns (the ABI's layout)."""
+    wmap = {}
+    for (a, b), w in zip(edges, weights):
+        wmap[(a, b)] = int(w)
+    keys = sorted(wmap)
+    offsets = np.zeros(n + 1, np.int64)
+    for a, _ in keys:
+        offsets[a + 1] += 1
+    offsets = np.cumsum(offsets)
+    tgt = np.array([b for _, b in keys], np.uint32)
+    wt = np.array([wmap[k] for k in keys], np.int64).astype(np.int32).view(np.uint32)
+    return offsets, tgt, wt
+
+
+def signed_expected(n: int, offsets, targets, w_u32, src: int, scope: int):
+    """Independent of the oracle: Floyd–Warshall over int32 weights (exact in
+    float64 for small ints) finds negative cycles (D[k,k] < 0); a boolean
+    transitive closure gives reachability.  v is -inf iff some k with D[k,k] < 0
+    is reachable from src and reaches v (scope 1), or, with scope 0, iff any
+    such k exists at all.  Otherwise D[src, v] (inf if unreachable)."""
+    w = w_u32.view(np.int32).astype(np.float64)
+    D = floyd_warshall(n, offsets, targets, w)
+    R = np.eye(n, dtype=bool)
+    for u in range(n):
+        for e in range(offsets[u], offsets[u + 1]):
+            R[u, targets[e]] = True
+    for k in range(n):
+        R = R | (R[:, k:k + 1] & R[k:k + 1, :])
+    neg = np.array([D[k, k] < 0 for k in range(n)])
+    bad = neg & R[src]
+    out = np.empty(n, np.int64)
+    down = (R[bad].any(axis=0)) if bad.any() else np.zeros(n, bool)
+    for v in range(n):
+        if bad.any() and (scope == 0 or down[v]):
+            out[v] = np.iinfo(np.int64).min
+        elif not R[src, v]:
+            out[v] = np.iinfo(np.int64).max
+        else:
+            out[v] = int(D[src, v])
+    return out, bool(bad.any())
+
+
+def johnson_reweight(offsets, targets, w_u32, phi):
+    """w'(u,v) = w(u,v) + phi(u) - phi(v): same shortest paths, no new negative
+    cycles (every cycle keeps its weight), d'(v) = d(v) + phi(src) - phi(v)."""
+    u = np.repeat(np.arange(offsets.shape[0] - 1), np.diff(offsets))
+    w2 = w_u32.astype(np.int64) + phi[u] - phi[targets]
+    assert (np.abs(w2) < 2 ** 31).all()
+    return w2.astype(np.int32).view(np.uint32)

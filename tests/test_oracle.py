@@ -383,3 +383,82 @@ def test_bc_closed_forms_and_spec_examples():
     _, s = oracle.betweenness(off, tgt, 0, want_sigma=True)
     from math import comb
     assert all(s[x + a * y] == comb(x + y, x) for y in range(b) for x in range(a))
+
+
+# ---- NEXT-4 general-weight SSSP (signed weights, -inf) ------------------------------
+
+from pins import johnson_reweight, signed_csr, signed_expected  # noqa: E402
+
+NEGINF = np.iinfo(np.int64).min
+POSINF = np.iinfo(np.int64).max
+
+
+def test_signed_spec_examples():
+    # S:336-337 (SPEC examples of the paper's General-Weight SSSP)
+    off, tgt, w = signed_csr(3, [(0, 1), (1, 2)], [4, -2])
+    for scope in (0, 1):
+        d, neg = oracle.bellman_ford_signed(off, tgt, w, 0, scope)
+        assert list(d) == [0, 4, 2] and not neg
+    off, tgt, w = signed_csr(2, [(0, 1), (1, 0)], [1, -3])
+    for scope in (0, 1):
+        d, neg = oracle.bellman_ford_signed(off, tgt, w, 0, scope)
+        assert list(d) == [NEGINF, NEGINF] and neg
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_signed_brute_force_fw(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(2, 9))
+    edges = [(int(a), int(b)) for a in range(n) for b in range(n)
+             if a != b and rng.random() < 0.35]
+    ws = rng.integers(-4, 9, len(edges))
+    off, tgt, w = signed_csr(n, edges, ws)
+    for src in range(n):
+        for scope in (0, 1):
+            exp, eneg = signed_expected(n, off, tgt, w, src, scope)
+            got, neg = oracle.bellman_ford_signed(off, tgt, w, src, scope)
+            assert neg == eneg and (got == exp).all(), (seed, src, scope, got, exp)
+
+
+def test_signed_planted_cycles_scopes():
+    # 0 -> 1 -> 2 -> 0 has weight -1; 2 -> 3 -> 4 downstream; 5 reaches the cycle
+    # but is not reachable from it; 6 isolated
+    edges = [(0, 1), (1, 2), (2, 0), (2, 3), (3, 4), (5, 0)]
+    ws = [2, -4, 1, 7, -1, 3]
+    off, tgt, w = signed_csr(7, edges, ws)
+    d, neg = oracle.bellman_ford_signed(off, tgt, w, 0, 1)
+    assert neg and list(d[:5]) == [NEGINF] * 5 and d[5] == POSINF and d[6] == POSINF
+    d, neg = oracle.bellman_ford_signed(off, tgt, w, 0, 0)
+    assert neg and (d == NEGINF).all()
+    d, neg = oracle.bellman_ford_signed(off, tgt, w, 3, 1)   # cycle unreachable from 3
+    assert not neg and list(d) == [POSINF, POSINF, POSINF, 0, -1, POSINF, POSINF]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_signed_johnson_closed_form(seed):
+    off, tgt = graphgen.random_graph(300, 0.02, 500 + seed, symmetric=False)
+    w = graphgen.pair_weights(off, tgt, seed, 40)
+    phi = np.random.default_rng(seed).integers(-1000, 1000, off.shape[0] - 1).astype(np.int64)
+    w2 = johnson_reweight(off, tgt, w, phi)
+    assert (w2.view(np.int32) < 0).any()
+    for src in (0, 17):
+        ref, _ = oracle.dijkstra64(off, tgt, w, src)
+        got, neg = oracle.bellman_ford_signed(off, tgt, w2, src, 1)
+        fin = ref != np.uint64(0xFFFFFFFFFFFFFFFF)
+        assert not neg
+        assert (got[~fin] == POSINF).all()
+        assert (got[fin] == ref[fin].astype(np.int64) + phi[src] - phi[fin]).all()
+
+
+def test_signed_nonnegative_equals_dijkstra_and_range():
+    off, tgt = graphgen.random_graph(400, 0.01, 9, symmetric=True)
+    w = graphgen.pair_weights(off, tgt, 3, 100)
+    ref, _ = oracle.dijkstra64(off, tgt, w, 0)
+    got, neg = oracle.bellman_ford_signed(off, tgt, w, 0)
+    fin = ref != np.uint64(0xFFFFFFFFFFFFFFFF)
+    assert not neg and (got[fin] == ref[fin].astype(np.int64)).all() and (got[~fin] == POSINF).all()
+    d, _ = oracle.bellman_ford_signed(off, tgt, None, 0)          # NULL = unit weights
+    b, _ = oracle.bfs(off, tgt, 0)
+    assert (d[b != INF] == b[b != INF]).all()
+    off, tgt, w = signed_csr(3, [(0, 1), (1, 2)], [-(2 ** 31), 5])
+    assert oracle.bellman_ford_signed(off, tgt, w, 0)[0][2] == -(2 ** 31) + 5
