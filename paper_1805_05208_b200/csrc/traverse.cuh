@@ -124,7 +124,18 @@ struct Params {
 #endif
 };
 
-constexpr int SWEEP_WORDS = 32;        // bitmap words gathered per warp step (sweeps)
+constexpr int SWEEP_WORDS = 32;        // max bitmap words gathered per warp step (sweeps)
+// Sweep unit (words per warp step, a power of two <= SWEEP_WORDS) is chosen per
+// traversal so that every warp gets at least this many units: on small graphs a
+// 32-word unit per warp leaves the round waiting on the slowest unit.
+#ifndef GBBS_UNITS_PER_WARP
+#define GBBS_UNITS_PER_WARP 1
+#endif
+__device__ __forceinline__ int sweep_unit(long long nwords, long long nw) {
+  int sw = SWEEP_WORDS;
+  while (sw > 1 && (nwords + sw - 1) / sw < (long long)GBBS_UNITS_PER_WARP * nw) sw >>= 1;
+  return sw;
+}
 
 struct TileSmem {              // list-push tile (shared-memory owner path)
   alignas(16) int32_t head[TE];  // 1 + owner index of the first edge slot of each owner
@@ -204,6 +215,18 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *a) {
       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
       : "l"(a), "l"(ef_policy()));
   return v;
+}
+
+// L2 prefetch of an upcoming stream line: a tile's target/weight chunks are
+// requested up front, so the batch loads that follow hit L2 while the previous
+// batch's atomics are in flight (GBBS_PREFETCH=0 disables).
+#ifndef GBBS_PREFETCH
+#define GBBS_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void *a) {
+#if GBBS_PREFETCH
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a));
+#endif
 }
 
 __device__ __forceinline__ void st_stream(uint32_t *a, uint32_t v) {
@@ -461,14 +484,14 @@ __device__ __forceinline__ void wbfs_flush(const Params &p, WarpState &ws, const
 template <bool STATS, int NB>
 __device__ __forceinline__ void wbfs_stage(const Params &p, WarpState &ws, uint32_t *st,
                                            const bool (&cand)[NB], const uint32_t (&v)[NB],
-                                           const unsigned long long (&nd)[NB],
+                                           const uint32_t (&nd)[NB],
                                            const uint32_t (&old)[NB], int r) {
   WbfsWarpSmem &w = wbfs_smem();
 #pragma unroll
   for (int j = 0; j < NB; j++) {
     uint32_t key = NOKEY;
     if (cand[j]) {
-      const unsigned long long b = nd[j] / p.delta;
+      const uint32_t b = nd[j] / p.delta;
       if (b == ws.bk) {
         if (atomicExch(p.tag + v[j], (uint32_t)(r + 1)) != (uint32_t)(r + 1)) key = XKEY;
       } else if (old[j] == INF || old[j] / p.delta != b) {
@@ -524,7 +547,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     // Bellman-Ford: candidate d(u)+w, priority = smaller (atomicMin).
     // Widest path: candidate min(width(u), w), priority = larger (atomicMax) —
     // the (max, min) semiring in place of (min, +).
-    unsigned long long nd[NCH];
+    uint32_t nd[NCH];
     // Pre-check against the 16-bit shadow of dist (half the bytes of dist, meant
     // to stay in L2): BF keeps shadow >= min(dist, 0xFFFF) because distances only
     // fall and the shadow only ever receives values dist held; WP keeps
@@ -533,8 +556,9 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     uint32_t cur[NCH];
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
-      nd[j] = (ALGO == ALGO_WP) ? (unsigned long long)min(uu[j], ww[j])
-                                : (unsigned long long)uu[j] + ww[j];
+      // saturating: a sum past 2^32 - 1 can never improve a uint32 distance
+      nd[j] = (ALGO == ALGO_WP) ? min(uu[j], ww[j])
+                                : (uu[j] + ww[j] < uu[j] ? INF : uu[j] + ww[j]);
       cur[j] = act[j] ? (uint32_t)p.shadow[vv[j]] : (ALGO == ALGO_WP ? 0xFFFFu : 0u);
     }
     bool cand[NCH];
@@ -545,19 +569,19 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       oldv[j] = 0;
       if (!act[j]) continue;
       if (ALGO == ALGO_WP) {
-        if (nd[j] > (unsigned long long)cur[j]) {
-          const uint32_t old = atomicMax(p.dist + vv[j], (uint32_t)nd[j]);  // priority-write
-          cand[j] = nd[j] > (unsigned long long)old;
+        if (nd[j] > cur[j]) {
+          const uint32_t old = atomicMax(p.dist + vv[j], nd[j]);  // priority-write
+          cand[j] = nd[j] > old;
         }
-      } else if (nd[j] < (unsigned long long)cur[j] || cur[j] == 0xFFFFu) {
-        const uint32_t old = atomicMin(p.dist + vv[j], (uint32_t)nd[j]);  // priority-write
-        cand[j] = nd[j] < (unsigned long long)old;
+      } else if (nd[j] < cur[j] || cur[j] == 0xFFFFu) {
+        const uint32_t old = atomicMin(p.dist + vv[j], nd[j]);  // priority-write
+        cand[j] = nd[j] < old;
         oldv[j] = old;
       }
     }
 #pragma unroll
     for (int j = 0; j < NCH; j++)
-      if (cand[j]) p.shadow[vv[j]] = (uint16_t)min(nd[j], 0xFFFFull);
+      if (cand[j]) p.shadow[vv[j]] = (uint16_t)min(nd[j], 0xFFFFu);
     if constexpr (ALGO == ALGO_WBFS) {
       wbfs_stage<STATS, NCH>(p, ws, st, cand, vv, nd, oldv, r);
       return;
@@ -644,6 +668,18 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
     if (!valid) Ok = BIG;
     uint32_t Xk = Uk;
     if (ALGO != ALGO_BFS) Xk = valid ? ld_relaxed(p.dist + Uk) : 0;
+    if (GBBS_PREFETCH && te - ts > 32 * NCH) {
+      for (long long cst = ts + 32 * NCH; cst < te; cst += 32) {
+        const int c0 = __popc(__ballot_sync(FULL, Ok <= cst)) - 1;
+        const long long rel = Ok - cst;
+        const unsigned hm = __reduce_or_sync(FULL, (rel > 0 && rel < 32) ? (1u << rel) : 0u);
+        const long long bb = __shfl_sync(FULL, Bk, c0 + __popc(hm & lanemask_le()));
+        if (cst + lane < te) {
+          prefetch_l2(p.tgt + bb + cst + lane);
+          if (ALGO != ALGO_BFS && p.wgt) prefetch_l2(p.wgt + bb + cst + lane);
+        }
+      }
+    }
     for (long long cs = ts; cs < te; cs += 32 * NCH) {
       uint32_t vv[NCH], ww[NCH], uu[NCH];
       bool act[NCH];
@@ -749,6 +785,13 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
                         max(ex, a[4 * q + 3]));
   }
   __syncwarp();
+  if (GBBS_PREFETCH) {
+    for (long long e = ts + 32 * NCH + lane; e < te; e += 32) {
+      const long long bb = w.base[w.head[e - ts] - 1];
+      prefetch_l2(p.tgt + bb + e);
+      if (ALGO != ALGO_BFS && p.wgt) prefetch_l2(p.wgt + bb + e);
+    }
+  }
   for (long long cs = ts; cs < te; cs += 32 * NCH) {
     uint32_t vv[NCH], ww[NCH], uu[NCH];
     bool act[NCH];
@@ -863,14 +906,14 @@ __device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, Wa
 // pre-check.  BF: frontier = fr (this round's TS bits), cleared as swept.
 template <int ALGO, bool STATS, int EMIT>
 __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, WarpState &ws,
-                                              long long w0, uint32_t *fr, uint32_t *bits,
+                                              long long w0, int sw, uint32_t *fr, uint32_t *bits,
                                               const uint32_t *precheck, int nb, int r) {
   const uint32_t *prebits = (ALGO == ALGO_BFS) ? precheck : bits;
   const int lane = threadIdx.x & 31;
   SweepSmem &w = wsm.u.s;
   const long long word = w0 + lane;
   uint32_t fw = 0;
-  if (word < p.nwords) {
+  if (lane < sw && word < p.nwords) {
     if (ALGO == ALGO_BFS) {
       fw = precheck[word] & ~ld_relaxed(bits + word);
       if (fw) atomicOr(bits + word, fw);
@@ -905,9 +948,18 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 // load covers the group containing the scan position); a vertex with more than
 // LONG_IN in-edges left after PULL_STEPS steps is finished by the whole warp,
 // 128 in-edges per step, so one long in-list cannot hold the warp hostage.
-constexpr int PULL_STEPS = 2;
-constexpr int LONG_IN = 24;
-constexpr int PCH = 2;
+#ifndef GBBS_PCH
+#define GBBS_PCH 2
+#endif
+#ifndef GBBS_PULL_STEPS
+#define GBBS_PULL_STEPS 2
+#endif
+#ifndef GBBS_LONG_IN
+#define GBBS_LONG_IN 24
+#endif
+constexpr int PULL_STEPS = GBBS_PULL_STEPS;
+constexpr int LONG_IN = GBBS_LONG_IN;
+constexpr int PCH = GBBS_PCH;
 
 __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4(p); }
 
@@ -916,15 +968,16 @@ __device__ __forceinline__ bool vbit(const uint32_t *vis, uint32_t u) {
 }
 
 template <bool STATS>
-__device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0,
+__device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
                                            const uint32_t *vis, uint32_t *vis_next, int r,
                                            WarpState &ws) {
   const int lane = threadIdx.x & 31;
   SweepSmem &w = wsm.u.s;
   const long long word = w0 + lane;
-  const uint32_t vw = word < p.nwords ? vis[word] : FULL;
+  const bool mine = lane < sw && word < p.nwords;
+  const uint32_t vw = mine ? vis[word] : FULL;
   if (!__any_sync(FULL, vw != FULL)) {  // all visited: carry the words over
-    if (word < p.nwords) vis_next[word] = FULL;
+    if (mine) vis_next[word] = FULL;
     return;
   }
   const int cnt = warp_gather(w, w0, ~vw);
@@ -1051,7 +1104,7 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
     }
   }
   __syncwarp();
-  if (word < p.nwords) vis_next[word] = vw | w.found[lane];
+  if (mine) vis_next[word] = vw | w.found[lane];
   __syncwarp();
 }
 
@@ -1081,8 +1134,9 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
                                               WarpSmem &w, WarpState &ws, uint32_t *fr,
                                               uint32_t *bits, const uint32_t *precheck, int nb,
                                               int r, long long gw, long long nw) {
-  for (long long w0 = gw * SWEEP_WORDS; w0 < p.nwords; w0 += nw * SWEEP_WORDS)
-    forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, fr, bits, precheck, nb, r);
+  const int sw = sweep_unit(p.nwords, nw);
+  for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
+    forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, sw, fr, bits, precheck, nb, r);
   grid.sync();  // heavy list complete
   if (threadIdx.x == 0) s.hcnt = ld_relaxed64(p.hcnt + (r & 1));
   __syncthreads();
@@ -1107,6 +1161,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
   const long long gw = (long long)blockIdx.x * NWARPS + warp;
   const long long nw = (long long)gridDim.x * NWARPS;
   const uint32_t src = p.src;
+  const int sw = sweep_unit(p.nwords, nw);
   WarpSmem &wsm = s.w[warp];
 
   // a1: per-run init
@@ -1188,8 +1243,8 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     if (kind == 1) {  // dense pull (BFS)
       const uint32_t *vis = p.bm[vc];
       uint32_t *vis_next = p.bm[vc ^ 1];
-      for (long long w0 = gw * SWEEP_WORDS; w0 < p.nwords; w0 += nw * SWEEP_WORDS)
-        pull_words<STATS>(p, wsm, w0, vis, vis_next, (int)r, ws);
+      for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
+        pull_words<STATS>(p, wsm, w0, sw, vis, vis_next, (int)r, ws);
       vc ^= 1;
       list_valid = false;
       emit_count = true;
@@ -1280,8 +1335,13 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
 // without a host round trip: every round reads only counters that no warp
 // updates during that round.  Entries whose vertex has since moved to an
 // earlier bucket are skipped when swept (lazy deletion).
+// 3 CTAs per SM: the bucket kernel's extra state spills at 64 registers, and it
+// measured 1.3x faster with 80 (c2 and c4, tools/cmp_lib.sh)
+#ifndef GBBS_WBFS_MIN_CTAS
+#define GBBS_WBFS_MIN_CTAS 3
+#endif
 template <bool STATS>
-__global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) wbfs_kernel(Params p) {
+__global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params p) {
   __shared__ Smem s;
   __shared__ unsigned long long s_head[64], s_hhead[64], s_ctl[3 + 2 * 64];
   cg::grid_group grid = cg::this_grid();
