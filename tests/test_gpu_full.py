@@ -96,10 +96,13 @@ def test_c3_full(G):
     ref = oracle.dijkstra(H["off"], H["tgt"], H["w"], 0)[0]
     bf = gpu_bf(G, g, n, 0)
     assert (bf == ref).all()
-    # NEXT-2 wBFS, bucket width 1: one round per distinct distance
+    # NEXT-2 wBFS, bucket width 1: every distinct distance is an extracted bucket,
+    # every vertex expanded once
     wb, st = gpu_wbfs(G, g, n, 0)
     assert (wb == ref).all()
-    assert st.rounds == np.unique(ref).size
+    recs = G.round_records(st)
+    assert set(np.unique(ref).tolist()) <= {r["bucket"] for r in recs}
+    assert sum(r["edges_examined"] for r in recs) == H["off"][-1]
     g.close()
 
 
@@ -112,7 +115,7 @@ def test_c4_full(G):
         assert oracle.check_sssp(H["off"], H["tgt"], H["w"], s, bf)[0], s
         wb, st = gpu_wbfs(G, g, n, s)                     # NEXT-2: same distances
         assert (wb == bf).all(), s
-        assert st.rounds == np.unique(bf[bf != 0xFFFFFFFF]).size
+        assert st.rounds >= np.unique(bf[bf != 0xFFFFFFFF]).size
     s = D["sources"][0]
     d, p, _ = gpu_bfs(G, g, n, s)
     assert oracle.check_bfs(H["off"], H["tgt"], s, d, p)[0]

@@ -4,11 +4,12 @@ against the oracle's Dijkstra, element by element (distances are unique, so the
 bar is bit-exact).
 
 Structure checked beside the values: with bucket width 1 and weights >= 1 every
-bucket is extracted once, so the kernel runs exactly one round per distinct
-finite distance (the number of distinct values of the oracle's output); the
-vertices swept in a round equal the entries of that bucket, and the sum over
-rounds of non-stale entries is the number of reached vertices (each expanded
-once: O(m) work, P:104-106).
+bucket is extracted once, in increasing order, and every distinct finite
+distance is one of the extracted buckets (a bucket whose entries all moved to
+earlier buckets is still extracted, so rounds >= distinct distances, with
+equality for unit or constant weights); every reached vertex is expanded exactly
+once, so the edges examined equal the out-degree sum of the reached set (O(m)
+work, P:104-106).
 """
 import numpy as np
 import pytest
@@ -91,8 +92,10 @@ def test_rounds_equal_distinct_distances(G):
     d = run_wbfs(G, g, 0, delta=1, stats=st)
     assert (d == ref).all()
     recs = G.round_records(st)
-    assert st.rounds == distinct_finite(ref)
-    assert [r["bucket"] for r in recs] == sorted(np.unique(ref[ref != INF]).tolist())
+    buckets = [r["bucket"] for r in recs]
+    assert buckets == sorted(set(buckets))                          # increasing, once each
+    assert set(np.unique(ref[ref != INF]).tolist()) <= set(buckets)
+    assert st.rounds >= distinct_finite(ref)
     assert all(r["dense"] == 3 for r in recs)          # no near-list rounds
     # every vertex of bucket k has dist k: the rounds' entry counts cover the
     # reached set (stale entries come on top)
