@@ -9,8 +9,11 @@ optimising, T=20) from each of the config's seeded sources on the resident graph
 (default c2: 8 sources in the largest component of the medium rMAT graph).  The
 Bellman-Ford leg of the metric is measured in the same run on the same graph with
 weights in [1, floor(log2 n)] (reading A6) and reported under "bellman_ford".
-Multi-GPU = replicas: every rank runs the same batch on its
-own copy; value = total traversed edges of all ranks / max-over-ranks time.
+Multi-GPU: every rank holds its own copy of the graph and
+traverses its own shard of the source sample (rank r: sources 8r .. 8r+7 of the
+config's sequential seeded sample, so rank 0's are the N=1 sources; configs with
+a single fixed source run it on every rank); value = traversed edges summed over
+ranks / max-over-ranks step time (weak scaling, no collective on the data path).
 --impl reference times the CPU oracle (sequential C queue-BFS / Dijkstra) — the
 only place besides cpu_baseline where bench.py executes oracle/.
 """
@@ -186,9 +189,27 @@ def replica_max(x, world, dist_mod=None, device="cpu"):
     return float(t.item())
 
 
-def replica_value(edges_per_rank_step, world, step_ms_max):
-    """Whole-job GTEPS: every rank traverses the same batch (weak scaling)."""
-    return world * edges_per_rank_step / (step_ms_max * 1e-3) / 1e9
+def replica_sum(x, world, dist_mod=None, device="cpu"):
+    """Sum over ranks of a per-rank count (the job's traversed edges)."""
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist_mod.all_reduce(t, op=dist_mod.ReduceOp.SUM)
+    return float(t.item())
+
+
+def replica_value(edges_all_ranks_step, step_ms_max):
+    """Whole-job GTEPS: edges traversed by all ranks per step / the slowest rank's
+    step time (weak scaling: each rank's batch is fixed)."""
+    return edges_all_ranks_step / (step_ms_max * 1e-3) / 1e9
+
+
+def shard_sources(sources, rank, world, per_rank):
+    """Rank r's sources: entries [per_rank*r, per_rank*(r+1)) of the sequential
+    sample, or the whole (single-source) list on every rank."""
+    if len(sources) < per_rank * world:
+        return list(sources)
+    return list(sources[per_rank * rank: per_rank * (rank + 1)])
 
 
 def run_ours(args, rank, world, local):
@@ -204,12 +225,14 @@ def run_ours(args, rank, world, local):
 
     t0 = time.time()
     want_w = (args.algo == "bf") or not args.no_bf_leg
-    G = gdev.build_config(args.workload, weights=want_w)
+    from graphgen import CONFIGS
+    per_rank = CONFIGS[args.workload].nsources
+    G = gdev.build_config(args.workload, weights=want_w, nsources=per_rank * world)
     cfg = G["cfg"]
     n, m = G["n"], G["m"]
     g = gbbs.Graph(G["offsets"], G["targets"], G["weights"], symmetric=G["symmetric"])
     setup_s = time.time() - t0
-    sources = G["sources"]
+    sources = shard_sources(G["sources"], rank, world, per_rank)
     off = G["offsets"]
     dist = torch.empty(n, dtype=torch.int32, device=dev)
     par = torch.empty(n, dtype=torch.int32, device=dev)
@@ -281,7 +304,31 @@ def run_ours(args, rank, world, local):
                        args.warmup if algo == args.algo else 1) for algo in algos}
     step_ms, clocks, kernel_ms = res[args.algo]
     edges_step = sum(per_src[(args.algo, s)]["m_reach"] for s in sources)
-    value = replica_value(edges_step, world, step_ms)
+    edges_job = replica_sum(edges_step, world, dist_mod, dev)
+    # every leg's edges summed over ranks (all ranks take part in the reduction)
+    leg_edges = {a: replica_sum(sum(per_src[(a, s)]["m_reach"] for s in sources), world, dist_mod, dev)
+                 for a in algos}
+    value = replica_value(edges_job, step_ms)
+
+    # e2e: the public API with pinned host output buffers on every rank; libgbbs
+    # copies dist/parent device->host inside each call (sources travel as kernel
+    # arguments); the step time is the slowest rank's (median over steps)
+    hd = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    hp = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    hdn, hpn = hd.numpy(), hp.numpy()
+    torch.cuda.synchronize()
+    e2e = []
+    for _ in range(max(2, min(args.steps, 5))):
+        if world > 1:
+            dist_mod.barrier()
+        t = time.perf_counter()
+        for s in sources:
+            if args.algo == "bfs":
+                gbbs.gbbs_bfs(g.handle, s, hdn, hpn, stream=stream)
+            else:
+                gbbs.gbbs_bellman_ford(g.handle, s, hdn, stream=stream)
+        e2e.append(replica_max(time.perf_counter() - t, world, dist_mod, dev))
+    e2e_s = float(np.median(e2e))
 
     out = None
     if rank == 0:
@@ -290,22 +337,6 @@ def run_ours(args, rank, world, local):
         alg_bytes = sum(per_src[(args.algo, s)]["alg_bytes"] for s in sources)
         achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
         traffic = ncu_traffic(cfg.name, args.algo)
-        # e2e: the public API with pinned host output buffers; libgbbs copies dist/parent
-        # device->host inside the call (sources travel as kernel arguments)
-        hd = torch.empty(n, dtype=torch.int32, pin_memory=True)
-        hp = torch.empty(n, dtype=torch.int32, pin_memory=True)
-        hdn, hpn = hd.numpy(), hp.numpy()
-        torch.cuda.synchronize()
-        e2e = []
-        for _ in range(max(2, min(args.steps, 5))):
-            t = time.perf_counter()
-            for s in sources:
-                if args.algo == "bfs":
-                    gbbs.gbbs_bfs(g.handle, s, hdn, hpn, stream=stream)
-                else:
-                    gbbs.gbbs_bellman_ford(g.handle, s, hdn, stream=stream)
-            e2e.append(time.perf_counter() - t)
-        e2e_s = float(np.median(e2e))
         d2h = len(sources) * n * (8 if args.algo == "bfs" else 4)
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "GTEPS",
@@ -317,7 +348,8 @@ def run_ours(args, rank, world, local):
                        "n": n, "m": m, "sources": sources, "threshold_T": args.threshold,
                        "traversals_per_step": len(sources), "edges_per_step": edges_step,
                        "l2": "flushed (256 MB write) before every timed step; graph > L2",
-                       "parallelism": f"replicas x{world}"},
+                       "parallelism": f"source-sharded replicas x{world}",
+                       "edges_per_step_all_ranks": edges_job},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic,
@@ -325,9 +357,15 @@ def run_ours(args, rank, world, local):
                          "frac_of_copy_same_run": round(achieved / copy_gbs, 4),
                          "kernel": "gbbs_dev::traverse_kernel (persistent; one launch per traversal)",
                          "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": round(kernel_ms, 4),
-                         "kernel_gteps": round(edges_step / (kernel_ms * 1e-3) / 1e9, 3)},
-            "e2e": {"value": round(edges_step / e2e_s / 1e9, 3), "unit": "GTEPS",
-                    "h2d_bytes_per_step": 4 * len(sources), "d2h_bytes_per_step": d2h,
+                         "kernel_gteps": round(edges_step / (kernel_ms * 1e-3) / 1e9, 3),
+                         # reading A21b: the edge-traffic roofline of a BFS is
+                         # 4 B per reached edge at peak; a direction-optimising BFS that
+                         # skips edges can exceed it (frac > 1)
+                         "edge_traffic": {"bytes_per_edge": 4,
+                                          "achieved": round(4 * edges_step / (kernel_ms * 1e-3) / 1e9, 1),
+                                          "frac": round(4 * edges_step / (kernel_ms * 1e-3) / 1e9 / peak, 4)}},
+            "e2e": {"value": round(edges_job / e2e_s / 1e9, 3), "unit": "GTEPS",
+                    "h2d_bytes_per_step": 4 * len(sources) * world, "d2h_bytes_per_step": d2h * world,
                     "note": "gbbs_bfs with pinned host dist/parent (library copies D2H); "
                             "h2d = the source ids, passed as kernel arguments"},
             "gpu_launches": args.steps * len(sources),
@@ -337,7 +375,7 @@ def run_ours(args, rank, world, local):
         }
         if "bf" in algos and args.algo == "bfs":
             bt, bclk, bkms = res["bf"]
-            be = sum(per_src[("bf", s)]["m_reach"] for s in sources)
+            be = leg_edges["bf"]
             brel = sum(per_src[("bf", s)]["relax"] for s in sources)
             balg = sum(per_src[("bf", s)]["alg_bytes"] for s in sources)
             out["bellman_ford"] = {
@@ -345,11 +383,15 @@ def run_ours(args, rank, world, local):
                 "relaxations_per_s_G": round(brel / (bt * 1e-3) / 1e9, 3), "ms_per_step": round(bt, 4),
                 "weights": f"[1,{cfg.W}] pair-hash (readings A5, A6)",
                 "roofline_frac": round(balg / (bkms * 1e-3) / 1e9 / peak, 4),
+                # every relaxation probes the 16-bit distance shadow at a random address;
+                # tools/gather_bench.cu measured 270 G random 2-byte L2 gathers/s and
+                # 110 G random atomicMin/s on this B200 (profiles/r01_gather_bench.txt)
+                "relax_vs_l2_gather_ceiling": round(brel / (bkms * 1e-3) / 1e9 / 270.0, 4),
                 "kernel_ms_per_step": round(bkms, 4), "clocks": bclk,
                 "rounds": [per_src[("bf", s)]["rounds"] for s in sources]}
         if "wbfs" in algos and args.algo == "bfs":
             wt, wclk, wkms = res["wbfs"]
-            we = sum(per_src[("wbfs", s)]["m_reach"] for s in sources)
+            we = leg_edges["wbfs"]
             out["wbfs"] = {
                 "value": round(we / (wt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective)",
                 "ms_per_step": round(wt, 4), "kernel_ms_per_step": round(wkms, 4),
@@ -358,7 +400,7 @@ def run_ours(args, rank, world, local):
                 "rounds": [per_src[("wbfs", s)]["rounds"] for s in sources]}
         if "wp" in algos and args.algo == "bfs":
             wt, wclk, wkms = res["wp"]
-            we = sum(per_src[("wp", s)]["m_reach"] for s in sources)
+            we = leg_edges["wp"]
             walg = sum(per_src[("wp", s)]["alg_bytes"] for s in sources)
             out["widest_path"] = {
                 "value": round(we / (wt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective)",
@@ -382,7 +424,7 @@ def run_ours(args, rank, world, local):
             bt = e0.elapsed_time(e1)
             out["betweenness"] = {
                 "value": round(edges_step / (bt * 1e-3) / 1e9, 3),
-                "unit": "GTEPS (m_reach of the BFS per source / time)",
+                "unit": "GTEPS (m_reach of the BFS per source / time; rank 0's shard)",
                 "ms_per_step": round(bt, 4),
                 "note": "NEXT-3: Brandes dependencies, forward CAS + fp64 fetch-and-add, backward per level"}
         if not args.profile:

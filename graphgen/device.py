@@ -78,9 +78,11 @@ def cc_labels(off, tgt):
     return lab
 
 
-def sources_for(cfg, off, tgt):
+def sources_for(cfg, off, tgt, count=None):
     """Reading A9: c1/c3 vertex 0; lcc: seeded sample of the largest component;
-    outdeg: seeded sample of vertices with out-degree >= 1."""
+    outdeg: seeded sample of vertices with out-degree >= 1.  count (default the
+    config's) > nsources extends the same sequential sample, so its first
+    nsources entries are the config's sources."""
     import torch
     if cfg.sources == "zero":
         return [0]
@@ -90,13 +92,14 @@ def sources_for(cfg, off, tgt):
         cand = torch.nonzero(lab == big).flatten()
     else:
         cand = torch.nonzero(off[1:] - off[:-1] > 0).flatten()
-    idx = choose_sources(np.arange(cand.numel()), cfg.nsources, cfg.source_seed)
+    idx = choose_sources(np.arange(cand.numel()), count or cfg.nsources, cfg.source_seed)
     return [int(cand[i]) for i in idx]
 
 
-def build_config(name, device="cuda", weights=None):
+def build_config(name, device="cuda", weights=None, nsources=None):
     """Build config `name` on the device.  weights: None = the config's own rule
-    (weights iff cfg.W and the config runs BF), True/False to force."""
+    (weights iff cfg.W and the config runs BF), True/False to force.  nsources:
+    sample that many sources (see sources_for)."""
     cfg = CONFIGS[name]
     if cfg.kind == "torus":
         off, tgt = torus_csr(cfg.L, device)
@@ -104,6 +107,6 @@ def build_config(name, device="cuda", weights=None):
         off, tgt = rmat_csr(cfg.levels, 1 << cfg.log_edges, cfg.graph_seed, *cfg.abc, cfg.symmetric, device)
     want_w = ("bf" in cfg.algos) if weights is None else weights
     w = pair_weights(off, tgt, cfg.weight_seed, cfg.W) if (want_w and cfg.W) else None
-    srcs = sources_for(cfg, off, tgt)
+    srcs = sources_for(cfg, off, tgt, nsources)
     return dict(cfg=cfg, n=off.shape[0] - 1, m=tgt.shape[0], offsets=off, targets=tgt, weights=w,
                 symmetric=cfg.symmetric, sources=srcs)

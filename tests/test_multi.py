@@ -1,5 +1,6 @@
-"""The N>1 path of bench.py (replicas) on CPU with gloo, world size 2:
-the only collective is the max-reduction of the per-rank step time."""
+"""The N>1 path of bench.py (source-sharded replicas) on CPU with
+gloo, world size 2: the only collectives are the max of the per-rank step time
+and the sum of the per-rank traversed edges (metric bookkeeping, not data path)."""
 import os
 import socket
 
@@ -24,7 +25,8 @@ def _worker(rank, world, port, out):
     import bench
     ms = 1.0 + 2.0 * rank            # rank 1 is slower
     t = bench.replica_max(ms, world, dist, "cpu")
-    v = bench.replica_value(1e9, world, t)
+    e = bench.replica_sum(1e9 * (rank + 1), world, dist, "cpu")   # ranks traverse different edges
+    v = bench.replica_value(e, t)
     out[rank] = (t, v)
     dist.barrier()
     dist.destroy_process_group()
@@ -37,13 +39,29 @@ def test_replica_timing_is_max_over_ranks():
     for r in range(world):
         t, v = out[r]
         assert t == 3.0                       # max over ranks, every rank agrees
-        assert abs(v - world * 1e9 / 3e-3 / 1e9) < 1e-9
+        assert abs(v - 3e9 / 3e-3 / 1e9) < 1e-9  # (1e9 + 2e9) edges / 3 ms
 
 
 def test_single_rank_identity():
     import bench
     assert bench.replica_max(1.5, 1) == 1.5
-    assert bench.replica_value(2e9, 1, 2.0) == pytest.approx(1000.0)
+    assert bench.replica_sum(7.0, 1) == 7.0
+    assert bench.replica_value(2e9, 2.0) == pytest.approx(1000.0)
+
+
+def test_source_sharding():
+    """Rank r takes entries [8r, 8r+8) of the sequential seeded sample: disjoint
+    shards, rank 0's equal the N=1 sources; a single-source config repeats."""
+    import bench
+    import graphgen
+    import numpy as np
+    cand = np.arange(10_000)
+    one = graphgen.choose_sources(cand, 8, 102)
+    four = graphgen.choose_sources(cand, 32, 102)
+    assert four[:8] == one
+    shards = [bench.shard_sources(four, r, 4, 8) for r in range(4)]
+    assert shards[0] == one and len({s for sh in shards for s in sh}) == 32
+    assert bench.shard_sources([0], 3, 4, 1) == [0]
 
 
 def test_reference_arm_nonzero_rank_prints_nothing(monkeypatch):
