@@ -148,3 +148,39 @@ def test_c2_betweenness_full(G):
     got = d.cpu().numpy()
     assert np.allclose(got, ref, rtol=1e-9, atol=1e-9 * float(np.abs(ref).max()))
     g.close()
+
+
+def test_paper_torus_row_1000_cubed(G):
+    """PAPER.md:2132 (sec:experiments, table:sizes) prints the 3D-Torus row: 10^9
+    vertices, 6*10^9 edges, diam 1500 (tests/golden/paper_torus_row.txt).  Build
+    exactly that graph on the GPU (≈100 GB: CSR 32 GB borrowed, frontier lists
+    60 GB, dist 4 GB) and run BFS from vertex 0 in the bench's launch
+    configuration: 1500 = the largest distance, 1501 edgeMap rounds, every round's
+    frontier equal to the closed-form level count, every vertex reached, and
+    sampled distances equal to the closed form."""
+    from golden_io import read_kv
+    from graphgen import device
+    row = read_kv("paper_torus_row.txt")
+    L = row["side"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < 110 * 2 ** 30:
+        pytest.skip(f"needs ~110 GB of free device memory, {free / 2 ** 30:.0f} GB free")
+    off, tgt = device.torus_csr(L)
+    assert off.shape[0] - 1 == row["vertices"] and tgt.shape[0] == row["edges"]
+    g = G.Graph(off, tgt, None, symmetric=True, borrow=True)
+    d = torch.empty(off.shape[0] - 1, dtype=torch.int32, device="cuda")
+    st = G.make_stats(4096)
+    g.bfs(0, d, None, opts=G.make_opts(20, G.GBBS_MODE_AUTO), stats=st)
+    lv = torus_level_counts(L)
+    assert st.rounds == len(lv) == row["diam"] + 1
+    assert [r["frontier"] for r in G.round_records(st)] == list(lv)
+    assert st.reached == row["vertices"]
+    assert int(d.max()) == row["diam"]
+    idx = torch.randint(0, row["vertices"], (1 << 20,), device="cuda", generator=None)
+    ii = idx.to(torch.int64)
+    x, y, z = ii % L, (ii // L) % L, ii // (L * L)
+    ring = lambda a: torch.minimum(a, L - a)  # noqa: E731  (src = vertex 0)
+    assert torch.equal(d[idx].to(torch.int64), ring(x) + ring(y) + ring(z))
+    g.close()
+    del off, tgt, d
+    torch.cuda.empty_cache()
