@@ -133,9 +133,10 @@ int gbbs_bfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
  * dist    uint32[n], caller-owned, host or device: shortest weighted
  *         distance from src, GBBS_INF if unreachable.
  * Same stream/synchronization/error conventions as gbbs_bfs, plus
- * GBBS_ERANGE if max(w) * (n-1) >= 2^32 - 1 (a finite distance, always a
- * simple-path length, might not fit below the uint32 sentinel), and
- * GBBS_EINTERNAL if more than n+1 rounds run (impossible with w >= 0).
+ * GBBS_ERANGE if some relaxation candidate d(u) + w reached 2^32 - 1 (the
+ * distances do not fit below the uint32 sentinel; detected during the run,
+ * dist is then incomplete), and GBBS_EINTERNAL if more than n+1 rounds run
+ * (impossible with w >= 0).
  */
 int gbbs_bellman_ford(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                       void *cuda_stream);

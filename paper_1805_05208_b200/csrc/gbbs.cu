@@ -535,22 +535,27 @@ static int wbfs_setup(gbbs_graph *g, uint32_t delta, Params &p) {
                 D, W);
   int nbq = 1;
   while ((unsigned long long)nbq <= span) nbq <<= 1;
-  unsigned long long qcap = 1;
-  while (qcap < (unsigned long long)g->n) qcap <<= 1;
+  const bool need_near = D > 1 || g->minw == 0;
   WbfsScratch *w = g->wb;
   if (w && w->nbq < nbq) {
     free_wbfs(g);
     w = nullptr;
   }
   if (!w) {
+    // list capacity: 2^ceil(log2 n) (a bucket can hold every vertex), or less when
+    // the ring would take more than half of the free device memory; a list that
+    // overflows is detected when its bucket is extracted (GBBS_ENOMEM)
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    unsigned long long qcap = 1;
+    while (qcap < (unsigned long long)g->n) qcap <<= 1;
+    while (qcap > (1ull << 16) && (unsigned long long)nbq * qcap * 4 > free_b / 2) qcap >>= 1;
     w = new (std::nothrow) WbfsScratch();
     if (!w) return fail(GBBS_ENOMEM, "host allocation");
     g->wb = w;
     w->nbq = nbq;
     w->qcap = qcap;
     CU(cudaMalloc(&w->bq, (size_t)nbq * qcap * 4));
-    for (int i = 0; i < 3; i++) CU(cudaMalloc(&w->xq[i], (size_t)g->n * 4));
-    CU(cudaMalloc(&w->tag, (size_t)g->n * 4));
     CU(cudaMalloc(&w->hv, (size_t)g->nwords * 4));
     CU(cudaMalloc(&w->ctr, (64 + 64 + 6 + 3) * 8));
     k_heavy_bits<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->n, g->nwords, w->hv);
@@ -559,7 +564,10 @@ static int wbfs_setup(gbbs_graph *g, uint32_t delta, Params &p) {
     if ((rc = wbfs_grid<false>(&w->grid[0]))) return rc;
     if ((rc = wbfs_grid<true>(&w->grid[1]))) return rc;
   }
-  const bool need_near = D > 1 || g->minw == 0;
+  if (need_near && !w->tag) {  // near lists + round tags: only for delta > 1 or w = 0
+    for (int i = 0; i < 3; i++) CU(cudaMalloc(&w->xq[i], (size_t)g->n * 4));
+    CU(cudaMalloc(&w->tag, (size_t)g->n * 4));
+  }
   p.bq = w->bq;
   p.qcap = w->qcap;
   p.nbq = w->nbq;
@@ -609,13 +617,6 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
     for (int i = 0; i < 3; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.mode < 0 || o.mode > 2) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
-  }
-  if (algo == ALGO_BF || algo == ALGO_WBFS) {
-    // uint32 distances: every finite distance is a simple-path length <= maxw*(n-1)
-    unsigned long long bound = (unsigned long long)g->maxw * (unsigned long long)(g->n - 1);
-    if (g->maxw != 0 && bound / g->maxw != (unsigned long long)(g->n - 1)) bound = ~0ull;
-    if (bound >= 0xFFFFFFFFull)
-      return fail(GBBS_ERANGE, "max weight %u * (n-1) does not fit below 2^32-1", g->maxw);
   }
   int dev = 0;
   CU(cudaGetDevice(&dev));
@@ -753,6 +754,13 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
               h[4 * i] / 1e3, h[4 * i + 1] / 1e3, h[4 * i + 2] / 1e3, h[4 * i + 3]);
   }
 #endif
+  if (ctrl.status & 4)
+    return fail(GBBS_ENOMEM, "wbfs: a bucket list exceeded its capacity of %llu entries "
+                "(device memory was short at first use; a larger delta needs fewer)",
+                g->wb ? g->wb->qcap : 0ull);
+  if (ctrl.status & 2)  // a relaxation candidate reached 2^32 - 1 (uint32 distances)
+    return fail(GBBS_ERANGE, "a distance candidate reached 2^32-1 (max weight %u): "
+                "distances do not fit the uint32 output", g->maxw);
   if (ctrl.status != 0)
     return fail(GBBS_EINTERNAL, "round cap (%lld rounds) exceeded", (long long)p.max_rounds);
   return GBBS_OK;

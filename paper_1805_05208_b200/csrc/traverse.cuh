@@ -556,9 +556,17 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     uint32_t cur[NCH];
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
-      // saturating: a sum past 2^32 - 1 can never improve a uint32 distance
-      nd[j] = (ALGO == ALGO_WP) ? min(uu[j], ww[j])
-                                : (uu[j] + ww[j] < uu[j] ? INF : uu[j] + ww[j]);
+      // saturating: a sum reaching 2^32 - 1 cannot be stored below the INF
+      // sentinel; it is flagged (status bit 2 -> GBBS_ERANGE) instead of the
+      // conservative up-front check max(w) * (n - 1) < 2^32 - 1
+      if (ALGO == ALGO_WP) {
+        nd[j] = min(uu[j], ww[j]);
+      } else {
+        const uint32_t sum = uu[j] + ww[j];
+        const bool ovf = sum < uu[j] || sum == INF;
+        nd[j] = ovf ? INF : sum;
+        if (ovf && act[j]) atomicOr(p.status, 2);
+      }
       cur[j] = act[j] ? (uint32_t)p.shadow[vv[j]] : (ALGO == ALGO_WP ? 0xFFFFu : 0u);
     }
     bool cand[NCH];
@@ -1422,6 +1430,10 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
       h = s_head[slot];
       t = s_ctl[3 + slot];
       heavy_any = s_ctl[3 + 64 + slot] > s_hhead[slot];
+      if (t - h > p.qcap) {  // entries were overwritten: the list overflowed
+        if (blockIdx.x == 0 && tid == 0) *p.status = 4;
+        break;
+      }
     }
     if (r >= p.max_rounds) {
       if (blockIdx.x == 0 && tid == 0) *p.status = 1;
