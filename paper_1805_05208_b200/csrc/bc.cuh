@@ -85,6 +85,7 @@ __device__ __forceinline__ void bc_flush(const BcParams &p, const uint32_t *st, 
     if (keep) {
       const unsigned long long pos = qbase + k + __popc(bal & lanemask_lt());
       const long long o = (long long)d + dex;
+      GBBS_CHECK(pos < (unsigned long long)p.n);
       p.qv[pos] = v;
       p.qo[pos] = o;
       p.qb[pos] = a - o;
@@ -179,6 +180,7 @@ __device__ __forceinline__ long long bc_tile(const BcParams &p, BcWarpSmem &w, i
       if (act[j]) {
         const int kk = w.head[e - ts] - 1;
         uu[j] = w.own[kk];
+        GBBS_CHECK(w.base[kk] + e >= 0 && w.base[kk] + e < p.m);
         vv[j] = ld_stream(p.tgt + w.base[kk] + e);
       }
     }

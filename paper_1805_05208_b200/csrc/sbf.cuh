@@ -104,6 +104,7 @@ __device__ __forceinline__ void sbf_tile(const Params &p, SbfWarpSmem &w, WarpSt
       const int kk = w.head[e - ts] - 1;
       const long long bb = w.base[kk];
       const long long du = w.dval[kk];
+      GBBS_CHECK(bb + e >= 0 && bb + e < p.m);
       v = ld_stream(p.tgt + bb + e);
       long long nd = du + sbf_weight(p, bb + e);
       if (nd < SBF_FLOOR) nd = SBF_FLOOR;
@@ -117,6 +118,7 @@ __device__ __forceinline__ void sbf_tile(const Params &p, SbfWarpSmem &w, WarpSt
       }
     }
     const unsigned b = __ballot_sync(FULL, win);
+    GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
     if (win) w.stage[ws.scnt + __popc(b & lanemask_lt())] = v;
     ws.scnt += __popc(b);
     if (ws.scnt > WCAP - 32) {

@@ -40,6 +40,24 @@
 
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <cstdio>
+
+// Device-side bounds checks (build with -DGBBS_CHECKS; compiled out otherwise):
+// every list, staging and edge-index write/read site below asserts its range and
+// traps on a violation — the stand-in for compute-sanitizer, closed on this pool.
+#ifdef GBBS_CHECKS
+#define GBBS_CHECK(c)                                                              \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("GBBS_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);            \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define GBBS_CHECK(c) \
+  do {                \
+  } while (0)
+#endif
 
 namespace gbbs_dev {
 
@@ -303,6 +321,7 @@ __device__ __forceinline__ void warp_append(const Params &p, int nb, unsigned lo
   if (keep) {
     const unsigned long long pos = (old >> p.ebits) + __popc(bal & lanemask_lt());
     const long long o = (long long)(old & ((1ull << p.ebits) - 1)) + dex;
+    GBBS_CHECK(pos < (unsigned long long)p.n);
     p.fv[nb][pos] = v;
     p.fo[nb][pos] = o;
     p.fb[nb][pos] = a - o;
@@ -384,6 +403,7 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
       const unsigned long long pos = k + __popc(bal & lanemask_lt());
       const long long o = (long long)d + dex;
       if (keep) {
+        GBBS_CHECK(pos < (unsigned long long)p.n);
         fv[pos] = vv[u];
         fo[pos] = o;
         fb[pos] = lo[u] - o;
@@ -464,9 +484,10 @@ __device__ __forceinline__ void wbfs_flush(const Params &p, WarpState &ws, const
       const uint32_t v = st[i];
       const unsigned long long pos =
           (key == XKEY ? x2 : (key >= 32 ? x1 : x0)) + atomicAdd(&w.hist[key], 1u);
-      if (key == XKEY)
+      if (key == XKEY) {
+        GBBS_CHECK(pos < (unsigned long long)p.n);
         p.xq[xr][pos] = v;
-      else
+      } else
         p.bq[(unsigned long long)key * p.qcap + (pos & (p.qcap - 1))] = v;
       if ((__ldg(p.hv + (v >> 5)) >> (v & 31)) & 1u)
         atomicAdd(key == XKEY ? p.xcnt + 3 + xr : p.bheavy + key, 1ull);
@@ -499,6 +520,7 @@ __device__ __forceinline__ void wbfs_stage(const Params &p, WarpState &ws, uint3
       }
     }
     const unsigned bal = __ballot_sync(FULL, key != NOKEY);
+    GBBS_CHECK(ws.scnt + __popc(bal) <= WCAP);
     if (key != NOKEY) {
       const int idx = ws.scnt + __popc(bal & lanemask_lt());
       st[idx] = v[j];
@@ -624,6 +646,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       const unsigned b = __ballot_sync(FULL, win[j]);
+      GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
       if (win[j]) st[ws.scnt + __popc(b & lanemask_lt())] = vv[j];
       ws.scnt += __popc(b);
     }
@@ -708,6 +731,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
           const long long bb = __shfl_sync(FULL, Bk, own);
           uu[j] = __shfl_sync(FULL, Xk, own);
           if (act[j]) {
+            GBBS_CHECK(bb + e >= 0 && bb + e < p.m);
             vv[j] = ld_stream(p.tgt + bb + e);
             if (ALGO != ALGO_BFS) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
           }
@@ -814,6 +838,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
         const int kk = w.head[e - ts] - 1;
         const long long bb = w.base[kk];
         uu[j] = w.own[kk];
+        GBBS_CHECK(bb + e >= 0 && bb + e < p.m);
         vv[j] = ld_stream(p.tgt + bb + e);
         if (ALGO != ALGO_BFS) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
       }
@@ -881,6 +906,7 @@ __device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, Wa
       for (int j = 0; j < NCH; j++) {
         const int e = cs + 32 * j + lane;
         act[j] = e < ld;
+        GBBS_CHECK(!act[j] || (la + e >= 0 && la + e < p.m));
         vv[j] = act[j] ? ld_stream(p.tgt + la + e) : 0;
         ww[j] = (ALGO != ALGO_BFS && act[j]) ? (p.wgt ? ld_stream(p.wgt + la + e) : 1u) : 0;
         uu[j] = lx;
@@ -899,6 +925,7 @@ __device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, Wa
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
       act[j] = jj + j < mine;
+      GBBS_CHECK(!act[j] || (a + jj + j >= 0 && a + jj + j < p.m));
       vv[j] = act[j] ? ld_stream(p.tgt + a + jj + j) : 0;
       ww[j] = (ALGO != ALGO_BFS && act[j]) ? (p.wgt ? ld_stream(p.wgt + a + jj + j) : 1u) : 0;
       uu[j] = x;
@@ -1013,7 +1040,10 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
       uint4 g[PCH];
 #pragma unroll
       for (int q = 0; q < PCH; q++)
-        if (rem[q] > 0) g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+        if (rem[q] > 0) {
+          GBBS_CHECK(js[q] >= 0 && js[q] < p.m);
+          g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+        }
       bool live = false;
 #pragma unroll
       for (int q = 0; q < PCH; q++) {
@@ -1046,6 +1076,7 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
         const bool go = rem[q] > 0 && rem[q] <= LONG_IN;
         if (!__any_sync(FULL, go)) break;
         if (go) {
+          GBBS_CHECK(js[q] >= 0 && js[q] < p.m);
           const uint4 g = ldg_v4(p.in_tgt + (js[q] & ~3ll));
           const int lo = (int)(js[q] & 3);
           const int hi = min(4, lo + rem[q]);
@@ -1481,6 +1512,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
       }
       if (big) {  // stage the live entries; one packed atomicAdd per full stage
         const unsigned bal = __ballot_sync(FULL, dg > 0);
+        GBBS_CHECK(ws.scnt + __popc(bal) <= WCAP);
         if (dg > 0) wsm.stage[ws.scnt + __popc(bal & lanemask_lt())] = v;
         ws.scnt += __popc(bal);
         if (ws.scnt > WCAP - 32) {
