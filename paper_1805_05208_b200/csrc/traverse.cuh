@@ -992,6 +992,9 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #ifndef GBBS_LONG_IN
 #define GBBS_LONG_IN 24
 #endif
+#ifndef GBBS_LONG_UNROLL
+#define GBBS_LONG_UNROLL 1
+#endif
 constexpr int PULL_STEPS = GBBS_PULL_STEPS;
 constexpr int LONG_IN = GBBS_LONG_IN;
 constexpr int PCH = GBBS_PCH;
@@ -1101,24 +1104,43 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
         long long a = __shfl_sync(FULL, js[q], l);
         const long long e_end = a + __shfl_sync(FULL, rem[q], l);
         uint32_t found = INF;
+        // GBBS_LONG_UNROLL groups of 128 in-edges per step: all loads, then all
+        // probes, so a step keeps UNROLL x 16 B per lane in flight
         while (a < e_end) {
           const long long a0 = a & ~3ll;
-          const long long gk = a0 + 4 * lane;
-          uint32_t hit = INF;
-          if (gk < e_end) {
-            const uint4 g = ldg_v4(p.in_tgt + gk);
-            const uint32_t e[4] = {g.x, g.y, g.z, g.w};
+          uint4 g[GBBS_LONG_UNROLL];
 #pragma unroll
-            for (int k = 3; k >= 0; k--)
-              if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit = e[k];
+          for (int u = 0; u < GBBS_LONG_UNROLL; u++) {
+            const long long gk = a0 + 128 * u + 4 * lane;
+            if (gk < e_end) {
+              GBBS_CHECK(gk >= 0 && gk < p.m);
+              g[u] = ldg_v4(p.in_tgt + gk);
+            }
           }
-          const unsigned hb = __ballot_sync(FULL, hit != INF);
-          if (STATS && lane == 0) ws.edges += min(a0 + 128, e_end) - a;
-          if (hb) {
-            found = __shfl_sync(FULL, hit, __ffs(hb) - 1);
-            break;
+          uint32_t hit[GBBS_LONG_UNROLL];
+#pragma unroll
+          for (int u = 0; u < GBBS_LONG_UNROLL; u++) {
+            const long long gk = a0 + 128 * u + 4 * lane;
+            hit[u] = INF;
+            if (gk < e_end) {
+              const uint32_t e[4] = {g[u].x, g[u].y, g[u].z, g[u].w};
+#pragma unroll
+              for (int k = 3; k >= 0; k--)
+                if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit[u] = e[k];
+            }
           }
-          a = a0 + 128;
+          if (STATS && lane == 0) ws.edges += min(a0 + 128 * GBBS_LONG_UNROLL, e_end) - a;
+          bool done = false;
+#pragma unroll
+          for (int u = 0; u < GBBS_LONG_UNROLL; u++) {  // first hit in CSC order
+            const unsigned hb = __ballot_sync(FULL, hit[u] != INF);
+            if (hb && !done) {
+              found = __shfl_sync(FULL, hit[u], __ffs(hb) - 1);
+              done = true;
+            }
+          }
+          if (done) break;
+          a = a0 + 128 * GBBS_LONG_UNROLL;
         }
         if (lane == l) {
           rem[q] = 0;
