@@ -125,6 +125,23 @@ int gbbs_bfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
              uint32_t *parent, void *cuda_stream);
 
 /*
+ * gbbs_bfs_batch / gbbs_bellman_ford_batch — k traversals, one per source
+ * srcs[0..k) (host array), with results in row i of dist (and parent):
+ * dist[i*n .. (i+1)*n).  Same results as k single calls.  With host outputs
+ * (pinned memory recommended) the device->host copy of traversal i overlaps
+ * traversal i+1 (double-buffered device staging of 8n bytes, allocated on first
+ * use, and a copy stream owned by the handle); device outputs are written in
+ * place.  The call returns when every row is written.
+ * Errors: GBBS_EINVAL (g NULL, k < 0, srcs or dist NULL with k > 0, a source
+ * >= n; nothing is run), else as gbbs_bfs / gbbs_bellman_ford for the first
+ * failing source (rows of the sources before it are complete).
+ */
+int gbbs_bfs_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                   uint32_t *dist, uint32_t *parent, void *cuda_stream);
+int gbbs_bellman_ford_batch(const gbbs_graph *g, const uint32_t *srcs,
+                            int64_t k, uint32_t *dist, void *cuda_stream);
+
+/*
  * gbbs_bellman_ford — frontier Bellman-Ford from src (output spec
  * P:1487-1490, sec:benchmark; algorithm, sec:algs).  Weights are the
  * uint32 weights given at create (non-negative, so no negative cycles;

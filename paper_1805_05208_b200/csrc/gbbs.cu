@@ -73,6 +73,9 @@ struct gbbs_graph {
   int *status = nullptr;
   long long *rounds = nullptr;
   uint32_t *tmp_dist = nullptr, *tmp_parent = nullptr;  // for host outputs
+  uint32_t *bst[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // batch staging [buf][dist/parent]
+  cudaStream_t cstream = nullptr;    // batch: device->host copy stream
+  cudaEvent_t cev[2] = {nullptr, nullptr};
   RoundStat *dstats = nullptr;
   long long dstats_cap = 0;
   unsigned long long *dcount = nullptr;
@@ -108,6 +111,12 @@ static void free_graph(gbbs_graph *g) {
   cudaFree(g->iso);
   cudaFree(g->tmp_dist);
   cudaFree(g->tmp_parent);
+  for (int i = 0; i < 2; i++) {
+    cudaFree(g->bst[i][0]);
+    cudaFree(g->bst[i][1]);
+    if (g->cev[i]) cudaEventDestroy(g->cev[i]);
+  }
+  if (g->cstream) cudaStreamDestroy(g->cstream);
   cudaFree(g->dstats);
   if (g->ev[0]) cudaEventDestroy(g->ev[0]);
   if (g->ev[1]) cudaEventDestroy(g->ev[1]);
@@ -764,6 +773,65 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   if (ctrl.status != 0)
     return fail(GBBS_EINTERNAL, "round cap (%lld rounds) exceeded", (long long)p.max_rounds);
   return GBBS_OK;
+}
+
+// Batch of traversals (one per source) into row i of dist/parent.  Host outputs:
+// traversal i writes double-buffered device staging; its device->host copy runs
+// on a second stream while traversal i+1 computes; traversal i+2 waits for the
+// copy that frees its buffer.  Device outputs: traversals write the rows directly.
+static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int64_t k,
+                     uint32_t *dist, uint32_t *parent, void *stream) {
+  g_last_error.clear();
+  if (!cg_) return fail(GBBS_EINVAL, "g is NULL");
+  gbbs_graph *g = const_cast<gbbs_graph *>(cg_);
+  if (k < 0 || (k > 0 && (!srcs || !dist))) return fail(GBBS_EINVAL, "bad batch arguments");
+  for (int64_t i = 0; i < k; i++)
+    if ((long long)srcs[i] >= g->n) return fail(GBBS_EINVAL, "srcs[%lld] = %u >= n %lld",
+                                                 (long long)i, srcs[i], g->n);
+  if (k == 0) return GBBS_OK;
+  const size_t n = (size_t)g->n;
+  const bool dist_dev = is_device_ptr(dist);
+  const bool par_dev = parent ? is_device_ptr(parent) : true;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dist_dev && par_dev) {
+    for (int64_t i = 0; i < k; i++) {
+      int rc = run(g, algo, srcs[i], dist + i * n, parent ? parent + i * n : nullptr, stream,
+                   nullptr, nullptr);
+      if (rc) return rc;
+    }
+    return GBBS_OK;
+  }
+  if (!g->cstream) {
+    CU(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; i++) CU(cudaEventCreateWithFlags(&g->cev[i], cudaEventDisableTiming));
+  }
+  for (int b = 0; b < 2; b++)
+    for (int j = 0; j < (parent ? 2 : 1); j++)
+      if (!g->bst[b][j]) CU(cudaMalloc(&g->bst[b][j], n * 4));
+  int rc = GBBS_OK;
+  for (int64_t i = 0; i < k && rc == GBBS_OK; i++) {
+    const int b = (int)(i & 1);
+    if (i >= 2) CU(cudaStreamWaitEvent(st, g->cev[b], 0));  // copy i-2 freed buffer b
+    rc = run(g, algo, srcs[i], g->bst[b][0], parent ? g->bst[b][1] : nullptr, stream, nullptr,
+             nullptr);  // returns with traversal i complete
+    if (rc) break;
+    CU(cudaMemcpyAsync(dist + i * n, g->bst[b][0], n * 4, cudaMemcpyDefault, g->cstream));
+    if (parent)
+      CU(cudaMemcpyAsync(parent + i * n, g->bst[b][1], n * 4, cudaMemcpyDefault, g->cstream));
+    CU(cudaEventRecord(g->cev[b], g->cstream));
+  }
+  CU(cudaStreamSynchronize(g->cstream));
+  return rc;
+}
+
+extern "C" int gbbs_bfs_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k, uint32_t *dist,
+                              uint32_t *parent, void *cuda_stream) {
+  return run_batch(g, ALGO_BFS, srcs, k, dist, parent, cuda_stream);
+}
+
+extern "C" int gbbs_bellman_ford_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                                       uint32_t *dist, void *cuda_stream) {
+  return run_batch(g, ALGO_BF, srcs, k, dist, nullptr, cuda_stream);
 }
 
 extern "C" int gbbs_bfs(const gbbs_graph *g, uint32_t src, uint32_t *dist, uint32_t *parent,

@@ -27,7 +27,8 @@ GBBS_MODE_AUTO, GBBS_MODE_SPARSE, GBBS_MODE_DENSE = 0, 1, 2
 EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_bfs",
            "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
            "gbbs_widest_path_ex", "gbbs_wbfs", "gbbs_wbfs_ex", "gbbs_bellman_ford_signed",
-           "gbbs_bellman_ford_signed_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
+           "gbbs_bellman_ford_signed_ex", "gbbs_bfs_batch", "gbbs_bellman_ford_batch",
+           "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
            "gbbs_launch_info", "gbbs_last_error")
 
 
@@ -72,6 +73,8 @@ def _load():
     lib.gbbs_bellman_ford_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts), ctypes.POINTER(gbbs_stats)]
     lib.gbbs_widest_path.argtypes = [p, u32, p, p]
     lib.gbbs_wbfs.argtypes = [p, u32, p, p]
+    lib.gbbs_bfs_batch.argtypes = [p, p, i64, p, p, p]
+    lib.gbbs_bellman_ford_batch.argtypes = [p, p, i64, p, p]
     lib.gbbs_bellman_ford_signed.argtypes = [p, u32, p, p]
     lib.gbbs_bellman_ford_signed_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts),
                                                 ctypes.POINTER(gbbs_stats)]
@@ -86,7 +89,8 @@ def _load():
     lib.gbbs_last_error.restype = ctypes.c_char_p
     for f in ("gbbs_graph_create", "gbbs_graph_info", "gbbs_bfs", "gbbs_bellman_ford", "gbbs_bfs_ex",
               "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_wbfs",
-              "gbbs_wbfs_ex", "gbbs_bellman_ford_signed", "gbbs_bellman_ford_signed_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
+              "gbbs_wbfs_ex", "gbbs_bellman_ford_signed", "gbbs_bellman_ford_signed_ex", "gbbs_bfs_batch",
+              "gbbs_bellman_ford_batch", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -195,6 +199,19 @@ def gbbs_bellman_ford_signed(handle, src, dist, stream=None, opts=None, stats=No
                                                ctypes.byref(stats) if stats is not None else None))
 
 
+def gbbs_bfs_batch(handle, srcs, dist, parent=None, stream=None):
+    """dist/parent: (k, n) uint32 arrays (row i = source i), host or device."""
+    s = np.ascontiguousarray(srcs, dtype=np.uint32)
+    st = _stream(stream, dist, parent)
+    _check(lib.gbbs_bfs_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), _ptr(parent), st))
+
+
+def gbbs_bellman_ford_batch(handle, srcs, dist, stream=None):
+    s = np.ascontiguousarray(srcs, dtype=np.uint32)
+    st = _stream(stream, dist)
+    _check(lib.gbbs_bellman_ford_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), st))
+
+
 def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
     st = _stream(stream, delta)
     if stats is None:
@@ -288,6 +305,12 @@ class Graph:
 
     def wbfs(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_wbfs(self.handle, src, dist, stream, opts, stats)
+
+    def bfs_batch(self, srcs, dist, parent=None, stream=None):
+        gbbs_bfs_batch(self.handle, srcs, dist, parent, stream)
+
+    def bellman_ford_batch(self, srcs, dist, stream=None):
+        gbbs_bellman_ford_batch(self.handle, srcs, dist, stream)
 
     def bellman_ford_signed(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_bellman_ford_signed(self.handle, src, dist, stream, opts, stats)

@@ -419,3 +419,38 @@ def test_bc_torus_and_grid(G):
     g = G.Graph(off, tgt, symmetric=True)
     assert_bc_close(run_bc(G, g, 0), oracle.betweenness(off, tgt, 0)[0])
     g.close()
+
+
+# ---- batch API (k traversals, copies overlapped) ------------------------------------
+
+def test_batch_matches_single_calls(G):
+    off, tgt = graphgen.rmat_graph(15, 1 << 19, 12, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 6, 15)
+    g = G.Graph(off, tgt, w, symmetric=True)
+    n = g.n
+    srcs = graphgen.choose_sources(np.nonzero(np.diff(off) > 0)[0], 5, 77)
+    refs = [oracle.bfs(off, tgt, s)[0] for s in srcs]
+    wrefs = [oracle.dijkstra(off, tgt, w, s)[0] for s in srcs]
+    # host (pinned) outputs: the overlapped path
+    hd = torch.empty((len(srcs), n), dtype=torch.int32, pin_memory=True)
+    hp = torch.empty_like(hd).pin_memory()
+    g.bfs_batch(srcs, hd.numpy(), hp.numpy())
+    for i, s in enumerate(srcs):
+        d, p = hd[i].numpy().view(np.uint32), hp[i].numpy().view(np.uint32)
+        assert (d == refs[i]).all() and oracle.check_bfs(off, tgt, s, d, p)[0]
+    # pageable host and device outputs, parent omitted
+    d2 = np.empty((len(srcs), n), np.uint32)
+    g.bfs_batch(srcs, d2)
+    assert all((d2[i] == refs[i]).all() for i in range(len(srcs)))
+    dd = torch.empty((len(srcs), n), dtype=torch.int32, device="cuda")
+    g.bfs_batch(srcs, dd)
+    dd = dd.cpu().numpy().view(np.uint32)
+    assert all((dd[i] == refs[i]).all() for i in range(len(srcs)))
+    bw = np.empty((len(srcs), n), np.uint32)
+    g.bellman_ford_batch(srcs, bw)
+    assert all((bw[i] == wrefs[i]).all() for i in range(len(srcs)))
+    g.bfs_batch([], np.empty((0, n), np.uint32))      # k = 0
+    with pytest.raises(G.GbbsError) as e:
+        g.bfs_batch([0, n], d2[:2])
+    assert e.value.code == -1
+    g.close()
