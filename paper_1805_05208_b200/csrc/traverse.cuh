@@ -436,6 +436,12 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
 // unprocessed, since distances only fall).  Lanes aiming at the same list are
 // grouped with match.any and reserve their slots with ONE atomicAdd.
 constexpr uint32_t XKEY = 64;    // near list
+// wBFS lane-owned push loop batch width (A/B knob: 8 and 16 edges per batch
+// measured 8 % and 20-65 % slower than 4 on c3/c4, tools/cmp_lib.sh)
+#ifndef GBBS_WBFS_LB
+#define GBBS_WBFS_LB 4
+#endif
+constexpr int WBFS_LB = GBBS_WBFS_LB;
 constexpr uint32_t NOKEY = 0xFFFFFFFFu;
 
 // Per-warp wBFS staging metadata in dynamic shared memory (wbfs_kernel only):
@@ -528,7 +534,7 @@ __device__ __forceinline__ void wbfs_stage(const Params &p, WarpState &ws, uint3
     }
     ws.scnt += __popc(bal);
   }
-  if (ws.scnt > WCAP - 32 * NB) {
+  if (ws.scnt > WCAP - 32 * WBFS_LB) {  // room for the widest batch (WBFS_LB chunks)
     wbfs_flush<STATS>(p, ws, st, ws.scnt, r);
     ws.scnt = 0;
   }
@@ -538,19 +544,19 @@ __device__ __forceinline__ void wbfs_stage(const Params &p, WarpState &ws, uint3
 // vv = targets, uu = owner id (BFS parent) or owner distance (BF), ww = weights.
 // EMIT_LIST: winners go to the warp's staging buffer (flushed into list cb^1).
 // EMIT_COUNT: winners are only counted (K, D) — the TS bits are the frontier.
-template <int ALGO, bool STATS, int EMIT>
+template <int ALGO, bool STATS, int EMIT, int NB>
 __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpState &ws,
-                                            const uint32_t (&vv)[NCH], const uint32_t (&uu)[NCH],
-                                            const uint32_t (&ww)[NCH], const bool (&act)[NCH],
+                                            const uint32_t (&vv)[NB], const uint32_t (&uu)[NB],
+                                            const uint32_t (&ww)[NB], const bool (&act)[NB],
                                             int nb, int r, uint32_t *bits, const uint32_t *prebits) {
   const int lane = threadIdx.x & 31;
-  bool win[NCH];
+  bool win[NB];
   if (ALGO == ALGO_BFS) {
-    uint32_t pre[NCH];
+    uint32_t pre[NB];
 #pragma unroll
-    for (int j = 0; j < NCH; j++) pre[j] = act[j] ? prebits[vv[j] >> 5] : FULL;
+    for (int j = 0; j < NB; j++) pre[j] = act[j] ? prebits[vv[j] >> 5] : FULL;
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < NB; j++) {
       const uint32_t bit = 1u << (vv[j] & 31);
       win[j] = false;
       if (!(pre[j] & bit)) {
@@ -559,7 +565,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       }
     }
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < NB; j++) {
       if (win[j]) {
         st_stream(p.dist + vv[j], (uint32_t)(r + 1));
         if (p.parent) st_stream(p.parent + vv[j], uu[j]);
@@ -569,15 +575,15 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     // Bellman-Ford: candidate d(u)+w, priority = smaller (atomicMin).
     // Widest path: candidate min(width(u), w), priority = larger (atomicMax) —
     // the (max, min) semiring in place of (min, +).
-    uint32_t nd[NCH];
+    uint32_t nd[NB];
     // Pre-check against the 16-bit shadow of dist (half the bytes of dist, meant
     // to stay in L2): BF keeps shadow >= min(dist, 0xFFFF) because distances only
     // fall and the shadow only ever receives values dist held; WP keeps
     // shadow <= width.  A relaxation the shadow proves useless is skipped; the
     // others go straight to the priority-write, whose returned old value decides.
-    uint32_t cur[NCH];
+    uint32_t cur[NB];
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < NB; j++) {
       // saturating: a sum reaching 2^32 - 1 cannot be stored below the INF
       // sentinel; it is flagged (status bit 2 -> GBBS_ERANGE) instead of the
       // conservative up-front check max(w) * (n - 1) < 2^32 - 1
@@ -591,10 +597,10 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       }
       cur[j] = act[j] ? (uint32_t)p.shadow[vv[j]] : (ALGO == ALGO_WP ? 0xFFFFu : 0u);
     }
-    bool cand[NCH];
-    uint32_t oldv[NCH];
+    bool cand[NB];
+    uint32_t oldv[NB];
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < NB; j++) {
       cand[j] = false;
       oldv[j] = 0;
       if (!act[j]) continue;
@@ -606,18 +612,21 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       } else if (nd[j] < cur[j] || cur[j] == 0xFFFFu) {
         const uint32_t old = atomicMin(p.dist + vv[j], nd[j]);  // priority-write
         cand[j] = nd[j] < old;
+#ifdef GBBS_DIAG_ATOMS  // diagnostic builds: executed priority-writes in `swept`
+        if (STATS) ws.swept += 1;
+#endif
         oldv[j] = old;
       }
     }
 #pragma unroll
-    for (int j = 0; j < NCH; j++)
+    for (int j = 0; j < NB; j++)
       if (cand[j]) p.shadow[vv[j]] = (uint16_t)min(nd[j], 0xFFFFu);
     if constexpr (ALGO == ALGO_WBFS) {
-      wbfs_stage<STATS, NCH>(p, ws, st, cand, vv, nd, oldv, r);
+      wbfs_stage<STATS, NB>(p, ws, st, cand, vv, nd, oldv, r);
       return;
     }
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < NB; j++) {
       win[j] = false;
       if (cand[j]) {
         const uint32_t bit = 1u << (vv[j] & 31);
@@ -627,9 +636,9 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     }
   }
   if (EMIT == EMIT_COUNT) {
-    long long lo[NCH], hi[NCH];
+    long long lo[NB], hi[NB];
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < NB; j++) {
       lo[j] = hi[j] = 0;
       if (win[j]) {
         lo[j] = __ldg(p.off + vv[j]);
@@ -637,20 +646,20 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       }
     }
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < NB; j++) {
       ws.K += hi[j] > lo[j];
       ws.D += (unsigned long long)(hi[j] - lo[j]);
       if (STATS) ws.acquired += win[j];
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < NB; j++) {
       const unsigned b = __ballot_sync(FULL, win[j]);
       GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
       if (win[j]) st[ws.scnt + __popc(b & lanemask_lt())] = vv[j];
       ws.scnt += __popc(b);
     }
-    if (ws.scnt > WCAP - 32 * NCH) {
+    if (ws.scnt > WCAP - 32 * NB) {
       if (STATS && lane == 0) ws.acquired += ws.scnt;
       warp_flush<ALGO>(p, st, ws.scnt, nb, r, bits);
       ws.scnt = 0;
@@ -919,11 +928,12 @@ __device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, Wa
   int mx = mine;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
-  for (int jj = 0; jj < mx; jj += NCH) {
-    uint32_t vv[NCH], ww[NCH], uu[NCH];
-    bool act[NCH];
+  constexpr int LB = (ALGO == ALGO_WBFS) ? WBFS_LB : NCH;
+  for (int jj = 0; jj < mx; jj += LB) {
+    uint32_t vv[LB], ww[LB], uu[LB];
+    bool act[LB];
 #pragma unroll
-    for (int j = 0; j < NCH; j++) {
+    for (int j = 0; j < LB; j++) {
       act[j] = jj + j < mine;
       GBBS_CHECK(!act[j] || (a + jj + j >= 0 && a + jj + j < p.m));
       vv[j] = act[j] ? ld_stream(p.tgt + a + jj + j) : 0;
@@ -1573,6 +1583,8 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
         list_round<ALGO_WBFS, STATS, EMIT_LIST>(p, wsm, ws, LIST_HEAVY, hf, hE, 0, (int)r, nullptr,
                                                 nullptr, gw, nw);
     }
+    unsigned long long t_work = 0;
+    if (STATS) t_work = globaltimer_ns();
     if (ws.scnt > 0) wbfs_flush<STATS>(p, ws, wsm.stage, ws.scnt, (int)r);
     // publish the lists this warp appended to
     unsigned long long pm = ws.pmask;
@@ -1580,6 +1592,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
     for (int o = 16; o > 0; o >>= 1) pm |= __shfl_xor_sync(FULL, pm, o);
     if (lane == 0 && pm) atomicOr(p.pub + xr, pm);
     if (STATS && p.stats && r < p.stats_cap) {
+      const unsigned long long t_flush = globaltimer_ns();
       const unsigned long long e = warp_sum64((long long)ws.edges);
       const unsigned long long sw = warp_sum64((long long)ws.swept);
       const unsigned long long aq = warp_sum64((long long)ws.acquired);
@@ -1587,6 +1600,8 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
         if (e) atomicAdd((unsigned long long *)&p.stats[r].edges_examined, e);
         if (sw) atomicAdd((unsigned long long *)&p.stats[r].vertices_swept, sw);
         if (aq) atomicAdd((unsigned long long *)&p.stats[r].acquired, aq);
+        atomicMax((unsigned long long *)&p.stats[r].t_work_ns, t_work);
+        atomicMax((unsigned long long *)&p.stats[r].t_flush_ns, t_flush);
       }
     }
     grid.sync();
