@@ -248,6 +248,12 @@ int gbbs_bellman_ford_signed(const gbbs_graph *g, uint32_t src, int64_t *dist,
 #define GBBS_MODE_AUTO 0
 #define GBBS_MODE_SPARSE 1 /* always push                                 */
 #define GBBS_MODE_DENSE 2  /* BFS: always pull; BF: bitmap-forward push   */
+#define GBBS_MODE_PULL 3   /* BFS: as AUTO; BF / widest path on symmetric
+                              graphs: a pull-min round (every vertex takes
+                              the best candidate over its in-edges from the
+                              frontier, no atomics) whenever
+                              |U| + sum deg(U) > m/T, else list push
+                              (SURVEY 8(a) a9's alternative, reading A11) */
 
 typedef struct {
   uint32_t threshold_den; /* T; 0 selects the default 20                  */

@@ -259,12 +259,12 @@ static int ensure_device_ok(int *dev_out) {
   return GBBS_OK;
 }
 
-template <int ALGO, bool STATS>
+template <int ALGO, bool STATS, bool PM = false>
 static int occupancy_grid(int *grid) {
   int dev = 0, nsm = 0, per = 0;
   CU(cudaGetDevice(&dev));
   CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, traverse_kernel<ALGO, STATS>, BLOCK, 0));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, traverse_kernel<ALGO, STATS, PM>, BLOCK, 0));
   if (per < 1) return fail(GBBS_ECUDA, "traverse kernel cannot be resident");
   *grid = per * nsm;
   return GBBS_OK;
@@ -473,11 +473,15 @@ __global__ void k_count_reached(const uint32_t *dist, long long n, unsigned long
   if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
 }
 
-template <int ALGO, bool STATS>
+template <int ALGO, bool STATS, bool PM = false>
 static int launch(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1,
                   unsigned ctas_per_sm) {
   void *args[] = {&p};
   int grid = g->grid[ALGO][STATS];
+  if constexpr (PM) {
+    int rc;
+    if ((rc = occupancy_grid<ALGO, STATS, true>(&grid))) return rc;
+  }
   if (ctas_per_sm) {
     int nsm = 0;
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
@@ -485,8 +489,8 @@ static int launch(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev0, cu
     if (want < grid) grid = (int)want;
   }
   if (ev0) CU(cudaEventRecord(ev0, st));
-  CU(cudaLaunchCooperativeKernel((const void *)traverse_kernel<ALGO, STATS>, grid, BLOCK, args, 0,
-                                 st));
+  CU(cudaLaunchCooperativeKernel((const void *)traverse_kernel<ALGO, STATS, PM>, grid, BLOCK, args,
+                                 0, st));
   if (ev1) CU(cudaEventRecord(ev1, st));
   return GBBS_OK;
 }
@@ -625,7 +629,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
     if (o.threshold_den == 0) o.threshold_den = 20;
     for (int i = 0; i < 3; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
-    if (o.mode < 0 || o.mode > 2) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
+    if (o.mode < 0 || o.mode > 3) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
   }
   int dev = 0;
   CU(cudaGetDevice(&dev));
@@ -712,8 +716,12 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   int rc;
   if (algo == ALGO_BFS)
     rc = want_rounds ? launch<ALGO_BFS, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_BFS, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
+  else if (algo == ALGO_BF && o.mode == GBBS_MODE_PULL)
+    rc = want_rounds ? launch<ALGO_BF, true, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_BF, false, true>(g, p, st, ev0, ev1, o.ctas_per_sm);
   else if (algo == ALGO_BF)
     rc = want_rounds ? launch<ALGO_BF, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_BF, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
+  else if (algo == ALGO_WP && o.mode == GBBS_MODE_PULL)
+    rc = want_rounds ? launch<ALGO_WP, true, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_WP, false, true>(g, p, st, ev0, ev1, o.ctas_per_sm);
   else if (algo == ALGO_WP)
     rc = want_rounds ? launch<ALGO_WP, true>(g, p, st, ev0, ev1, o.ctas_per_sm) : launch<ALGO_WP, false>(g, p, st, ev0, ev1, o.ctas_per_sm);
   else

@@ -1179,6 +1179,104 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
   __syncwarp();
 }
 
+// ---- dense pull-min (Bellman-Ford / widest path, GBBS_MODE_PULL) ---------------------
+// SURVEY §8(a) a9's alternative dense BF round (reading A11): every non-isolated
+// vertex v takes, over its in-edges (u, v) whose source is in the frontier
+// bitmap fr, the best candidate d(u) + w (BF) or min(d(u), w) (widest path), and
+// its owner lane writes it if it improves dist[v] — no atomics; the warp owns
+// its words, so the next frontier bitmap is written word-wise.  Symmetric graphs
+// only (the in-edge weights are the CSR weights at the same index).  In-lists
+// longer than 32 are scanned by the whole warp, 128 edges per step.
+template <int ALGO>
+__device__ __forceinline__ void pullmin_edge(const Params &p, const uint32_t *fr, uint32_t u,
+                                             long long e, uint32_t &best) {
+  if (!vbit(fr, u)) return;
+  const uint32_t du = ld_relaxed(p.dist + u);
+  const uint32_t w = p.wgt ? ld_stream(p.wgt + e) : 1u;
+  if (ALGO == ALGO_WP) {
+    best = max(best, min(du, w));
+  } else {
+    const uint32_t sum = du + w;
+    const bool ovf = sum < du || sum == INF;
+    if (ovf && du != INF) atomicOr(p.status, 2);
+    best = min(best, ovf ? INF : sum);
+  }
+}
+
+template <int ALGO, bool STATS>
+__device__ __forceinline__ void pullmin_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
+                                              const uint32_t *fr, uint32_t *nxt, WarpState &ws) {
+  constexpr uint32_t WORST = (ALGO == ALGO_WP) ? 0u : INF;
+  const int lane = threadIdx.x & 31;
+  SweepSmem &w = wsm.u.s;
+  const long long word = w0 + lane;
+  const bool mine = lane < sw && word < p.nwords;
+  const uint32_t cw = mine ? ~p.iso[word] : 0u;
+  if (mine) w.found[lane] = 0;
+  if (!__any_sync(FULL, cw != 0)) {
+    if (mine) nxt[word] = 0;
+    return;
+  }
+  const int cnt = warp_gather(w, w0, cw);
+  if (!mine) w.found[lane] = 0;
+  __syncwarp();
+  if (STATS && lane == 0) ws.swept += cnt;
+  for (int c0 = 0; c0 < cnt; c0 += 32) {
+    const bool valid = c0 + lane < cnt;
+    const uint32_t v = valid ? w.cand[c0 + lane] : 0;
+    long long js = 0, je = 0;
+    if (valid) {
+      js = ld_stream64(p.in_off + v);
+      je = ld_stream64(p.in_off + v + 1);
+    }
+    uint32_t best = WORST;
+    const bool longl = je - js > 32;
+    if (!longl) {
+      for (long long e = js; e < je; e++) {
+        GBBS_CHECK(e >= 0 && e < p.m);
+        pullmin_edge<ALGO>(p, fr, ld_stream(p.in_tgt + e), e, best);
+      }
+      if (STATS) ws.edges += je - js;
+    }
+    unsigned lg = __ballot_sync(FULL, longl);
+    while (lg) {  // long in-lists: the whole warp, then a warp reduction
+      const int l = __ffs(lg) - 1;
+      lg &= lg - 1;
+      const long long a = __shfl_sync(FULL, js, l), b = __shfl_sync(FULL, je, l);
+      uint32_t bl = WORST;
+      for (long long e = a + lane; e < b; e += 32) {
+        GBBS_CHECK(e >= 0 && e < p.m);
+        pullmin_edge<ALGO>(p, fr, ld_stream(p.in_tgt + e), e, bl);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t y = __shfl_xor_sync(FULL, bl, o);
+        bl = (ALGO == ALGO_WP) ? max(bl, y) : min(bl, y);
+      }
+      if (STATS && lane == 0) ws.edges += b - a;
+      if (lane == l) best = bl;
+    }
+    if (valid) {
+      const uint32_t cur = ld_relaxed(p.dist + v);
+      const bool imp = (ALGO == ALGO_WP) ? best > cur : best < cur;
+      if (imp) {  // only v's owner writes dist[v]
+        p.dist[v] = best;
+        p.shadow[v] = (uint16_t)min(best, 0xFFFFu);
+        atomicOr(&w.found[(v >> 5) - (uint32_t)w0], 1u << (v & 31));
+        const long long dgo = je - js;  // symmetric: out-degree = in-degree
+        if (dgo > 0) {
+          ws.K += 1;
+          ws.D += (unsigned long long)dgo;
+        }
+        if (STATS) ws.acquired += 1;
+      }
+    }
+  }
+  __syncwarp();
+  if (mine) nxt[word] = w.found[lane];
+  __syncwarp();
+}
+
 // ---- the persistent kernel ---------------------------------------------------
 
 template <int ALGO, bool STATS, int EMIT>
@@ -1219,7 +1317,9 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
                                   (ALGO == ALGO_BFS) ? precheck : bits, gw, nw);
 }
 
-template <int ALGO, bool STATS>
+// PM: the instantiation that contains the pull-min round (launched only for
+// GBBS_MODE_PULL), so its code does not raise the default kernels' registers.
+template <int ALGO, bool STATS, bool PM = false>
 #ifndef GBBS_MIN_CTAS
 #define GBBS_MIN_CTAS 4
 #endif
@@ -1293,11 +1393,15 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     // kind: 0 list push, 1 dense pull, 2 bitmap-forward.  BFS: dense pull iff
     // |U| + sum deg(U) > m/T.  Bellman-Ford: list push unless GBBS_MODE_DENSE
     // forces bitmap-forward rounds (reading A11: measured slower on rMAT).
+    // mode 3 (GBBS_MODE_PULL): BFS as auto; BF / widest path take a pull-min
+    // round (kind 3, symmetric graphs) when |U| + sum deg(U) > m/T
+    const bool over = f + E > p.dense_threshold;
     const bool big = (ALGO == ALGO_BFS)
-                         ? (p.mode == 2 || (p.mode == 0 && f + E > p.dense_threshold))
-                         : p.mode == 2;
+                         ? (p.mode == 2 || ((p.mode == 0 || p.mode == 3) && over))
+                         : (p.mode == 2 || (p.mode == 3 && over));
     int kind;
     if (ALGO == ALGO_BFS) kind = big ? 1 : (list_valid ? 0 : 2);
+    else if (PM && big && p.mode == 3 && p.symmetric) kind = 3;
     else kind = (big || !list_valid) ? 2 : 0;
     if (blockIdx.x == 0 && tid == 0) {
       p.cnt[(r + 2) & 3] = 0;
@@ -1317,6 +1421,16 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
       for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
         pull_words<STATS>(p, wsm, w0, sw, vis, vis_next, (int)r, ws);
       vc ^= 1;
+      list_valid = false;
+      emit_count = true;
+    } else if (kind == 3) {  // pull-min (BF / widest path, GBBS_MODE_PULL)
+      if constexpr (PM && ALGO != ALGO_BFS) {
+        // the frontier as a bitmap: a list frontier's TS bits already are one
+        for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
+          pullmin_words<ALGO, STATS>(p, wsm, w0, sw, p.bm[cb], p.bm[nb], ws);
+        grid.sync();  // every probe of bm[cb] is done: clear it for reuse as TS bits
+        for (long long i = gtid; i < p.nwords; i += gstride) p.bm[cb][i] = 0;
+      }
       list_valid = false;
       emit_count = true;
     } else if (kind == 2) {  // bitmap-forward

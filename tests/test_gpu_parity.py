@@ -454,3 +454,35 @@ def test_batch_matches_single_calls(G):
         g.bfs_batch([0, n], d2[:2])
     assert e.value.code == -1
     g.close()
+
+
+# ---- a9 alternative: pull-min dense rounds for Bellman-Ford / widest path ----------
+
+@pytest.mark.parametrize("T", [20, 1000])
+def test_pull_min_bf_and_widest(G, T):
+    """GBBS_MODE_PULL: a dense BF round is a pull-min (owner-computes, no atomics);
+    distances and widths identical to the oracle; directed graphs fall back to
+    the bitmap-forward push.  T = 1000 makes almost every round dense."""
+    cfg = graphgen.CONFIGS["c1"]
+    off, tgt = graphgen.rmat_graph(cfg.levels, 1 << cfg.log_edges, cfg.graph_seed, *cfg.abc)
+    w = graphgen.pair_weights(off, tgt, cfg.weight_seed, cfg.W)
+    cases = [(off, tgt, w, True)]
+    toff, ttgt = graphgen.torus3d(20)
+    cases.append((toff, ttgt, graphgen.pair_weights(toff, ttgt, 7, 24), True))
+    roff, rtgt = graphgen.random_graph(700, 0.01, 3, symmetric=True)
+    cases.append((roff, rtgt, graphgen.pair_weights(roff, rtgt, 3, 50), True))
+    doff, dtgt = graphgen.random_graph(700, 0.01, 4, symmetric=False)
+    cases.append((doff, dtgt, graphgen.pair_weights(doff, dtgt, 4, 50), False))
+    for o, t, ww, sym in cases:
+        g = G.Graph(o, t, ww, symmetric=sym)
+        opts = G.make_opts(T, G.GBBS_MODE_PULL)
+        for src in (0, 5):
+            d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+            st = G.make_stats(4096)
+            g.bellman_ford(src, d, opts=opts, stats=st)
+            assert (d.cpu().numpy().view(np.uint32) == oracle.dijkstra(o, t, ww, src)[0]).all()
+            if sym and T == 1000:
+                assert any(r["dense"] == 3 for r in G.round_records(st))
+            g.widest_path(src, d, opts=opts)
+            assert (d.cpu().numpy().view(np.uint32) == oracle.widest_path(o, t, ww, src)).all()
+        g.close()
