@@ -23,6 +23,7 @@ PRODUCT = dict(
     srcs=[os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "gbbs.cu")],
     deps=[os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "traverse.cuh"),
           os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "bc.cuh"),
+          os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "sbf.cuh"),
           os.path.join(ROOT, "include", "gbbs.h")],
 )
 GEN = dict(
