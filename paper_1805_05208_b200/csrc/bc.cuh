@@ -20,6 +20,17 @@
 
 #include "traverse.cuh"
 
+// Backward-pass A/B knobs (tools/bc_probe.py): SEG = one atomicAdd per (owner,
+// chunk) after a segmented warp sum (c2 -10 %, c4 -4 % time); SPEC = load the
+// target's sigma and delta speculatively beside its level (measured 35-55 %
+// slower: two extra random fp64 sectors per non-DAG edge).
+#ifndef GBBS_BC_SPEC
+#define GBBS_BC_SPEC 0
+#endif
+#ifndef GBBS_BC_SEG
+#define GBBS_BC_SEG 1
+#endif
+
 namespace gbbs_dev {
 
 struct BcParams {
@@ -210,11 +221,27 @@ __device__ __forceinline__ long long bc_tile(const BcParams &p, BcWarpSmem &w, i
         scnt = 0;
       }
     } else {
+#if GBBS_BC_SPEC  // level, sigma and delta of the target loaded together
+      uint32_t dv[NCH];
+      double sv[NCH], tv[NCH], su[NCH];
 #pragma unroll
       for (int j = 0; j < NCH; j++) {
+        dv[j] = act[j] ? p.dist[vv[j]] : INF;
+        sv[j] = act[j] ? p.sigma[vv[j]] : 1.0;
+        tv[j] = act[j] ? p.delta[vv[j]] : 0.0;
+        su[j] = act[j] ? p.sigma[uu[j]] : 0.0;
+      }
+#endif
+#pragma unroll
+      for (int j = 0; j < NCH; j++) {
+#if GBBS_BC_SPEC
+        double c = (dv[j] == nl) ? su[j] / sv[j] * (1.0 + tv[j]) : 0.0;
+#else
         double c = 0.0;
         if (act[j] && p.dist[vv[j]] == nl)
           c = p.sigma[uu[j]] / p.sigma[vv[j]] * (1.0 + p.delta[vv[j]]);
+#endif
+#if !GBBS_BC_SEG
         const unsigned same = __match_any_sync(FULL, act[j] ? uu[j] : INF);
         if (same == FULL) {  // one owner for the whole chunk (a hub): reduce first
 #pragma unroll
@@ -223,6 +250,22 @@ __device__ __forceinline__ long long bc_tile(const BcParams &p, BcWarpSmem &w, i
         } else if (c != 0.0) {
           atomicAdd(p.delta + uu[j], c);
         }
+        continue;
+#endif
+        // segmented sum over runs of the same owner (edges of an owner are
+        // contiguous in the chunk): ONE atomicAdd per (owner, chunk)
+        const uint32_t ow = act[j] ? uu[j] : INF;
+        const uint32_t prev = __shfl_up_sync(FULL, ow, 1);
+        const unsigned heads = __ballot_sync(FULL, lane == 0 || prev != ow);
+        const int seg0 = 31 - __clz(heads & lanemask_le());  // first lane of my run
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(FULL, c, o);
+          if (lane - o >= seg0) c += y;
+        }
+        const uint32_t next = __shfl_down_sync(FULL, ow, 1);
+        const bool last = lane == 31 || next != ow;
+        if (last && ow != INF && c != 0.0) atomicAdd(p.delta + ow, c);
       }
     }
   }
@@ -303,6 +346,12 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
     grid.sync();
   }
   const int L = l;  // levels with a non-empty list: 0 .. L-1
+#ifdef GBBS_DIAG_BC_FORWARD_ONLY  // measurement-only build
+  if (L > 0) {
+    if (blockIdx.x == 0 && tid == 0) *p.rounds_out = L;
+    return;
+  }
+#endif
   for (int b = L - 1; b >= 1; b--) {
     const long long st0 = p.lvl[3 * b], f = p.lvl[3 * b + 1], E = p.lvl[3 * b + 2];
     int scnt = 0;
