@@ -79,7 +79,33 @@ def test_c2_full(G):
         if i == 0:
             for T in (10, 40):
                 assert (gpu_bfs(G, g, n, s, T)[0] == ref).all()
-            assert (gpu_bf(G, g, n, s) == oracle.dijkstra(H["off"], H["tgt"], H["w"], s)[0]).all()
+            wref = oracle.dijkstra(H["off"], H["tgt"], H["w"], s)[0]
+            assert (gpu_bf(G, g, n, s) == wref).all()
+            for delta in (0, 4):                         # NEXT-2: wBFS and Delta-stepping
+                assert (gpu_wbfs(G, g, n, s, delta)[0] == wref).all(), delta
+    g.close()
+
+
+def test_c2_signed_johnson_full(G):
+    """NEXT-4 at full c2 size: Johnson reweighting w'(u,v) = w + phi(u) - phi(v)
+    makes ~half the edges negative without creating a negative cycle, so the signed
+    Bellman-Ford must return d(v) + phi(src) - phi(v) with d from the oracle's
+    Dijkstra on the original weights."""
+    from pins import johnson_reweight
+    D, H = build("c2", True)
+    n = D["n"]
+    phi = np.random.default_rng(11).integers(-1000, 1000, n).astype(np.int64)
+    w2 = johnson_reweight(H["off"], H["tgt"], H["w"], phi)
+    assert (w2.view(np.int32) < 0).mean() > 0.3
+    g = G.Graph(D["offsets"], D["targets"], w2, symmetric=True)
+    s = D["sources"][0]
+    ref = oracle.dijkstra64(H["off"], H["tgt"], H["w"], s)[0]
+    fin = ref != np.uint64(0xFFFFFFFFFFFFFFFF)
+    exp = np.full(n, np.iinfo(np.int64).max, np.int64)
+    exp[fin] = ref[fin].astype(np.int64) + phi[s] - phi[fin]
+    d = torch.empty(n, dtype=torch.int64, device="cuda")
+    g.bellman_ford_signed(s, d)
+    assert (d.cpu().numpy() == exp).all()
     g.close()
 
 
