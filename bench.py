@@ -6,7 +6,8 @@ Contract (task README + DESIGN.md §Measurement):
                   [--workload c2] [--algo bfs|bf]
 One step = one pass of the hot path over the workload's batch: BFS (direction-
 optimising, T=20) from each of the config's seeded sources on the resident graph
-(default c2: 8 sources in the largest component of the medium rMAT graph).  The
+(default c2: 8 sources in the largest component of the medium rMAT graph), issued
+as one gbbs_bfs_batch call into device rows.  The
 Bellman-Ford leg of the metric is measured in the same run on the same graph with
 weights in [1, floor(log2 n)] (reading A6) and reported under "bellman_ford".
 Multi-GPU: every rank holds its own copy of the graph and
@@ -266,10 +267,24 @@ def run_ours(args, rank, world, local):
                                       dense_rounds=st.dense_rounds, alg_bytes=alg, state_bytes=state,
                                       relax=sum(r["edges_examined"] for r in recs))
 
-    def timed(algo, steps, warmup):
-        for _ in range(warmup):
+    # one step = the batch call over this rank's sources into device rows (the k
+    # launches are enqueued back to back, one synchronisation per step); the NEXT
+    # legs use the per-source calls
+    drows = torch.empty((len(sources), n), dtype=torch.int32, device=dev)
+    prows = torch.empty_like(drows) if args.algo == "bfs" else None
+
+    def step(algo):
+        if algo == "bfs":
+            g.bfs_batch(sources, drows, prows, stream=stream, opts=opts)
+        elif algo == "bf":
+            g.bellman_ford_batch(sources, drows, stream=stream)
+        else:
             for s in sources:
                 one(s, algo)
+
+    def timed(algo, steps, warmup):
+        for _ in range(warmup):
+            step(algo)
         if world > 1:
             dist_mod.barrier()
         torch.cuda.synchronize()
@@ -280,8 +295,7 @@ def run_ours(args, rank, world, local):
             flush_buf.fill_(1)  # L2 flush between timed steps (outside the events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for s in sources:
-                one(s, algo)
+            step(algo)
             e1.record(stream)
             evs.append((e0, e1))
         torch.cuda.synchronize()

@@ -140,6 +140,9 @@ int gbbs_bfs_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
                    uint32_t *dist, uint32_t *parent, void *cuda_stream);
 int gbbs_bellman_ford_batch(const gbbs_graph *g, const uint32_t *srcs,
                             int64_t k, uint32_t *dist, void *cuda_stream);
+/* The k launches are enqueued without host synchronisation between them
+ * (each traversal's status word is kept in a device slot and checked after
+ * the single synchronisation at the end); _ex variants with options below. */
 
 /*
  * gbbs_bellman_ford — frontier Bellman-Ford from src (output spec
@@ -325,6 +328,14 @@ int gbbs_betweenness_ex(const gbbs_graph *g, uint32_t src, double *delta,
 int gbbs_bellman_ford_signed_ex(const gbbs_graph *g, uint32_t src, int64_t *dist,
                                 void *cuda_stream, const gbbs_opts *opts,
                                 gbbs_stats *stats);
+/* Batch calls with options (threshold T, modes 0-2; NULL = defaults;
+ * ctas_per_sm must be 0). */
+int gbbs_bfs_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                      uint32_t *dist, uint32_t *parent, void *cuda_stream,
+                      const gbbs_opts *opts);
+int gbbs_bellman_ford_batch_ex(const gbbs_graph *g, const uint32_t *srcs,
+                               int64_t k, uint32_t *dist, void *cuda_stream,
+                               const gbbs_opts *opts);
 int gbbs_wbfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                  void *cuda_stream, const gbbs_opts *opts, gbbs_stats *stats);
 int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *width,

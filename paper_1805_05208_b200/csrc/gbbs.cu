@@ -13,6 +13,7 @@
 #include <cstddef>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/gbbs.h"
 #include "traverse.cuh"
@@ -75,7 +76,10 @@ struct gbbs_graph {
   uint32_t *tmp_dist = nullptr, *tmp_parent = nullptr;  // for host outputs
   uint32_t *bst[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // batch staging [buf][dist/parent]
   cudaStream_t cstream = nullptr;    // batch: device->host copy stream
-  cudaEvent_t cev[2] = {nullptr, nullptr};
+  cudaEvent_t cev[2] = {nullptr, nullptr};  // batch: copy of buffer b done
+  cudaEvent_t kev[2] = {nullptr, nullptr};  // batch: traversal into buffer b done
+  long long *bstat = nullptr;        // batch: per-traversal (status, rounds) slots
+  long long bstat_cap = 0;
   RoundStat *dstats = nullptr;
   long long dstats_cap = 0;
   unsigned long long *dcount = nullptr;
@@ -115,8 +119,10 @@ static void free_graph(gbbs_graph *g) {
     cudaFree(g->bst[i][0]);
     cudaFree(g->bst[i][1]);
     if (g->cev[i]) cudaEventDestroy(g->cev[i]);
+    if (g->kev[i]) cudaEventDestroy(g->kev[i]);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
+  cudaFree(g->bstat);
   cudaFree(g->dstats);
   if (g->ev[0]) cudaEventDestroy(g->ev[0]);
   if (g->ev[1]) cudaEventDestroy(g->ev[1]);
@@ -615,6 +621,55 @@ static int launch_wbfs(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev
   return GBBS_OK;
 }
 
+// Kernel parameters of one traversal (no statistics) on device outputs.
+static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, uint32_t *dpar,
+                        const gbbs_opts &o, Params &p) {
+  memset(&p, 0, sizeof p);
+  p.n = g->n;
+  p.m = g->m;
+  p.off = g->off;
+  p.tgt = g->tgt;
+  p.wgt = g->wgt;
+  p.in_off = g->in_off;
+  p.in_tgt = g->in_tgt;
+  p.dist = ddist;
+  p.parent = (algo == ALGO_BFS) ? dpar : nullptr;
+  p.bm[0] = g->bm[0];
+  p.bm[1] = g->bm[1];
+  for (int i = 0; i < 3; i++) {
+    p.fv[i] = g->fv[i];
+    p.fo[i] = g->fo[i];
+    p.fb[i] = g->fb[i];
+  }
+  p.cnt = g->cnt;
+  p.hcnt = g->cnt + 8;
+  p.status = g->status;
+  p.rounds_out = g->rounds;
+  p.nwords = g->nwords;
+  p.dense_threshold = g->m / (long long)o.threshold_den;
+  p.max_rounds = g->n + 1;
+  p.ebits = g->ebits;
+  p.iso = g->iso;
+  p.odeg = g->odeg;
+  p.shadow = g->shadow;
+  p.symmetric = (g->flags & GBBS_SYMMETRIC) ? 1 : 0;
+  p.mode = o.mode;
+  p.src = src;
+}
+
+static int status_error(const gbbs_graph *g, int status, long long max_rounds) {
+  if (status & 4)
+    return fail(GBBS_ENOMEM, "wbfs: a bucket list exceeded its capacity of %llu entries "
+                "(device memory was short at first use; a larger delta needs fewer)",
+                g->wb ? g->wb->qcap : 0ull);
+  if (status & 2)  // a relaxation candidate reached 2^32 - 1 (uint32 distances)
+    return fail(GBBS_ERANGE, "a distance candidate reached 2^32-1 (max weight %u): "
+                "distances do not fit the uint32 output", g->maxw);
+  if (status != 0)
+    return fail(GBBS_EINTERNAL, "round cap (%lld rounds) exceeded", max_rounds);
+  return GBBS_OK;
+}
+
 static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, uint32_t *parent,
                void *stream, const gbbs_opts *opts, gbbs_stats *stats) {
   g_last_error.clear();
@@ -660,39 +715,9 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   }
 
   Params p;
-  memset(&p, 0, sizeof p);
-  p.n = g->n;
-  p.m = g->m;
-  p.off = g->off;
-  p.tgt = g->tgt;
-  p.wgt = g->wgt;
-  p.in_off = g->in_off;
-  p.in_tgt = g->in_tgt;
-  p.dist = ddist;
-  p.parent = (algo == ALGO_BFS) ? dpar : nullptr;
-  p.bm[0] = g->bm[0];
-  p.bm[1] = g->bm[1];
-  for (int i = 0; i < 3; i++) {
-    p.fv[i] = g->fv[i];
-    p.fo[i] = g->fo[i];
-    p.fb[i] = g->fb[i];
-  }
-  p.cnt = g->cnt;
-  p.hcnt = g->cnt + 8;
-  p.status = g->status;
-  p.rounds_out = g->rounds;
+  fill_params(g, algo, src, ddist, dpar, o, p);
   p.stats = want_rounds ? g->dstats : nullptr;
   p.stats_cap = cap;
-  p.nwords = g->nwords;
-  p.dense_threshold = g->m / (long long)o.threshold_den;
-  p.max_rounds = g->n + 1;
-  p.ebits = g->ebits;
-  p.iso = g->iso;
-  p.odeg = g->odeg;
-  p.shadow = g->shadow;
-  p.symmetric = (g->flags & GBBS_SYMMETRIC) ? 1 : 0;
-  p.mode = o.mode;
-  p.src = src;
 
   if (algo == ALGO_WBFS) {
     int rc2 = wbfs_setup(g, o.delta, p);
@@ -771,24 +796,17 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
               h[4 * i] / 1e3, h[4 * i + 1] / 1e3, h[4 * i + 2] / 1e3, h[4 * i + 3]);
   }
 #endif
-  if (ctrl.status & 4)
-    return fail(GBBS_ENOMEM, "wbfs: a bucket list exceeded its capacity of %llu entries "
-                "(device memory was short at first use; a larger delta needs fewer)",
-                g->wb ? g->wb->qcap : 0ull);
-  if (ctrl.status & 2)  // a relaxation candidate reached 2^32 - 1 (uint32 distances)
-    return fail(GBBS_ERANGE, "a distance candidate reached 2^32-1 (max weight %u): "
-                "distances do not fit the uint32 output", g->maxw);
-  if (ctrl.status != 0)
-    return fail(GBBS_EINTERNAL, "round cap (%lld rounds) exceeded", (long long)p.max_rounds);
-  return GBBS_OK;
+  return status_error(g, ctrl.status, p.max_rounds);
 }
 
-// Batch of traversals (one per source) into row i of dist/parent.  Host outputs:
-// traversal i writes double-buffered device staging; its device->host copy runs
-// on a second stream while traversal i+1 computes; traversal i+2 waits for the
-// copy that frees its buffer.  Device outputs: traversals write the rows directly.
+// Batch of traversals (one per source) into row i of dist/parent, enqueued with
+// no host synchronisation between them: each launch is followed by a copy of its
+// status word into a per-traversal device slot, and the host synchronises once.
+// Host outputs: traversal i writes double-buffered device staging and an event;
+// the copy stream waits for it and copies the rows while traversal i+1 computes;
+// traversal i+2 waits for the copy event that frees its buffer.
 static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int64_t k,
-                     uint32_t *dist, uint32_t *parent, void *stream) {
+                     uint32_t *dist, uint32_t *parent, void *stream, const gbbs_opts *opts) {
   g_last_error.clear();
   if (!cg_) return fail(GBBS_EINVAL, "g is NULL");
   gbbs_graph *g = const_cast<gbbs_graph *>(cg_);
@@ -797,49 +815,97 @@ static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int6
     if ((long long)srcs[i] >= g->n) return fail(GBBS_EINVAL, "srcs[%lld] = %u >= n %lld",
                                                  (long long)i, srcs[i], g->n);
   if (k == 0) return GBBS_OK;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  if (dev != g->device) CU(cudaSetDevice(g->device));
   const size_t n = (size_t)g->n;
   const bool dist_dev = is_device_ptr(dist);
   const bool par_dev = parent ? is_device_ptr(parent) : true;
+  const bool host_out = !(dist_dev && par_dev);
   cudaStream_t st = (cudaStream_t)stream;
-  if (dist_dev && par_dev) {
-    for (int64_t i = 0; i < k; i++) {
-      int rc = run(g, algo, srcs[i], dist + i * n, parent ? parent + i * n : nullptr, stream,
-                   nullptr, nullptr);
-      if (rc) return rc;
+  gbbs_opts o;
+  gbbs_default_opts(&o);
+  if (opts) {
+    o = *opts;
+    if (o.threshold_den == 0) o.threshold_den = 20;
+    for (int i = 0; i < 3; i++)
+      if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
+    if (o.mode < 0 || o.mode > 2 || o.ctas_per_sm != 0)
+      return fail(GBBS_EINVAL, "batch calls take modes 0-2 and ctas_per_sm = 0");
+  }
+  if (g->bstat_cap < k) {
+    cudaFree(g->bstat);
+    g->bstat = nullptr;
+    g->bstat_cap = 0;
+    CU(cudaMalloc(&g->bstat, (size_t)k * 16));
+    g->bstat_cap = k;
+  }
+  if (host_out) {
+    if (!g->cstream) {
+      CU(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; i++) {
+        CU(cudaEventCreateWithFlags(&g->cev[i], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&g->kev[i], cudaEventDisableTiming));
+      }
     }
-    return GBBS_OK;
+    for (int b = 0; b < 2; b++)
+      for (int j = 0; j < (parent ? 2 : 1); j++)
+        if (!g->bst[b][j]) CU(cudaMalloc(&g->bst[b][j], n * 4));
   }
-  if (!g->cstream) {
-    CU(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; i++) CU(cudaEventCreateWithFlags(&g->cev[i], cudaEventDisableTiming));
-  }
-  for (int b = 0; b < 2; b++)
-    for (int j = 0; j < (parent ? 2 : 1); j++)
-      if (!g->bst[b][j]) CU(cudaMalloc(&g->bst[b][j], n * 4));
-  int rc = GBBS_OK;
-  for (int64_t i = 0; i < k && rc == GBBS_OK; i++) {
+  for (int64_t i = 0; i < k; i++) {
     const int b = (int)(i & 1);
-    if (i >= 2) CU(cudaStreamWaitEvent(st, g->cev[b], 0));  // copy i-2 freed buffer b
-    rc = run(g, algo, srcs[i], g->bst[b][0], parent ? g->bst[b][1] : nullptr, stream, nullptr,
-             nullptr);  // returns with traversal i complete
-    if (rc) break;
-    CU(cudaMemcpyAsync(dist + i * n, g->bst[b][0], n * 4, cudaMemcpyDefault, g->cstream));
-    if (parent)
-      CU(cudaMemcpyAsync(parent + i * n, g->bst[b][1], n * 4, cudaMemcpyDefault, g->cstream));
-    CU(cudaEventRecord(g->cev[b], g->cstream));
+    uint32_t *dd = dist + i * n, *dp = parent ? parent + i * n : nullptr;
+    if (host_out) {
+      if (i >= 2) CU(cudaStreamWaitEvent(st, g->cev[b], 0));  // copy i-2 freed buffer b
+      dd = g->bst[b][0];
+      dp = parent ? g->bst[b][1] : nullptr;
+    }
+    Params p;
+    fill_params(g, algo, srcs[i], dd, dp, o, p);
+    const int rc = (algo == ALGO_BFS) ? launch<ALGO_BFS, false>(g, p, st, nullptr, nullptr, 0)
+                                      : launch<ALGO_BF, false>(g, p, st, nullptr, nullptr, 0);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(g->bstat + 2 * i, g->status, 16, cudaMemcpyDeviceToDevice, st));
+    if (host_out) {
+      CU(cudaEventRecord(g->kev[b], st));
+      CU(cudaStreamWaitEvent(g->cstream, g->kev[b], 0));
+      CU(cudaMemcpyAsync(dist + i * n, g->bst[b][0], n * 4, cudaMemcpyDefault, g->cstream));
+      if (parent)
+        CU(cudaMemcpyAsync(parent + i * n, g->bst[b][1], n * 4, cudaMemcpyDefault, g->cstream));
+      CU(cudaEventRecord(g->cev[b], g->cstream));
+    }
   }
-  CU(cudaStreamSynchronize(g->cstream));
-  return rc;
+  std::vector<long long> hs((size_t)k * 2);
+  CU(cudaMemcpyAsync(hs.data(), g->bstat, (size_t)k * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (host_out) CU(cudaStreamSynchronize(g->cstream));
+  for (int64_t i = 0; i < k; i++) {
+    const int rc = status_error(g, (int)(hs[2 * i] & 0xFFFFFFFF), g->n + 1);
+    if (rc) return rc;
+  }
+  return GBBS_OK;
 }
 
 extern "C" int gbbs_bfs_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k, uint32_t *dist,
                               uint32_t *parent, void *cuda_stream) {
-  return run_batch(g, ALGO_BFS, srcs, k, dist, parent, cuda_stream);
+  return run_batch(g, ALGO_BFS, srcs, k, dist, parent, cuda_stream, nullptr);
 }
 
 extern "C" int gbbs_bellman_ford_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
                                        uint32_t *dist, void *cuda_stream) {
-  return run_batch(g, ALGO_BF, srcs, k, dist, nullptr, cuda_stream);
+  return run_batch(g, ALGO_BF, srcs, k, dist, nullptr, cuda_stream, nullptr);
+}
+
+extern "C" int gbbs_bfs_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                                 uint32_t *dist, uint32_t *parent, void *cuda_stream,
+                                 const gbbs_opts *opts) {
+  return run_batch(g, ALGO_BFS, srcs, k, dist, parent, cuda_stream, opts);
+}
+
+extern "C" int gbbs_bellman_ford_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                                          uint32_t *dist, void *cuda_stream,
+                                          const gbbs_opts *opts) {
+  return run_batch(g, ALGO_BF, srcs, k, dist, nullptr, cuda_stream, opts);
 }
 
 extern "C" int gbbs_bfs(const gbbs_graph *g, uint32_t src, uint32_t *dist, uint32_t *parent,

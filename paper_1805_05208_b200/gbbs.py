@@ -28,7 +28,7 @@ EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_b
            "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
            "gbbs_widest_path_ex", "gbbs_wbfs", "gbbs_wbfs_ex", "gbbs_bellman_ford_signed",
            "gbbs_bellman_ford_signed_ex", "gbbs_bfs_batch", "gbbs_bellman_ford_batch",
-           "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
+           "gbbs_bfs_batch_ex", "gbbs_bellman_ford_batch_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
            "gbbs_launch_info", "gbbs_last_error")
 
 
@@ -75,6 +75,8 @@ def _load():
     lib.gbbs_wbfs.argtypes = [p, u32, p, p]
     lib.gbbs_bfs_batch.argtypes = [p, p, i64, p, p, p]
     lib.gbbs_bellman_ford_batch.argtypes = [p, p, i64, p, p]
+    lib.gbbs_bfs_batch_ex.argtypes = [p, p, i64, p, p, p, ctypes.POINTER(gbbs_opts)]
+    lib.gbbs_bellman_ford_batch_ex.argtypes = [p, p, i64, p, p, ctypes.POINTER(gbbs_opts)]
     lib.gbbs_bellman_ford_signed.argtypes = [p, u32, p, p]
     lib.gbbs_bellman_ford_signed_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts),
                                                 ctypes.POINTER(gbbs_stats)]
@@ -90,7 +92,8 @@ def _load():
     for f in ("gbbs_graph_create", "gbbs_graph_info", "gbbs_bfs", "gbbs_bellman_ford", "gbbs_bfs_ex",
               "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_wbfs",
               "gbbs_wbfs_ex", "gbbs_bellman_ford_signed", "gbbs_bellman_ford_signed_ex", "gbbs_bfs_batch",
-              "gbbs_bellman_ford_batch", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
+              "gbbs_bellman_ford_batch", "gbbs_bfs_batch_ex", "gbbs_bellman_ford_batch_ex",
+              "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -199,17 +202,26 @@ def gbbs_bellman_ford_signed(handle, src, dist, stream=None, opts=None, stats=No
                                                ctypes.byref(stats) if stats is not None else None))
 
 
-def gbbs_bfs_batch(handle, srcs, dist, parent=None, stream=None):
+def gbbs_bfs_batch(handle, srcs, dist, parent=None, stream=None, opts=None):
     """dist/parent: (k, n) uint32 arrays (row i = source i), host or device."""
     s = np.ascontiguousarray(srcs, dtype=np.uint32)
     st = _stream(stream, dist, parent)
-    _check(lib.gbbs_bfs_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), _ptr(parent), st))
+    if opts is None:
+        _check(lib.gbbs_bfs_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), _ptr(parent),
+                                  st))
+    else:
+        _check(lib.gbbs_bfs_batch_ex(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist),
+                                     _ptr(parent), st, ctypes.byref(opts)))
 
 
-def gbbs_bellman_ford_batch(handle, srcs, dist, stream=None):
+def gbbs_bellman_ford_batch(handle, srcs, dist, stream=None, opts=None):
     s = np.ascontiguousarray(srcs, dtype=np.uint32)
     st = _stream(stream, dist)
-    _check(lib.gbbs_bellman_ford_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), st))
+    if opts is None:
+        _check(lib.gbbs_bellman_ford_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), st))
+    else:
+        _check(lib.gbbs_bellman_ford_batch_ex(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist),
+                                              st, ctypes.byref(opts)))
 
 
 def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
@@ -306,11 +318,11 @@ class Graph:
     def wbfs(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_wbfs(self.handle, src, dist, stream, opts, stats)
 
-    def bfs_batch(self, srcs, dist, parent=None, stream=None):
-        gbbs_bfs_batch(self.handle, srcs, dist, parent, stream)
+    def bfs_batch(self, srcs, dist, parent=None, stream=None, opts=None):
+        gbbs_bfs_batch(self.handle, srcs, dist, parent, stream, opts)
 
-    def bellman_ford_batch(self, srcs, dist, stream=None):
-        gbbs_bellman_ford_batch(self.handle, srcs, dist, stream)
+    def bellman_ford_batch(self, srcs, dist, stream=None, opts=None):
+        gbbs_bellman_ford_batch(self.handle, srcs, dist, stream, opts)
 
     def bellman_ford_signed(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_bellman_ford_signed(self.handle, src, dist, stream, opts, stats)

@@ -449,6 +449,16 @@ def test_batch_matches_single_calls(G):
     bw = np.empty((len(srcs), n), np.uint32)
     g.bellman_ford_batch(srcs, bw)
     assert all((bw[i] == wrefs[i]).all() for i in range(len(srcs)))
+    for T in (10, 40):                                # options: threshold T, forced modes
+        for mode in (G.GBBS_MODE_SPARSE, G.GBBS_MODE_DENSE):
+            dd = torch.empty((len(srcs), n), dtype=torch.int32, device="cuda")
+            pp = torch.empty_like(dd)
+            g.bfs_batch(srcs, dd, pp, opts=G.make_opts(T, mode))
+            dd, pp = dd.cpu().numpy().view(np.uint32), pp.cpu().numpy().view(np.uint32)
+            for i, s in enumerate(srcs):
+                assert (dd[i] == refs[i]).all() and oracle.check_bfs(off, tgt, s, dd[i], pp[i])[0]
+    with pytest.raises(G.GbbsError):
+        g.bfs_batch(srcs, d2, opts=G.make_opts(20, G.GBBS_MODE_PULL))
     g.bfs_batch([], np.empty((0, n), np.uint32))      # k = 0
     with pytest.raises(G.GbbsError) as e:
         g.bfs_batch([0, n], d2[:2])
