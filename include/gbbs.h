@@ -275,7 +275,12 @@ typedef struct {
                              read literally, reading N1); 1 = exactly the
                              vertices reachable from such a cycle
                              (reading N2).  Other calls ignore it.         */
-  uint32_t reserved[3];   /* must be zero                                  */
+  uint32_t bsize;         /* edges per warp tile of a list-push round
+                             (edgeMapBlocked's block size):
+                             a power of two in [32, 256]; 0 (default) =
+                             256, halved while the round has fewer than
+                             two tiles per warp                            */
+  uint32_t reserved[2];   /* must be zero                                  */
 } gbbs_opts;
 
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */

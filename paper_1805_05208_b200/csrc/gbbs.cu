@@ -654,6 +654,7 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   p.shadow = g->shadow;
   p.symmetric = (g->flags & GBBS_SYMMETRIC) ? 1 : 0;
   p.mode = o.mode;
+  p.bsize = (int)o.bsize;
   p.src = src;
 }
 
@@ -682,9 +683,11 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   if (opts) {
     o = *opts;
     if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 3; i++)
+    for (int i = 0; i < 2; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.mode < 0 || o.mode > 3) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
+    if (o.bsize && (o.bsize < 32 || o.bsize > (uint32_t)TE || (o.bsize & (o.bsize - 1))))
+      return fail(GBBS_EINVAL, "bsize %u: a power of two in [32, %d], or 0", o.bsize, TE);
   }
   int dev = 0;
   CU(cudaGetDevice(&dev));
@@ -828,8 +831,10 @@ static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int6
   if (opts) {
     o = *opts;
     if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 3; i++)
+    for (int i = 0; i < 2; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
+    if (o.bsize && (o.bsize < 32 || o.bsize > (uint32_t)TE || (o.bsize & (o.bsize - 1))))
+      return fail(GBBS_EINVAL, "bsize %u: a power of two in [32, %d], or 0", o.bsize, TE);
     if (o.mode < 0 || o.mode > 2 || o.ctas_per_sm != 0)
       return fail(GBBS_EINVAL, "batch calls take modes 0-2 and ctas_per_sm = 0");
   }
@@ -959,7 +964,7 @@ extern "C" int gbbs_bellman_ford_signed_ex(const gbbs_graph *cg_, uint32_t src, 
   gbbs_default_opts(&o);
   if (opts) {
     o = *opts;
-    for (int i = 0; i < 3; i++)
+    for (int i = 0; i < 2; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.neg_scope > 1) return fail(GBBS_EINVAL, "bad neg_scope %u", o.neg_scope);
   }
@@ -1145,7 +1150,7 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   if (!delta) return fail(GBBS_EINVAL, "delta is NULL");
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   if (opts)
-      for (int i = 0; i < 3; i++)
+      for (int i = 0; i < 2; i++)
       if (opts->reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
   int rc = GBBS_OK;
   BcScratch *b = bc_scratch(g, &rc);

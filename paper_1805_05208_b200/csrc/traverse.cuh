@@ -119,7 +119,8 @@ struct Params {
   long long dense_threshold; // dense iff |U| + sum deg(U) > dense_threshold
   long long max_rounds;
   int ebits;
-  int mode;                  // 0 auto, 1 sparse, 2 dense
+  int mode;                  // 0 auto, 1 sparse, 2 dense, 3 pull
+  int bsize;                 // list-push tile edges (power of two in [32, TE]); 0 = adaptive
   int symmetric;
   uint32_t src;
   // wBFS (ALGO_WBFS) bucket structure, wbfs_kernel
@@ -1316,7 +1317,9 @@ __device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpSta
   // Tile size: TE, or smaller (power of two >= 32) when the round has fewer than
   // TE edges per warp, so a small round costs each warp a single batch.
   int TR = TE;
-  while (TR > 32 && (E + TR / 2 - 1) / (TR / 2) <= nw) TR >>= 1;
+  if (p.bsize) TR = p.bsize;  // fixed block size (gbbs_opts.bsize, edgeMapBlocked's bsize)
+  else
+    while (TR > 32 && (E + TR / 2 - 1) / (TR / 2) <= nw) TR >>= 1;
   // contiguous blocks of tiles per warp: one owner search per warp and round
   const long long ntiles = (E + TR - 1) / TR;
   const long long per = (ntiles + nw - 1) / nw;

@@ -496,3 +496,29 @@ def test_pull_min_bf_and_widest(G, T):
             g.widest_path(src, d, opts=opts)
             assert (d.cpu().numpy().view(np.uint32) == oracle.widest_path(o, t, ww, src)).all()
         g.close()
+
+
+def test_block_size_option(G):
+    """gbbs_opts.bsize (edgeMapBlocked's block size): every fixed tile size gives the
+    same distances as the adaptive default; invalid sizes are rejected."""
+    off, tgt = graphgen.rmat_graph(15, 1 << 19, 21, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 2, 15)
+    g = G.Graph(off, tgt, w, symmetric=True)
+    ref, _ = oracle.bfs(off, tgt, 0)
+    wref, _ = oracle.dijkstra(off, tgt, w, 0)
+    d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    p = torch.empty_like(d)
+    for bs in (32, 64, 128, 256):
+        for mode in (G.GBBS_MODE_AUTO, G.GBBS_MODE_SPARSE):
+            g.bfs(0, d, p, opts=G.make_opts(20, mode, bsize=bs))
+            dd, pp = d.cpu().numpy().view(np.uint32), p.cpu().numpy().view(np.uint32)
+            assert (dd == ref).all() and oracle.check_bfs(off, tgt, 0, dd, pp)[0], (bs, mode)
+        g.bellman_ford(0, d, opts=G.make_opts(bsize=bs))
+        assert (d.cpu().numpy().view(np.uint32) == wref).all(), bs
+        g.wbfs(0, d, opts=G.make_opts(bsize=bs))
+        assert (d.cpu().numpy().view(np.uint32) == wref).all(), bs
+    for bad in (16, 48, 512):
+        with pytest.raises(G.GbbsError) as e:
+            g.bfs(0, d, p, opts=G.make_opts(bsize=bad))
+        assert e.value.code == -1
+    g.close()
