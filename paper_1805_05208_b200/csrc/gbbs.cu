@@ -406,8 +406,8 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
   CU(cudaMalloc(&g->iso, (size_t)g->nwords * 4));
   k_isolated<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->in_off, n, g->nwords, g->iso);
   CU(cudaGetLastError());
-  CU(cudaMalloc(&g->cnt, 10 * 8));  // ring[4], status, rounds, count, -, heavy[2]
-  CU(cudaMemset(g->cnt, 0, 10 * 8));
+  CU(cudaMalloc(&g->cnt, 18 * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8]
+  CU(cudaMemset(g->cnt, 0, 18 * 8));
   g->status = (int *)(g->cnt + 4);
   g->rounds = (long long *)(g->cnt + 5);
   g->dcount = g->cnt + 6;
@@ -643,6 +643,7 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   }
   p.cnt = g->cnt;
   p.hcnt = g->cnt + 8;
+  p.wq = g->cnt + 10;
   p.status = g->status;
   p.rounds_out = g->rounds;
   p.nwords = g->nwords;

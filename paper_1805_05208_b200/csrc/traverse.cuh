@@ -111,6 +111,8 @@ struct Params {
   long long *fb[3];          //   base = offset(v) - O
   unsigned long long *cnt;   // packed (count << ebits | edges) ring [4]
   unsigned long long *hcnt;  // heavy-list packed counters [2]
+  unsigned long long *wq;    // rings [4] + [4] of per-round work-queue counters (sweeps and
+                             // list tiles; heavy-list tiles of a forward round)
   int *status;               // 0 ok, 1 = round cap hit
   long long *rounds_out;
   RoundStat *stats;          // per round, or nullptr
@@ -1027,6 +1029,17 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #ifndef GBBS_PCH
 #define GBBS_PCH 2
 #endif
+#ifndef GBBS_PULL_DYNQ
+#define GBBS_PULL_DYNQ 1
+#endif
+#ifndef GBBS_LIST_DYNQ
+#define GBBS_LIST_DYNQ 1
+#endif
+// words per dynamically assigned sweep unit (0 = sweep_unit's); measured (c2/c4/c5
+// BFS): 32 beats 16 and 8 by 2-5 % and 4 by 20 %; the queue itself -17 % on c4/c5
+#ifndef GBBS_PULL_SW
+#define GBBS_PULL_SW 32
+#endif
 #ifndef GBBS_PULL_STEPS
 #define GBBS_PULL_STEPS 2
 #endif
@@ -1313,15 +1326,36 @@ __device__ __forceinline__ void pullmin_words(const Params &p, WarpSmem &wsm, lo
 template <int ALGO, bool STATS, int EMIT>
 __device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpState &ws, int lb,
                                            long long f, long long E, int nb, int r, uint32_t *bits,
-                                           const uint32_t *prebits, long long gw, long long nw) {
+                                           const uint32_t *prebits, long long gw, long long nw,
+                                           unsigned long long *q = nullptr) {
   // Tile size: TE, or smaller (power of two >= 32) when the round has fewer than
   // TE edges per warp, so a small round costs each warp a single batch.
   int TR = TE;
   if (p.bsize) TR = p.bsize;  // fixed block size (gbbs_opts.bsize, edgeMapBlocked's bsize)
   else
     while (TR > 32 && (E + TR / 2 - 1) / (TR / 2) <= nw) TR >>= 1;
-  // contiguous blocks of tiles per warp: one owner search per warp and round
   const long long ntiles = (E + TR - 1) / TR;
+  if (ALGO != ALGO_BFS && GBBS_LIST_DYNQ && q && ntiles >= 16 * nw) {  // not compiled into BFS:
+    // it perturbed the BFS kernel's code generation (-5 to -9 %) without a BFS round using it.
+    // Big rounds: warps grab runs of G tiles from the round's counter (one owner
+    // search per grab), G sized for >= 4 grabs per warp — measured BF/widest path
+    // -10 % on c4; small rounds keep the static blocks (one search per warp),
+    // where a grab per tile cost c3 up to 19 %
+    const int lane = threadIdx.x & 31;
+    const long long G = max(1ll, min(16ll, ntiles / (4 * nw)));
+    for (;;) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(q, (unsigned long long)G);
+      long long t = (long long)__shfl_sync(FULL, u, 0);
+      if (t >= ntiles) break;
+      const long long t1 = min(t + G, ntiles);
+      long long i0 = warp_upper(p.fo[lb], 0, f, t * TR);
+      for (; t < t1; t++)
+        i0 = push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, i0, t, f, E, nb, r, bits, prebits, TR);
+    }
+    return;
+  }
+  // contiguous blocks of tiles per warp: one owner search per warp and round
   const long long per = (ntiles + nw - 1) / nw;
   long long t = gw * per;
   const long long t1 = min(t + per, ntiles);
@@ -1337,9 +1371,21 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
                                               uint32_t *bits, const uint32_t *precheck, int nb,
                                               int r, long long gw, long long nw,
                                               bool convert = false) {
-  const int sw = sweep_unit(p.nwords, nw);
-  for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
-    forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, sw, fr, bits, precheck, nb, r, convert);
+  if (GBBS_PULL_DYNQ) {  // dynamic unit assignment, as the dense pull
+    const int lane = threadIdx.x & 31;
+    const int psw = GBBS_PULL_SW ? GBBS_PULL_SW : sweep_unit(p.nwords, nw);
+    for (;;) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(p.wq + (r & 3), 1ull);
+      const long long w0 = (long long)__shfl_sync(FULL, u, 0) * psw;
+      if (w0 >= p.nwords) break;
+      forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, psw, fr, bits, precheck, nb, r, convert);
+    }
+  } else {
+    const int sw = sweep_unit(p.nwords, nw);
+    for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
+      forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, sw, fr, bits, precheck, nb, r, convert);
+  }
   if (ALGO == ALGO_BFS && convert && ws.scnt > 0) {
     warp_flush<ALGO>(p, w.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr, p.hcnt + (r & 1));
     ws.scnt = 0;
@@ -1352,7 +1398,8 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
   const long long hE = (long long)(hc & ((1ull << p.ebits) - 1));
   if (hf > 0)
     list_round<ALGO, STATS, EMIT>(p, w, ws, LIST_HEAVY, hf, hE, nb, r, bits,
-                                  (ALGO == ALGO_BFS) ? precheck : bits, gw, nw);
+                                  (ALGO == ALGO_BFS) ? precheck : bits, gw, nw,
+                                  p.wq + 4 + (r & 3));
 }
 
 // PM: the instantiation that contains the pull-min round (launched only for
@@ -1399,6 +1446,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
   if (blockIdx.x == 0 && tid == 0) {
     p.cnt[1] = p.cnt[2] = p.cnt[3] = 0;
     p.hcnt[0] = p.hcnt[1] = 0;
+    for (int q = 0; q < 8; q++) p.wq[q] = 0;
     if (d0 > 0) {
       p.fv[0][0] = src;
       p.fo[0][0] = 0;
@@ -1443,6 +1491,8 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     else kind = (big || !list_valid) ? 2 : 0;
     if (blockIdx.x == 0 && tid == 0) {
       p.cnt[(r + 2) & 3] = 0;
+      p.wq[(r + 2) & 3] = 0;
+      p.wq[4 + ((r + 2) & 3)] = 0;
       p.hcnt[(r + 1) & 1] = 0;
       if (STATS && p.stats && r < p.stats_cap) {
         p.stats[r].dense = kind;
@@ -1456,8 +1506,22 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     if (kind == 1) {  // dense pull (BFS)
       const uint32_t *vis = p.bm[vc];
       uint32_t *vis_next = p.bm[vc ^ 1];
-      for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
-        pull_words<STATS>(p, wsm, w0, sw, vis, vis_next, (int)r, ws);
+      if (GBBS_PULL_DYNQ) {
+        // dynamic assignment: a warp takes the next unit of psw words from a
+        // per-round counter as soon as it is done, so no warp waits at the
+        // barrier for another that drew two units
+        const int psw = GBBS_PULL_SW ? GBBS_PULL_SW : sw;
+        for (;;) {
+          unsigned long long u = 0;
+          if (lane == 0) u = atomicAdd(p.wq + (r & 3), 1ull);
+          const long long w0 = (long long)__shfl_sync(FULL, u, 0) * psw;
+          if (w0 >= p.nwords) break;
+          pull_words<STATS>(p, wsm, w0, psw, vis, vis_next, (int)r, ws);
+        }
+      } else {
+        for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
+          pull_words<STATS>(p, wsm, w0, sw, vis, vis_next, (int)r, ws);
+      }
       vc ^= 1;
       list_valid = false;
       emit_count = true;
@@ -1496,7 +1560,8 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
         const uint32_t *F = p.fv[cb];
         for (long long i = gtid; i < f; i += gstride) cur_bits[__ldcg(F + i) >> 5] = 0;
       }
-      list_round<ALGO, STATS, EMIT_LIST>(p, wsm, ws, cb, f, E, nb, (int)r, bits, bits, gw, nw);
+      list_round<ALGO, STATS, EMIT_LIST>(p, wsm, ws, cb, f, E, nb, (int)r, bits, bits, gw, nw,
+                                         p.wq + (r & 3));
       list_valid = true;
     }
     unsigned long long t_work = 0, t_flush = 0;
@@ -1591,6 +1656,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
     for (int q = 0; q < 3; q++) p.pub[q] = 0;
     p.hcnt[0] = p.hcnt[1] = 0;
     p.cnt[0] = p.cnt[1] = p.cnt[2] = 0;
+    for (int q = 0; q < 8; q++) p.wq[q] = 0;
     p.bq[0] = src;  // bucket 0 = {src}
     p.btail[0] = 1;
     p.bheavy[0] = (p.hv[src >> 5] >> (src & 31)) & 1u;
@@ -1665,6 +1731,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
       p.xcnt[nr] = p.xcnt[3 + nr] = 0;
       p.pub[nr] = 0;
       p.cnt[nr] = 0;
+      p.wq[(r + 2) & 3] = p.wq[4 + ((r + 2) & 3)] = 0;
       p.hcnt[(r + 1) & 1] = 0;
       if (STATS && p.stats && r < p.stats_cap) {
         p.stats[r].dense = slot >= 0 ? 3 : 4;
@@ -1724,7 +1791,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
         p.stats[r].frontier_edges = E;
       if (f > 0)
         list_round<ALGO_WBFS, STATS, EMIT_LIST>(p, wsm, ws, 0, f, E, 0, (int)r, nullptr, nullptr,
-                                                gw, nw);
+                                                gw, nw, p.wq + (r & 3));
     } else if (heavy_any) {  // hubs of this bucket, spread over all warps in list tiles
       grid.sync();
       if (tid == 0) s.hcnt = ld_relaxed64(p.hcnt + (r & 1));
@@ -1734,7 +1801,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
       const long long hE = (long long)(hc & ((1ull << p.ebits) - 1));
       if (hf > 0)
         list_round<ALGO_WBFS, STATS, EMIT_LIST>(p, wsm, ws, LIST_HEAVY, hf, hE, 0, (int)r, nullptr,
-                                                nullptr, gw, nw);
+                                                nullptr, gw, nw, p.wq + 4 + (r & 3));
     }
     unsigned long long t_work = 0;
     if (STATS) t_work = globaltimer_ns();
