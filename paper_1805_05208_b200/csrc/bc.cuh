@@ -30,6 +30,12 @@
 #ifndef GBBS_BC_SEG
 #define GBBS_BC_SEG 1
 #endif
+#ifndef GBBS_BC_DYNQ_FWD
+#define GBBS_BC_DYNQ_FWD 1
+#endif
+#ifndef GBBS_BC_DYNQ_BACK
+#define GBBS_BC_DYNQ_BACK 1
+#endif
 
 namespace gbbs_dev {
 
@@ -46,6 +52,7 @@ struct BcParams {
   long long *lvl;            // [3 * lvl_cap]: start, count, edges per level
   long long lvl_cap;
   unsigned long long *cnt;   // packed (count << ebits | edges) ring [4]
+  unsigned long long *wq;    // [8] tile work-queue counters: forward ring [4], backward ring [4]
   int *status;
   long long *rounds_out;
   int ebits;
@@ -277,11 +284,26 @@ template <bool BACK>
 __device__ __forceinline__ void bc_level(const BcParams &p, BcWarpSmem &w, int &scnt,
                                          long long start, long long f, long long E, int l,
                                          long long qnext, unsigned long long *ctr, long long gw,
-                                         long long nw) {
+                                         long long nw, unsigned long long *q) {
   const uint32_t *F = p.qv + start;
   const long long *O = p.qo + start;
   const long long *B = p.qb + start;
   const long long ntiles = (E + TE - 1) / TE;
+  if (((BACK && GBBS_BC_DYNQ_BACK) || (!BACK && GBBS_BC_DYNQ_FWD)) && ntiles >= 16 * nw) {
+    // big level: runs of G tiles from the level's counter
+    const int lane = threadIdx.x & 31;
+    const long long G = max(1ll, min(16ll, ntiles / (4 * nw)));
+    for (;;) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(q, (unsigned long long)G);
+      long long t = (long long)__shfl_sync(FULL, u, 0);
+      if (t >= ntiles) break;
+      const long long t1 = min(t + G, ntiles);
+      long long i0 = warp_upper(O, 0, f, t * TE);
+      for (; t < t1; t++) i0 = bc_tile<BACK>(p, w, scnt, F, O, B, f, E, i0, t, l, qnext, ctr);
+    }
+    return;
+  }
   const long long per = (ntiles + nw - 1) / nw;
   long long t = gw * per;
   const long long t1 = min(t + per, ntiles);
@@ -318,6 +340,7 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
       p.cnt[0] = 0;
     }
     *p.status = 0;
+    for (int q = 0; q < 8; q++) p.wq[q] = 0;
   }
   grid.sync();
 
@@ -335,12 +358,14 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
     }
     if (blockIdx.x == 0 && tid == 0) {
       p.cnt[(l + 2) & 3] = 0;
+      p.wq[(l + 2) & 3] = 0;
       p.lvl[3 * l] = start;
       p.lvl[3 * l + 1] = f;
       p.lvl[3 * l + 2] = E;
     }
     int scnt = 0;
-    bc_level<false>(p, w, scnt, start, f, E, l, start + f, p.cnt + ((l + 1) & 3), gw, nw);
+    bc_level<false>(p, w, scnt, start, f, E, l, start + f, p.cnt + ((l + 1) & 3), gw, nw,
+                    p.wq + (l & 3));
     if (scnt > 0) bc_flush(p, w.stage, scnt, start + f, p.cnt + ((l + 1) & 3));
     start += f;
     grid.sync();
@@ -355,7 +380,8 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
   for (int b = L - 1; b >= 1; b--) {
     const long long st0 = p.lvl[3 * b], f = p.lvl[3 * b + 1], E = p.lvl[3 * b + 2];
     int scnt = 0;
-    bc_level<true>(p, w, scnt, st0, f, E, b, 0, nullptr, gw, nw);
+    if (blockIdx.x == 0 && tid == 0) p.wq[4 + ((b - 2) & 3)] = 0;  // used two levels down
+    bc_level<true>(p, w, scnt, st0, f, E, b, 0, nullptr, gw, nw, p.wq + 4 + (b & 3));
     grid.sync();
   }
   if (blockIdx.x == 0 && tid == 0) *p.rounds_out = L;

@@ -1173,6 +1173,7 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   p.lvl = b->lvl;
   p.lvl_cap = b->lvl_cap;
   p.cnt = g->cnt;
+  p.wq = g->cnt + 10;
   p.status = g->status;
   p.rounds_out = g->rounds;
   p.ebits = g->ebits;
