@@ -1035,6 +1035,9 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #ifndef GBBS_LIST_DYNQ
 #define GBBS_LIST_DYNQ 1
 #endif
+#ifndef GBBS_LIST_DYNQ_BFS
+#define GBBS_LIST_DYNQ_BFS 0
+#endif
 // words per dynamically assigned sweep unit (0 = sweep_unit's); measured (c2/c4/c5
 // BFS): 32 beats 16 and 8 by 2-5 % and 4 by 20 %; the queue itself -17 % on c4/c5
 #ifndef GBBS_PULL_SW
@@ -1335,7 +1338,7 @@ __device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpSta
   else
     while (TR > 32 && (E + TR / 2 - 1) / (TR / 2) <= nw) TR >>= 1;
   const long long ntiles = (E + TR - 1) / TR;
-  if (ALGO != ALGO_BFS && GBBS_LIST_DYNQ && q && ntiles >= 16 * nw) {  // not compiled into BFS:
+  if ((ALGO != ALGO_BFS || GBBS_LIST_DYNQ_BFS) && GBBS_LIST_DYNQ && q && ntiles >= 16 * nw) {  // not compiled into BFS:
     // it perturbed the BFS kernel's code generation (-5 to -9 %) without a BFS round using it.
     // Big rounds: warps grab runs of G tiles from the round's counter (one owner
     // search per grab), G sized for >= 4 grabs per warp — measured BF/widest path
