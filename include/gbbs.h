@@ -280,7 +280,16 @@ typedef struct {
                              a power of two in [32, 256]; 0 (default) =
                              256, halved while the round has fewer than
                              two tiles per warp                            */
-  uint32_t reserved[2];   /* must be zero                                  */
+  uint32_t teams;         /* batch calls with device outputs: traversals
+                             run concurrently in one cooperative launch,
+                             the CTAs interleaved into this many teams of
+                             independent traversals (1-4).  0 = auto: 4 for
+                             BFS on graphs with n <= 2^24 and m <= 2^28
+                             (latency-bound traversals overlap), else 1.
+                             Teams 1-3 allocate their own scratch (~20n
+                             bytes of lists each) on first use.  Other
+                             calls ignore it.                              */
+  uint32_t reserved[1];   /* must be zero                                  */
 } gbbs_opts;
 
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */

@@ -80,6 +80,9 @@ struct gbbs_graph {
   cudaEvent_t kev[2] = {nullptr, nullptr};  // batch: traversal into buffer b done
   long long *bstat = nullptr;        // batch: per-traversal (status, rounds) slots
   long long bstat_cap = 0;
+  struct TeamScratch *team[4] = {nullptr, nullptr, nullptr, nullptr};  // batch teams 1..3
+  unsigned *bar0 = nullptr;          // team 0's barrier words
+  int mg_grid[3] = {0, 0, 0};        // co-resident CTAs of traverse_mg_kernel<ALGO>
   RoundStat *dstats = nullptr;
   long long dstats_cap = 0;
   unsigned long long *dcount = nullptr;
@@ -95,6 +98,7 @@ struct gbbs_graph {
 
 static void free_bc(gbbs_graph *g);
 static void free_wbfs(gbbs_graph *g);
+static void free_teams(gbbs_graph *g);
 
 static void free_graph(gbbs_graph *g) {
   if (!g) return;
@@ -128,6 +132,7 @@ static void free_graph(gbbs_graph *g) {
   if (g->ev[1]) cudaEventDestroy(g->ev[1]);
   free_bc(g);
   free_wbfs(g);
+  free_teams(g);
   cudaFree(g->tmp_sdist);
   delete g;
 }
@@ -621,6 +626,66 @@ static int launch_wbfs(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev
   return GBBS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// batch teams: scratch of the traversals that run beside team 0 in one launch
+// ---------------------------------------------------------------------------
+struct TeamScratch {
+  uint32_t *bm[2] = {nullptr, nullptr};
+  uint32_t *fv[3] = {nullptr, nullptr, nullptr};
+  long long *fo[3] = {nullptr, nullptr, nullptr};
+  long long *fb[3] = {nullptr, nullptr, nullptr};
+  unsigned long long *cnt = nullptr;  // same layout as the handle's (18 words)
+  uint16_t *shadow = nullptr;
+  unsigned *bar = nullptr;
+};
+
+static void free_teams(gbbs_graph *g) {
+  for (int t = 0; t < 4; t++) {
+    TeamScratch *x = g->team[t];
+    if (!x) continue;
+    for (int i = 0; i < 3; i++) {
+      if (i < 2) cudaFree(x->bm[i]);
+      cudaFree(x->fv[i]);
+      cudaFree(x->fo[i]);
+      cudaFree(x->fb[i]);
+    }
+    cudaFree(x->cnt);
+    cudaFree(x->shadow);
+    cudaFree(x->bar);
+    delete x;
+    g->team[t] = nullptr;
+  }
+  cudaFree(g->bar0);
+  g->bar0 = nullptr;
+}
+
+static int team_scratch(gbbs_graph *g, int t) {
+  if (t == 0) {
+    if (!g->bar0) {
+      CU(cudaMalloc(&g->bar0, 8));
+      CU(cudaMemset(g->bar0, 0, 8));
+    }
+    return GBBS_OK;
+  }
+  if (g->team[t]) return GBBS_OK;
+  TeamScratch *x = new (std::nothrow) TeamScratch();
+  if (!x) return fail(GBBS_ENOMEM, "host allocation");
+  g->team[t] = x;
+  const size_t n = (size_t)g->n;
+  for (int i = 0; i < 2; i++) CU(cudaMalloc(&x->bm[i], (size_t)g->nwords * 4));
+  for (int i = 0; i < 3; i++) {
+    CU(cudaMalloc(&x->fv[i], n * 4));
+    CU(cudaMalloc(&x->fo[i], n * 8));
+    CU(cudaMalloc(&x->fb[i], n * 8));
+  }
+  CU(cudaMalloc(&x->cnt, 18 * 8));
+  CU(cudaMemset(x->cnt, 0, 18 * 8));
+  CU(cudaMalloc(&x->shadow, n * 2));
+  CU(cudaMalloc(&x->bar, 8));
+  CU(cudaMemset(x->bar, 0, 8));
+  return GBBS_OK;
+}
+
 // Kernel parameters of one traversal (no statistics) on device outputs.
 static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, uint32_t *dpar,
                         const gbbs_opts &o, Params &p) {
@@ -659,6 +724,46 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   p.src = src;
 }
 
+// The same for team t of a multi-traversal launch (t = 0: the handle's scratch).
+static void fill_params_team(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist,
+                             uint32_t *dpar, const gbbs_opts &o, int t, Params &p) {
+  fill_params(g, algo, src, ddist, dpar, o, p);
+  if (t == 0) {
+    p.bar = g->bar0;
+    return;
+  }
+  TeamScratch *x = g->team[t];
+  p.bm[0] = x->bm[0];
+  p.bm[1] = x->bm[1];
+  for (int i = 0; i < 3; i++) {
+    p.fv[i] = x->fv[i];
+    p.fo[i] = x->fo[i];
+    p.fb[i] = x->fb[i];
+  }
+  p.cnt = x->cnt;
+  p.hcnt = x->cnt + 8;
+  p.wq = x->cnt + 10;
+  p.status = (int *)(x->cnt + 4);
+  p.rounds_out = (long long *)(x->cnt + 5);
+  p.shadow = x->shadow;
+  p.bar = x->bar;
+}
+
+template <int ALGO>
+static int launch_mg(gbbs_graph *g, MultiParams &mp, cudaStream_t st) {
+  if (!g->mg_grid[ALGO]) {
+    int nsm = 0, per = 0;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, traverse_mg_kernel<ALGO>, BLOCK, 0));
+    if (per < 1) return fail(GBBS_ECUDA, "multi-traversal kernel cannot be resident");
+    g->mg_grid[ALGO] = per * nsm;
+  }
+  void *args[] = {&mp};
+  CU(cudaLaunchCooperativeKernel((const void *)traverse_mg_kernel<ALGO>, g->mg_grid[ALGO], BLOCK,
+                                 args, 0, st));
+  return GBBS_OK;
+}
+
 static int status_error(const gbbs_graph *g, int status, long long max_rounds) {
   if (status & 4)
     return fail(GBBS_ENOMEM, "wbfs: a bucket list exceeded its capacity of %llu entries "
@@ -684,7 +789,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   if (opts) {
     o = *opts;
     if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 2; i++)
+    for (int i = 0; i < 1; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.mode < 0 || o.mode > 3) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
     if (o.bsize && (o.bsize < 32 || o.bsize > (uint32_t)TE || (o.bsize & (o.bsize - 1))))
@@ -832,12 +937,13 @@ static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int6
   if (opts) {
     o = *opts;
     if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 2; i++)
+    for (int i = 0; i < 1; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.bsize && (o.bsize < 32 || o.bsize > (uint32_t)TE || (o.bsize & (o.bsize - 1))))
       return fail(GBBS_EINVAL, "bsize %u: a power of two in [32, %d], or 0", o.bsize, TE);
     if (o.mode < 0 || o.mode > 2 || o.ctas_per_sm != 0)
       return fail(GBBS_EINVAL, "batch calls take modes 0-2 and ctas_per_sm = 0");
+    if (o.teams > (uint32_t)GMAX) return fail(GBBS_EINVAL, "teams %u > %d", o.teams, GMAX);
   }
   if (g->bstat_cap < k) {
     cudaFree(g->bstat);
@@ -858,7 +964,35 @@ static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int6
       for (int j = 0; j < (parent ? 2 : 1); j++)
         if (!g->bst[b][j]) CU(cudaMalloc(&g->bst[b][j], n * 4));
   }
-  for (int64_t i = 0; i < k; i++) {
+  // device outputs: G traversals per launch (teams).  Default (teams = 0): 4 for
+  // BFS on graphs with n <= 2^24 and m <= 2^28, else 1 — measured (tools/
+  // teams_probe.py): c2 BFS batch -31 % at 4 teams; BFS on c4/c5 and every BF
+  // batch slower with teams (throughput-bound rounds, teams contend for L2)
+  int G = 1;
+  if (!host_out) {
+    if (o.teams) G = (int)o.teams;
+    else if (algo == ALGO_BFS && g->n <= (1ll << 24) && g->m <= (1ll << 28)) G = 4;
+  }
+  if (G > 1) {
+    for (int t = 0; t < G; t++) {
+      const int rc = team_scratch(g, t);
+      if (rc) return rc;
+    }
+    for (int64_t i0 = 0; i0 < k; i0 += G) {
+      MultiParams mp;
+      memset(&mp, 0, sizeof mp);
+      mp.G = (int)((k - i0) < G ? (k - i0) : G);
+      for (int t = 0; t < mp.G; t++)
+        fill_params_team(g, algo, srcs[i0 + t], dist + (i0 + t) * n,
+                         parent ? parent + (i0 + t) * n : nullptr, o, t, mp.ps[t]);
+      const int rc = (algo == ALGO_BFS) ? launch_mg<ALGO_BFS>(g, mp, st) : launch_mg<ALGO_BF>(g, mp, st);
+      if (rc) return rc;
+      for (int t = 0; t < mp.G; t++)
+        CU(cudaMemcpyAsync(g->bstat + 2 * (i0 + t), mp.ps[t].status, 16,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  for (int64_t i = (G > 1 ? k : 0); i < k; i++) {
     const int b = (int)(i & 1);
     uint32_t *dd = dist + i * n, *dp = parent ? parent + i * n : nullptr;
     if (host_out) {
@@ -965,7 +1099,7 @@ extern "C" int gbbs_bellman_ford_signed_ex(const gbbs_graph *cg_, uint32_t src, 
   gbbs_default_opts(&o);
   if (opts) {
     o = *opts;
-    for (int i = 0; i < 2; i++)
+    for (int i = 0; i < 1; i++)
       if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
     if (o.neg_scope > 1) return fail(GBBS_EINVAL, "bad neg_scope %u", o.neg_scope);
   }
@@ -1151,7 +1285,7 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   if (!delta) return fail(GBBS_EINVAL, "delta is NULL");
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   if (opts)
-      for (int i = 0; i < 2; i++)
+      for (int i = 0; i < 1; i++)
       if (opts->reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
   int rc = GBBS_OK;
   BcScratch *b = bc_scratch(g, &rc);

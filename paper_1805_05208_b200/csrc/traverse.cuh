@@ -111,6 +111,7 @@ struct Params {
   long long *fb[3];          //   base = offset(v) - O
   unsigned long long *cnt;   // packed (count << ebits | edges) ring [4]
   unsigned long long *hcnt;  // heavy-list packed counters [2]
+  unsigned *bar;             // team barrier (count, generation) of a multi-traversal launch
   unsigned long long *wq;    // rings [4] + [4] of per-round work-queue counters (sweeps and
                              // list tiles; heavy-list tiles of a forward round)
   int *status;               // 0 ok, 1 = round cap hit
@@ -1368,12 +1369,46 @@ __device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpSta
     i0 = push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, i0, t, f, E, nb, r, bits, prebits, TR);
 }
 
-template <int ALGO, bool STATS, int EMIT>
+// ---- teams: several traversals in one cooperative launch --------------------------
+// A multi-traversal launch (MG) interleaves the CTAs into G teams, one traversal
+// each with its own scratch; a team synchronises with a sense-counting barrier on
+// its own two words instead of the grid barrier.  MG = false is the plain
+// single-traversal kernel (grid.sync, the whole grid as the team).
+__device__ __forceinline__ unsigned ld_acquire32(const unsigned *a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a));
+  return v;
+}
+
+template <bool MG>
+__device__ __forceinline__ void team_sync(cg::grid_group &grid, unsigned *bar, long long nblk) {
+  if constexpr (!MG) {
+    grid.sync();
+  } else {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned g0 = ld_acquire32(bar + 1);  // generation, read before arriving
+      __threadfence();
+      if (atomicAdd(bar, 1u) == (unsigned)nblk - 1) {
+        bar[0] = 0;  // last arriver: reset, then release the team
+        __threadfence();
+        atomicAdd(bar + 1, 1u);
+      } else {
+        while (ld_acquire32(bar + 1) == g0) {
+        }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+
+template <int ALGO, bool STATS, int EMIT, bool MG = false>
 __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid_group &grid,
                                               WarpSmem &w, WarpState &ws, uint32_t *fr,
                                               uint32_t *bits, const uint32_t *precheck, int nb,
                                               int r, long long gw, long long nw,
-                                              bool convert = false) {
+                                              bool convert = false, long long nblk = 0) {
   if (GBBS_PULL_DYNQ) {  // dynamic unit assignment, as the dense pull
     const int lane = threadIdx.x & 31;
     const int psw = GBBS_PULL_SW ? GBBS_PULL_SW : sweep_unit(p.nwords, nw);
@@ -1393,7 +1428,7 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
     warp_flush<ALGO>(p, w.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr, p.hcnt + (r & 1));
     ws.scnt = 0;
   }
-  grid.sync();  // heavy list complete
+  team_sync<MG>(grid, p.bar, nblk);  // heavy list complete
   if (threadIdx.x == 0) s.hcnt = ld_relaxed64(p.hcnt + (r & 1));
   __syncthreads();
   const unsigned long long hc = s.hcnt;
@@ -1405,20 +1440,27 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
                                   p.wq + 4 + (r & 3));
 }
 
-// PM: the instantiation that contains the pull-min round (launched only for
-// GBBS_MODE_PULL), so its code does not raise the default kernels' registers.
-template <int ALGO, bool STATS, bool PM = false>
-#ifndef GBBS_MIN_CTAS
-#define GBBS_MIN_CTAS 4
-#endif
-__global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p) {
-  __shared__ Smem s;
+// The traversal: per-run init, then edgeMap rounds until the frontier is empty.
+// (bid, nblk) = this CTA's index and the number of CTAs in its team (MG: CTA b
+// serves team b mod G).
+template <int ALGO, bool STATS, bool PM, bool MG>
+__device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
   cg::grid_group grid = cg::this_grid();
+  // MG: team-local index and size; the single-traversal kernel reads the special
+  // registers at each use (holding them in registers raised its spills)
+  long long bid_ = 0, nblk_ = 0;
+  if constexpr (MG) {
+    const int g = (int)(blockIdx.x % G);
+    bid_ = blockIdx.x / G;
+    nblk_ = ((long long)gridDim.x - g + G - 1) / G;
+  }
+#define GBBS_BID (MG ? bid_ : (long long)blockIdx.x)
+#define GBBS_NBLK (MG ? nblk_ : (long long)gridDim.x)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long gtid = (long long)blockIdx.x * BLOCK + tid;
-  const long long gstride = (long long)gridDim.x * BLOCK;
-  const long long gw = (long long)blockIdx.x * NWARPS + warp;
-  const long long nw = (long long)gridDim.x * NWARPS;
+  const long long gtid = GBBS_BID * BLOCK + tid;
+  const long long gstride = GBBS_NBLK * BLOCK;
+  const long long gw = GBBS_BID * NWARPS + warp;
+  const long long nw = GBBS_NBLK * NWARPS;
   const uint32_t src = p.src;
   const int sw = sweep_unit(p.nwords, nw);
   WarpSmem &wsm = s.w[warp];
@@ -1446,7 +1488,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     }
   }
   const long long a0 = p.off[src], d0 = p.off[src + 1] - a0;
-  if (blockIdx.x == 0 && tid == 0) {
+  if (GBBS_BID == 0 && tid == 0) {
     p.cnt[1] = p.cnt[2] = p.cnt[3] = 0;
     p.hcnt[0] = p.hcnt[1] = 0;
     for (int q = 0; q < 8; q++) p.wq[q] = 0;
@@ -1460,7 +1502,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     }
     *p.status = 0;
   }
-  grid.sync();
+  team_sync<MG>(grid, p.bar, GBBS_NBLK);
 
   const unsigned long long emask = (1ull << p.ebits) - 1;
   int vc = 0;              // BFS: index of the current visited bitmap
@@ -1472,11 +1514,11 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     const unsigned long long c = s.cnt;
     const long long f = (long long)(c >> p.ebits);
     const long long E = (long long)(c & emask);
-    if (STATS && blockIdx.x == 0 && tid == 0 && p.stats && r < p.stats_cap)
+    if (STATS && GBBS_BID == 0 && tid == 0 && p.stats && r < p.stats_cap)
       p.stats[r].t_start_ns = (long long)globaltimer_ns();
     if (f == 0) break;
     if (r >= p.max_rounds) {
-      if (blockIdx.x == 0 && tid == 0) *p.status = 1;
+      if (GBBS_BID == 0 && tid == 0) *p.status = 1;
       break;
     }
     // kind: 0 list push, 1 dense pull, 2 bitmap-forward.  BFS: dense pull iff
@@ -1492,7 +1534,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
     if (ALGO == ALGO_BFS) kind = big ? 1 : (list_valid ? 0 : 2);
     else if (PM && big && p.mode == 3 && p.symmetric) kind = 3;
     else kind = (big || !list_valid) ? 2 : 0;
-    if (blockIdx.x == 0 && tid == 0) {
+    if (GBBS_BID == 0 && tid == 0) {
       p.cnt[(r + 2) & 3] = 0;
       p.wq[(r + 2) & 3] = 0;
       p.wq[4 + ((r + 2) & 3)] = 0;
@@ -1533,26 +1575,26 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
         // the frontier as a bitmap: a list frontier's TS bits already are one
         for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
           pullmin_words<ALGO, STATS>(p, wsm, w0, sw, p.bm[cb], p.bm[nb], ws);
-        grid.sync();  // every probe of bm[cb] is done: clear it for reuse as TS bits
+        team_sync<MG>(grid, p.bar, GBBS_NBLK);  // every probe of bm[cb] is done: clear it for reuse as TS bits
         for (long long i = gtid; i < p.nwords; i += gstride) p.bm[cb][i] = 0;
       }
       list_valid = false;
       emit_count = true;
     } else if (kind == 2) {  // bitmap-forward
       if (ALGO == ALGO_BFS) {
-        forward_round<ALGO, STATS, EMIT_LIST>(
+        forward_round<ALGO, STATS, EMIT_LIST, MG>(
             s, p, grid, wsm, ws, nullptr, p.bm[vc ^ 1], p.bm[vc], nb, (int)r, gw, nw,
-            GBBS_FWD_CONVERT && E >= (long long)GBBS_FWD_CONVERT_DEG * f);
+            GBBS_FWD_CONVERT && E >= (long long)GBBS_FWD_CONVERT_DEG * f, GBBS_NBLK);
         vc ^= 1;
         list_valid = true;
       } else if (big) {
-        forward_round<ALGO, STATS, EMIT_COUNT>(s, p, grid, wsm, ws, p.bm[cb], p.bm[nb], nullptr,
-                                               nb, (int)r, gw, nw);
+        forward_round<ALGO, STATS, EMIT_COUNT, MG>(s, p, grid, wsm, ws, p.bm[cb], p.bm[nb],
+                                                   nullptr, nb, (int)r, gw, nw, false, GBBS_NBLK);
         list_valid = false;
         emit_count = true;
       } else {
-        forward_round<ALGO, STATS, EMIT_LIST>(s, p, grid, wsm, ws, p.bm[cb], p.bm[nb], nullptr,
-                                              nb, (int)r, gw, nw);
+        forward_round<ALGO, STATS, EMIT_LIST, MG>(s, p, grid, wsm, ws, p.bm[cb], p.bm[nb],
+                                                  nullptr, nb, (int)r, gw, nw, false, GBBS_NBLK);
         list_valid = true;
       }
     } else {  // list push
@@ -1602,9 +1644,36 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS) traverse_kernel(Params p
         atomicMax((unsigned long long *)&p.stats[r].t_flush_ns, s.sacc[4]);
       }
     }
-    grid.sync();
+    team_sync<MG>(grid, p.bar, GBBS_NBLK);
   }
-  if (blockIdx.x == 0 && tid == 0) *p.rounds_out = r;
+  if (GBBS_BID == 0 && tid == 0) *p.rounds_out = r;
+}
+#undef GBBS_BID
+#undef GBBS_NBLK
+
+#ifndef GBBS_MIN_CTAS
+#define GBBS_MIN_CTAS 4
+#endif
+// PM: the instantiation that contains the pull-min round (launched only for
+// GBBS_MODE_PULL), so its code does not raise the default kernels' registers.
+template <int ALGO, bool STATS, bool PM = false>
+__global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS)
+    traverse_kernel(const __grid_constant__ Params p) {
+  __shared__ Smem s;
+  traverse_body<ALGO, STATS, PM, false>(p, s, 1);
+}
+
+// G traversals in one cooperative launch: CTA b serves team b mod G.
+constexpr int GMAX = 4;
+struct MultiParams {
+  Params ps[GMAX];
+  int G;
+};
+template <int ALGO>
+__global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS)
+    traverse_mg_kernel(const __grid_constant__ MultiParams mp) {
+  __shared__ Smem s;
+  traverse_body<ALGO, false, false, true>(mp.ps[blockIdx.x % mp.G], s, mp.G);
 }
 
 // ---- wBFS: integral-weight SSSP over buckets (NEXT-2) ---------------------------------

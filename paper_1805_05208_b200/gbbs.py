@@ -42,7 +42,7 @@ class gbbs_opts(ctypes.Structure):
     _fields_ = [("threshold_den", ctypes.c_uint32), ("mode", ctypes.c_int32),
                 ("ctas_per_sm", ctypes.c_uint32), ("delta", ctypes.c_uint32),
                 ("neg_scope", ctypes.c_uint32), ("bsize", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32 * 2)]
+                ("teams", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 1)]
 
 
 class gbbs_round_stat(ctypes.Structure):
@@ -233,7 +233,8 @@ def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
         _check(lib.gbbs_betweenness_ex(handle, int(src), _ptr(delta), st, None, ctypes.byref(stats)))
 
 
-def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0, neg_scope=0, bsize=0):
+def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0, neg_scope=0, bsize=0,
+              teams=0):
     o = gbbs_opts()
     lib.gbbs_default_opts(ctypes.byref(o))
     o.threshold_den = threshold_den
@@ -242,6 +243,7 @@ def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0, neg
     o.delta = delta
     o.neg_scope = neg_scope
     o.bsize = bsize
+    o.teams = teams
     return o
 
 

@@ -522,3 +522,42 @@ def test_block_size_option(G):
             g.bfs(0, d, p, opts=G.make_opts(bsize=bad))
         assert e.value.code == -1
     g.close()
+
+
+@pytest.mark.parametrize("teams", [2, 3, 4])
+def test_batch_teams(G, teams):
+    """gbbs_opts.teams: G traversals per cooperative launch (interleaved CTA teams,
+    each with its own scratch and barrier) give the same rows as single calls,
+    including a batch size that is not a multiple of G and every direction mode."""
+    off, tgt = graphgen.rmat_graph(16, 1 << 20, 33, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 9, 16)
+    g = G.Graph(off, tgt, w, symmetric=True)
+    n = g.n
+    srcs = graphgen.choose_sources(np.nonzero(np.diff(off) > 0)[0], 7, 91)
+    refs = [oracle.bfs(off, tgt, s)[0] for s in srcs]
+    wrefs = [oracle.dijkstra(off, tgt, w, s)[0] for s in srcs]
+    for mode in (G.GBBS_MODE_AUTO, G.GBBS_MODE_SPARSE, G.GBBS_MODE_DENSE):
+        dd = torch.empty((len(srcs), n), dtype=torch.int32, device="cuda")
+        pp = torch.empty_like(dd)
+        g.bfs_batch(srcs, dd, pp, opts=G.make_opts(20, mode, teams=teams))
+        dd, pp = dd.cpu().numpy().view(np.uint32), pp.cpu().numpy().view(np.uint32)
+        for i, s in enumerate(srcs):
+            assert (dd[i] == refs[i]).all(), (mode, i)
+            assert oracle.check_bfs(off, tgt, s, dd[i], pp[i])[0], (mode, i)
+    bw = torch.empty((len(srcs), n), dtype=torch.int32, device="cuda")
+    g.bellman_ford_batch(srcs, bw, opts=G.make_opts(teams=teams))
+    bw = bw.cpu().numpy().view(np.uint32)
+    assert all((bw[i] == wrefs[i]).all() for i in range(len(srcs)))
+    g.close()
+    # directed graph (CSC pulls) with teams
+    doff, dtgt = graphgen.rmat_graph(15, 1 << 19, 35, 0.6, 0.15, 0.15, symmetric=False)
+    g = G.Graph(doff, dtgt, symmetric=False)
+    ds = graphgen.choose_sources(np.nonzero(np.diff(doff) > 0)[0], 5, 92)
+    dd = torch.empty((len(ds), g.n), dtype=torch.int32, device="cuda")
+    pp = torch.empty_like(dd)
+    g.bfs_batch(ds, dd, pp, opts=G.make_opts(teams=teams))
+    dd, pp = dd.cpu().numpy().view(np.uint32), pp.cpu().numpy().view(np.uint32)
+    for i, s in enumerate(ds):
+        assert (dd[i] == oracle.bfs(doff, dtgt, s)[0]).all()
+        assert oracle.check_bfs(doff, dtgt, s, dd[i], pp[i])[0]
+    g.close()
