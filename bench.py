@@ -170,8 +170,8 @@ def reached_edges(torch, off, d):
 
 
 def ncu_traffic(workload, algo):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of traverse_kernel from the
-    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from
+    the committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
@@ -374,7 +374,7 @@ def run_ours(args, rank, world, local):
                        "edges_per_step_all_ranks": edges_job},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic,
+                         "traffic": traffic, "traffic_unit": "bytes per launch of the kernel below",
                          "peak_source": peak_src, "copy_gbs_same_run": round(copy_gbs, 1),
                          "frac_of_copy_same_run": round(achieved / copy_gbs, 4),
                          "kernel": kname, "teams": teams,
