@@ -350,7 +350,8 @@ def run_ours(args, rank, world, local):
         copy_gbs = copy_bandwidth(torch)
         alg_bytes = sum(per_src[(args.algo, s)]["alg_bytes"] for s in sources)
         # the step's launches: G traversals each (gbbs_opts.teams auto rule, gbbs.h)
-        teams = 4 if (args.algo == "bfs" and n <= (1 << 24) and m <= (1 << 28)) else 1
+        teams = min(8, len(sources)) if (args.algo == "bfs" and n <= (1 << 24)
+                                         and m <= (1 << 28)) else 1
         launches = -(-len(sources) // teams)
         kname = ("gbbs_dev::traverse_mg_kernel<BFS> (persistent; %d traversals per launch, "
                  "%d launches per step)" % (teams, launches)) if teams > 1 else \

@@ -283,10 +283,10 @@ typedef struct {
   uint32_t teams;         /* batch calls with device outputs: traversals
                              run concurrently in one cooperative launch,
                              the CTAs interleaved into this many teams of
-                             independent traversals (1-4).  0 = auto: 4 for
+                             independent traversals (1-8).  0 = auto: 8 for
                              BFS on graphs with n <= 2^24 and m <= 2^28
                              (latency-bound traversals overlap), else 1.
-                             Teams 1-3 allocate their own scratch (~20n
+                             Teams 1-7 allocate their own scratch (~60n
                              bytes of lists each) on first use.  Other
                              calls ignore it.                              */
   uint32_t reserved[1];   /* must be zero                                  */

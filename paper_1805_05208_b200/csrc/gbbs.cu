@@ -80,7 +80,7 @@ struct gbbs_graph {
   cudaEvent_t kev[2] = {nullptr, nullptr};  // batch: traversal into buffer b done
   long long *bstat = nullptr;        // batch: per-traversal (status, rounds) slots
   long long bstat_cap = 0;
-  struct TeamScratch *team[4] = {nullptr, nullptr, nullptr, nullptr};  // batch teams 1..3
+  struct TeamScratch *team[8] = {};  // batch teams 1..7
   unsigned *bar0 = nullptr;          // team 0's barrier words
   int mg_grid[3] = {0, 0, 0};        // co-resident CTAs of traverse_mg_kernel<ALGO>
   RoundStat *dstats = nullptr;
@@ -640,7 +640,7 @@ struct TeamScratch {
 };
 
 static void free_teams(gbbs_graph *g) {
-  for (int t = 0; t < 4; t++) {
+  for (int t = 0; t < 8; t++) {
     TeamScratch *x = g->team[t];
     if (!x) continue;
     for (int i = 0; i < 3; i++) {
@@ -964,14 +964,15 @@ static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int6
       for (int j = 0; j < (parent ? 2 : 1); j++)
         if (!g->bst[b][j]) CU(cudaMalloc(&g->bst[b][j], n * 4));
   }
-  // device outputs: G traversals per launch (teams).  Default (teams = 0): 4 for
+  // device outputs: G traversals per launch (teams).  Default (teams = 0): 8 for
   // BFS on graphs with n <= 2^24 and m <= 2^28, else 1 — measured (tools/
-  // teams_probe.py): c2 BFS batch -31 % at 4 teams; BFS on c4/c5 and every BF
-  // batch slower with teams (throughput-bound rounds, teams contend for L2)
+  // teams_probe.py): the c2 8-source BFS batch takes 1.34 / 0.94 / 0.88 ms with
+  // 1 / 4 / 8 teams; BFS on c4/c5 and every BF batch got slower with teams
+  // (throughput-bound rounds, the teams contend for L2)
   int G = 1;
   if (!host_out) {
     if (o.teams) G = (int)o.teams;
-    else if (algo == ALGO_BFS && g->n <= (1ll << 24) && g->m <= (1ll << 28)) G = 4;
+    else if (algo == ALGO_BFS && g->n <= (1ll << 24) && g->m <= (1ll << 28)) G = 8;
   }
   if (G > 1) {
     for (int t = 0; t < G; t++) {

@@ -1664,7 +1664,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS)
 }
 
 // G traversals in one cooperative launch: CTA b serves team b mod G.
-constexpr int GMAX = 4;
+constexpr int GMAX = 8;
 struct MultiParams {
   Params ps[GMAX];
   int G;

@@ -24,7 +24,7 @@ def main():
         algos = ("bfs", "bf") if G["weights"] is not None else ("bfs",)
         for algo in algos:
             base = None
-            for teams in (1, 2, 3, 4):
+            for teams in [int(x) for x in os.environ.get("TEAMS", "1,2,3,4").split(",")]:
                 opts = gbbs.make_opts(teams=teams)
                 ts = []
                 for rep in range(4):
