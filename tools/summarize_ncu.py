@@ -48,12 +48,13 @@ def full(rep, label=""):
     try:
         i = hdr.index("gpu__time_duration.sum")
         t_ms = float(rows[2][i]) if units[i] == "ms" else float(rows[2][i]) / 1e3
-        rd = float(rows[2][hdr.index("dram__bytes_read.sum")])
-        wr = float(rows[2][hdr.index("dram__bytes_write.sum")])
-        u = units[hdr.index("dram__bytes_read.sum")]
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[u]
-        print(f"{'derived: dram read+write bytes':60s} {(rd + wr) * scale:.4e}")
-        print(f"{'derived: achieved DRAM GB/s':60s} {(rd + wr) * scale / (t_ms * 1e-3) / 1e9:.1f}")
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
+        rd = float(rows[2][hdr.index("dram__bytes_read.sum")]) * \
+            scale[units[hdr.index("dram__bytes_read.sum")]]
+        wr = float(rows[2][hdr.index("dram__bytes_write.sum")]) * \
+            scale[units[hdr.index("dram__bytes_write.sum")]]
+        print(f"{'derived: dram read+write bytes':60s} {rd + wr:.4e}")
+        print(f"{'derived: achieved DRAM GB/s':60s} {(rd + wr) / (t_ms * 1e-3) / 1e9:.1f}")
     except (ValueError, KeyError, IndexError):
         pass
     print()
