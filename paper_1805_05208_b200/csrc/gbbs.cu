@@ -627,6 +627,29 @@ static int launch_wbfs(gbbs_graph *g, Params &p, cudaStream_t st, cudaEvent_t ev
 }
 
 // ---------------------------------------------------------------------------
+// options: defaults and validation shared by every entry point
+// ---------------------------------------------------------------------------
+enum OptsKind { OPTS_TRAVERSE, OPTS_BATCH, OPTS_SIGNED, OPTS_OTHER };
+
+static int parse_opts(const gbbs_opts *opts, OptsKind kind, gbbs_opts &o) {
+  gbbs_default_opts(&o);
+  if (!opts) return GBBS_OK;
+  o = *opts;
+  if (o.threshold_den == 0) o.threshold_den = 20;
+  for (int i = 0; i < 1; i++)
+    if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
+  const int max_mode = (kind == OPTS_BATCH) ? 2 : 3;
+  if (o.mode < 0 || o.mode > max_mode) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
+  if (o.bsize && (o.bsize < 32 || o.bsize > (uint32_t)TE || (o.bsize & (o.bsize - 1))))
+    return fail(GBBS_EINVAL, "bsize %u: a power of two in [32, %d], or 0", o.bsize, TE);
+  if (kind == OPTS_BATCH && o.ctas_per_sm != 0)
+    return fail(GBBS_EINVAL, "batch calls take ctas_per_sm = 0");
+  if (o.teams > (uint32_t)GMAX) return fail(GBBS_EINVAL, "teams %u > %d", o.teams, GMAX);
+  if (o.neg_scope > 1) return fail(GBBS_EINVAL, "bad neg_scope %u", o.neg_scope);
+  return GBBS_OK;
+}
+
+// ---------------------------------------------------------------------------
 // batch teams: scratch of the traversals that run beside team 0 in one launch
 // ---------------------------------------------------------------------------
 struct TeamScratch {
@@ -785,16 +808,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   if (!dist) return fail(GBBS_EINVAL, "dist is NULL");
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   gbbs_opts o;
-  gbbs_default_opts(&o);
-  if (opts) {
-    o = *opts;
-    if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 1; i++)
-      if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
-    if (o.mode < 0 || o.mode > 3) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
-    if (o.bsize && (o.bsize < 32 || o.bsize > (uint32_t)TE || (o.bsize & (o.bsize - 1))))
-      return fail(GBBS_EINVAL, "bsize %u: a power of two in [32, %d], or 0", o.bsize, TE);
-  }
+  if (int rc0 = parse_opts(opts, OPTS_TRAVERSE, o)) return rc0;
   int dev = 0;
   CU(cudaGetDevice(&dev));
   if (dev != g->device) CU(cudaSetDevice(g->device));
@@ -933,18 +947,7 @@ static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int6
   const bool host_out = !(dist_dev && par_dev);
   cudaStream_t st = (cudaStream_t)stream;
   gbbs_opts o;
-  gbbs_default_opts(&o);
-  if (opts) {
-    o = *opts;
-    if (o.threshold_den == 0) o.threshold_den = 20;
-    for (int i = 0; i < 1; i++)
-      if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
-    if (o.bsize && (o.bsize < 32 || o.bsize > (uint32_t)TE || (o.bsize & (o.bsize - 1))))
-      return fail(GBBS_EINVAL, "bsize %u: a power of two in [32, %d], or 0", o.bsize, TE);
-    if (o.mode < 0 || o.mode > 2 || o.ctas_per_sm != 0)
-      return fail(GBBS_EINVAL, "batch calls take modes 0-2 and ctas_per_sm = 0");
-    if (o.teams > (uint32_t)GMAX) return fail(GBBS_EINVAL, "teams %u > %d", o.teams, GMAX);
-  }
+  if (int rc0 = parse_opts(opts, OPTS_BATCH, o)) return rc0;
   if (g->bstat_cap < k) {
     cudaFree(g->bstat);
     g->bstat = nullptr;
@@ -1097,13 +1100,7 @@ extern "C" int gbbs_bellman_ford_signed_ex(const gbbs_graph *cg_, uint32_t src, 
   if (!dist) return fail(GBBS_EINVAL, "dist is NULL");
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   gbbs_opts o;
-  gbbs_default_opts(&o);
-  if (opts) {
-    o = *opts;
-    for (int i = 0; i < 1; i++)
-      if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
-    if (o.neg_scope > 1) return fail(GBBS_EINVAL, "bad neg_scope %u", o.neg_scope);
-  }
+  if (int rc0 = parse_opts(opts, OPTS_SIGNED, o)) return rc0;
   int dev = 0;
   CU(cudaGetDevice(&dev));
   if (dev != g->device) CU(cudaSetDevice(g->device));
@@ -1285,9 +1282,8 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   gbbs_graph *g = const_cast<gbbs_graph *>(cg_);
   if (!delta) return fail(GBBS_EINVAL, "delta is NULL");
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
-  if (opts)
-      for (int i = 0; i < 1; i++)
-      if (opts->reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
+  gbbs_opts o;
+  if (int rc0 = parse_opts(opts, OPTS_OTHER, o)) return rc0;
   int rc = GBBS_OK;
   BcScratch *b = bc_scratch(g, &rc);
   if (!b) return rc;
