@@ -38,6 +38,9 @@ def full(rep, label=""):
             "l1tex__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
             "launch__occupancy_limit_registers", "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum",
+            "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_atom.sum",
+            "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum",
+            "lts__t_sectors.sum", "lts__t_requests.sum",
             "lts__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum"]
     print(f"# ncu --set full --clock-control none: {label or rep}")
     for r in rows[2:]:
@@ -55,6 +58,15 @@ def full(rep, label=""):
             scale[units[hdr.index("dram__bytes_write.sum")]]
         print(f"{'derived: dram read+write bytes':60s} {rd + wr:.4e}")
         print(f"{'derived: achieved DRAM GB/s':60s} {(rd + wr) / (t_ms * 1e-3) / 1e9:.1f}")
+        for nm, lab in (("l1tex__m_l1tex2xbar_write_sectors_mem_global_op_atom.sum", "atomic"),
+                        ("l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum", "reduction")):
+            if nm in hdr:
+                x = float(rows[2][hdr.index(nm)].replace(",", ""))
+                print(f"{'derived: global ' + lab + ' sectors to L2 per second (G)':60s} "
+                      f"{x / (t_ms * 1e-3) / 1e9:.2f}")
+        if "lts__t_sectors.sum" in hdr:
+            x = float(rows[2][hdr.index("lts__t_sectors.sum")].replace(",", ""))
+            print(f"{'derived: L2 sectors per second (G)':60s} {x / (t_ms * 1e-3) / 1e9:.1f}")
     except (ValueError, KeyError, IndexError):
         pass
     print()
