@@ -169,13 +169,17 @@ def reached_edges(torch, off, d):
     return int(deg[d != -1].sum())
 
 
-def ncu_traffic(workload, algo):
+def ncu_traffic(workload, algo, what="bytes"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from
-    the committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    the committed ncu --set full capture (profiles/ncu_traffic.json), or None;
+    what="us": that launch's ncu duration."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(workload, {}).get(algo)
+            d = json.load(f)
+        if what == "us":
+            return d.get("_duration_us", {}).get(workload, {}).get(algo)
+        return d.get(workload, {}).get(algo)
     except (OSError, ValueError):
         return None
 
@@ -376,6 +380,12 @@ def run_ours(args, rank, world, local):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "traffic_unit": "bytes per launch of the kernel below",
+                         # context: the DRAM utilisation ncu measured for that launch
+                         # (cold-cache, serialised replay; its duration, not this run's)
+                         "ncu_dram_frac": (round(traffic / (ncu_traffic(cfg.name, args.algo, "us")
+                                                           * 1e-6) / 1e9 / peak, 4)
+                                           if traffic and ncu_traffic(cfg.name, args.algo, "us")
+                                           else None),
                          "peak_source": peak_src, "copy_gbs_same_run": round(copy_gbs, 1),
                          "frac_of_copy_same_run": round(achieved / copy_gbs, 4),
                          "kernel": kname, "teams": teams,
