@@ -282,6 +282,8 @@ def run_ours(args, rank, world, local):
             g.bfs_batch(sources, drows, prows, stream=stream, opts=opts)
         elif algo == "bf":
             g.bellman_ford_batch(sources, drows, stream=stream)
+        elif algo == "wbfs":
+            g.wbfs_batch(sources, drows, stream=stream)
         else:
             for s in sources:
                 one(s, algo)
@@ -431,7 +433,8 @@ def run_ours(args, rank, world, local):
                 "value": round(we / (wt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective)",
                 "ms_per_step": round(wt, 4), "kernel_ms_per_step": round(wkms, 4),
                 "note": "NEXT-2: integral-weight SSSP over distance buckets (bucket width 1), "
-                        "same graph and weights as the Bellman-Ford leg",
+                        "same graph and weights as the Bellman-Ford leg; one gbbs_wbfs_batch call "
+                        "per step (teams of traversals per launch)",
                 "rounds": [per_src[("wbfs", s)]["rounds"] for s in sources]}
         if "wp" in algos and args.algo == "bfs":
             wt, wclk, wkms = res["wp"]

@@ -241,6 +241,18 @@ int gbbs_wbfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
 int gbbs_bellman_ford_signed(const gbbs_graph *g, uint32_t src, int64_t *dist,
                              void *cuda_stream);
 
+/*
+ * gbbs_wbfs_batch — k wBFS traversals (sources srcs[0..k), host array) into
+ * device rows dist[i*n .. (i+1)*n); same results as k gbbs_wbfs calls.  The
+ * traversals run concurrently, `teams` per cooperative launch (gbbs_opts.teams
+ * in gbbs_wbfs_batch_ex; default 8 on graphs with n <= 2^24 and m <= 2^28,
+ * else 1), each team with its own bucket ring and
+ * scratch allocated on first use.  Errors as gbbs_wbfs, plus GBBS_EINVAL for
+ * host rows.
+ */
+int gbbs_wbfs_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                    uint32_t *dist, void *cuda_stream);
+
 /* ---- extended calls (bench / tests) ------------------------------------ */
 
 /* Representation choice per round (threshold rule reading A10).
@@ -342,8 +354,10 @@ int gbbs_betweenness_ex(const gbbs_graph *g, uint32_t src, double *delta,
 int gbbs_bellman_ford_signed_ex(const gbbs_graph *g, uint32_t src, int64_t *dist,
                                 void *cuda_stream, const gbbs_opts *opts,
                                 gbbs_stats *stats);
-/* Batch calls with options (threshold T, modes 0-2; NULL = defaults;
- * ctas_per_sm must be 0). */
+/* Batch calls with options (threshold T, modes 0-2, bsize, teams, wBFS delta;
+ * NULL = defaults; ctas_per_sm must be 0). */
+int gbbs_wbfs_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                       uint32_t *dist, void *cuda_stream, const gbbs_opts *opts);
 int gbbs_bfs_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
                       uint32_t *dist, uint32_t *parent, void *cuda_stream,
                       const gbbs_opts *opts);

@@ -83,6 +83,7 @@ struct gbbs_graph {
   struct TeamScratch *team[8] = {};  // batch teams 1..7
   unsigned *bar0 = nullptr;          // team 0's barrier words
   int mg_grid[3] = {0, 0, 0};        // co-resident CTAs of traverse_mg_kernel<ALGO>
+  int wb_mg_grid = 0;                // co-resident CTAs of wbfs_mg_kernel
   RoundStat *dstats = nullptr;
   long long dstats_cap = 0;
   unsigned long long *dcount = nullptr;
@@ -660,6 +661,13 @@ struct TeamScratch {
   unsigned long long *cnt = nullptr;  // same layout as the handle's (18 words)
   uint16_t *shadow = nullptr;
   unsigned *bar = nullptr;
+  // wBFS bucket structure of this team (hv is shared with team 0's)
+  uint32_t *bq = nullptr;
+  unsigned long long *wctr = nullptr;
+  uint32_t *xq[3] = {nullptr, nullptr, nullptr};
+  uint32_t *tag = nullptr;
+  int nbq = 0;
+  unsigned long long qcap = 0;
 };
 
 static void free_teams(gbbs_graph *g) {
@@ -675,6 +683,10 @@ static void free_teams(gbbs_graph *g) {
     cudaFree(x->cnt);
     cudaFree(x->shadow);
     cudaFree(x->bar);
+    cudaFree(x->bq);
+    cudaFree(x->wctr);
+    for (int i = 0; i < 3; i++) cudaFree(x->xq[i]);
+    cudaFree(x->tag);
     delete x;
     g->team[t] = nullptr;
   }
@@ -1206,6 +1218,122 @@ extern "C" int gbbs_bellman_ford_signed_ex(const gbbs_graph *cg_, uint32_t src, 
 extern "C" int gbbs_bellman_ford_signed(const gbbs_graph *g, uint32_t src, int64_t *dist,
                                         void *cuda_stream) {
   return gbbs_bellman_ford_signed_ex(g, src, dist, cuda_stream, nullptr, nullptr);
+}
+
+// Batch of wBFS traversals into device rows, G per launch (teams of
+// wbfs_mg_kernel, each with its own bucket ring and scratch).
+static int run_wbfs_batch(const gbbs_graph *cg_, const uint32_t *srcs, int64_t k, uint32_t *dist,
+                          void *stream, const gbbs_opts *opts) {
+  g_last_error.clear();
+  if (!cg_) return fail(GBBS_EINVAL, "g is NULL");
+  gbbs_graph *g = const_cast<gbbs_graph *>(cg_);
+  if (k < 0 || (k > 0 && (!srcs || !dist))) return fail(GBBS_EINVAL, "bad batch arguments");
+  for (int64_t i = 0; i < k; i++)
+    if ((long long)srcs[i] >= g->n) return fail(GBBS_EINVAL, "srcs[%lld] = %u >= n %lld",
+                                                 (long long)i, srcs[i], g->n);
+  if (k == 0) return GBBS_OK;
+  if (!is_device_ptr(dist)) return fail(GBBS_EINVAL, "gbbs_wbfs_batch writes device rows");
+  gbbs_opts o;
+  if (int rc0 = parse_opts(opts, OPTS_BATCH, o)) return rc0;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  if (dev != g->device) CU(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t n = (size_t)g->n;
+  // teams: default 8 on graphs with n <= 2^24 and m <= 2^28, else 1 — measured
+  // (tools/teams_probe.py): c2 21.3 / 15.1 / 14.6 ms with 1 / 4 / 8 teams for its 8
+  // sources, c4 flat (62-64 ms)
+  const int G = (int)(o.teams ? o.teams
+                              : ((g->n <= (1ll << 24) && g->m <= (1ll << 28)) ? 8 : 1));
+  if (g->bstat_cap < k) {
+    cudaFree(g->bstat);
+    g->bstat = nullptr;
+    g->bstat_cap = 0;
+    CU(cudaMalloc(&g->bstat, (size_t)k * 16));
+    g->bstat_cap = k;
+  }
+  for (int t = 0; t < G; t++)
+    if (int rc = team_scratch(g, t)) return rc;
+  if (!g->wb_mg_grid) {
+    int nsm = 0, per = 0;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    CU(cudaFuncSetAttribute(wbfs_mg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)WBFS_DYN_SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, wbfs_mg_kernel, BLOCK, WBFS_DYN_SMEM));
+    if (per < 1) return fail(GBBS_ECUDA, "multi-traversal wbfs kernel cannot be resident");
+    g->wb_mg_grid = per * nsm;
+  }
+  for (int64_t i0 = 0; i0 < k; i0 += G) {
+    MultiParams mp;
+    memset(&mp, 0, sizeof mp);
+    mp.G = (int)((k - i0) < G ? (k - i0) : G);
+    for (int t = 0; t < mp.G; t++) {
+      Params &p = mp.ps[t];
+      fill_params_team(g, ALGO_WBFS, srcs[i0 + t], dist + (i0 + t) * n, nullptr, o, t, p);
+      Params p0;  // team 0's bucket structure decides delta, nbq and the list capacity
+      fill_params(g, ALGO_WBFS, srcs[i0 + t], dist, nullptr, o, p0);
+      if (int rc = wbfs_setup(g, o.delta, p0)) return rc;
+      p.delta = p0.delta;
+      p.nbq = p0.nbq;
+      p.qcap = p0.qcap;
+      p.hv = p0.hv;
+      p.max_rounds = p0.max_rounds;
+      if (t == 0) {
+        p.bq = p0.bq;
+        p.btail = p0.btail;
+        p.bheavy = p0.bheavy;
+        p.xcnt = p0.xcnt;
+        p.pub = p0.pub;
+        for (int i = 0; i < 3; i++) p.xq[i] = p0.xq[i];
+        p.tag = p0.tag;
+        continue;
+      }
+      TeamScratch *x = g->team[t];
+      if (x->nbq < p0.nbq || x->qcap != p0.qcap) {
+        cudaFree(x->bq);
+        x->bq = nullptr;
+        CU(cudaMalloc(&x->bq, (size_t)p0.nbq * p0.qcap * 4));
+        x->nbq = p0.nbq;
+        x->qcap = p0.qcap;
+      }
+      if (!x->wctr) CU(cudaMalloc(&x->wctr, (64 + 64 + 6 + 3) * 8));
+      if (p0.tag && !x->tag) {
+        for (int i = 0; i < 3; i++) CU(cudaMalloc(&x->xq[i], n * 4));
+        CU(cudaMalloc(&x->tag, n * 4));
+      }
+      p.bq = x->bq;
+      p.btail = x->wctr;
+      p.bheavy = x->wctr + 64;
+      p.xcnt = x->wctr + 128;
+      p.pub = x->wctr + 134;
+      for (int i = 0; i < 3; i++) p.xq[i] = x->xq[i];
+      p.tag = p0.tag ? x->tag : nullptr;
+    }
+    void *args[] = {&mp};
+    CU(cudaLaunchCooperativeKernel((const void *)wbfs_mg_kernel, g->wb_mg_grid, BLOCK, args,
+                                   WBFS_DYN_SMEM, st));
+    for (int t = 0; t < mp.G; t++)
+      CU(cudaMemcpyAsync(g->bstat + 2 * (i0 + t), mp.ps[t].status, 16, cudaMemcpyDeviceToDevice,
+                         st));
+  }
+  std::vector<long long> hs((size_t)k * 2);
+  CU(cudaMemcpyAsync(hs.data(), g->bstat, (size_t)k * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < k; i++) {
+    const int rc = status_error(g, (int)(hs[2 * i] & 0xFFFFFFFF), -1);
+    if (rc) return rc;
+  }
+  return GBBS_OK;
+}
+
+extern "C" int gbbs_wbfs_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                               uint32_t *dist, void *cuda_stream) {
+  return run_wbfs_batch(g, srcs, k, dist, cuda_stream, nullptr);
+}
+
+extern "C" int gbbs_wbfs_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                                  uint32_t *dist, void *cuda_stream, const gbbs_opts *opts) {
+  return run_wbfs_batch(g, srcs, k, dist, cuda_stream, opts);
 }
 
 extern "C" int gbbs_wbfs(const gbbs_graph *g, uint32_t src, uint32_t *dist, void *cuda_stream) {

@@ -1701,16 +1701,24 @@ __global__ void __launch_bounds__(BLOCK, GBBS_MIN_CTAS)
 #ifndef GBBS_WBFS_MIN_CTAS
 #define GBBS_WBFS_MIN_CTAS 3
 #endif
-template <bool STATS>
-__global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params p) {
+template <bool STATS, bool MG>
+__device__ __forceinline__ void wbfs_body(const Params &p, int G) {
   __shared__ Smem s;
   __shared__ unsigned long long s_head[64], s_hhead[64], s_ctl[3 + 2 * 64];
   cg::grid_group grid = cg::this_grid();
+  long long bid_ = 0, nblk_ = 0;  // MG: team-local index and size (as traverse_body)
+  if constexpr (MG) {
+    const int g = (int)(blockIdx.x % G);
+    bid_ = blockIdx.x / G;
+    nblk_ = ((long long)gridDim.x - g + G - 1) / G;
+  }
+#define GBBS_BID (MG ? bid_ : (long long)blockIdx.x)
+#define GBBS_NBLK (MG ? nblk_ : (long long)gridDim.x)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long gtid = (long long)blockIdx.x * BLOCK + tid;
-  const long long gstride = (long long)gridDim.x * BLOCK;
-  const long long gw = (long long)blockIdx.x * NWARPS + warp;
-  const long long nw = (long long)gridDim.x * NWARPS;
+  const long long gtid = GBBS_BID * BLOCK + tid;
+  const long long gstride = GBBS_NBLK * BLOCK;
+  const long long gw = GBBS_BID * NWARPS + warp;
+  const long long nw = GBBS_NBLK * NWARPS;
   const uint32_t src = p.src;
   const int nbq = p.nbq;
   const unsigned long long qmask = p.qcap - 1;
@@ -1722,7 +1730,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
     p.shadow[i] = (i == src) ? 0u : 0xFFFFu;
     if (p.tag) p.tag[i] = 0;
   }
-  if (blockIdx.x == 0 && tid == 0) {
+  if (GBBS_BID == 0 && tid == 0) {
     for (int q = 0; q < nbq; q++) p.btail[q] = p.bheavy[q] = 0;
     for (int q = 0; q < 6; q++) p.xcnt[q] = 0;
     for (int q = 0; q < 3; q++) p.pub[q] = 0;
@@ -1740,7 +1748,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
     w.hist[lane] = w.hist[lane + 32] = 0;
     if (lane == 0) w.hist[XKEY] = 0;
   }
-  grid.sync();
+  team_sync<MG>(grid, p.bar, GBBS_NBLK);
 
   unsigned long long pend = 1;  // lists with pending entries: bucket 0's
   unsigned long long k = 0;     // bucket being processed
@@ -1785,12 +1793,12 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
       t = s_ctl[3 + slot];
       heavy_any = s_ctl[3 + 64 + slot] > s_hhead[slot];
       if (t - h > p.qcap) {  // entries were overwritten: the list overflowed
-        if (blockIdx.x == 0 && tid == 0) *p.status = 4;
+        if (GBBS_BID == 0 && tid == 0) *p.status = 4;
         break;
       }
     }
     if (r >= p.max_rounds) {
-      if (blockIdx.x == 0 && tid == 0) *p.status = 1;
+      if (GBBS_BID == 0 && tid == 0) *p.status = 1;
       break;
     }
     __syncthreads();
@@ -1798,7 +1806,7 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
       s_head[slot] = t;
       s_hhead[slot] = s_ctl[3 + 64 + slot];
     }
-    if (blockIdx.x == 0 && tid == 0) {
+    if (GBBS_BID == 0 && tid == 0) {
       const int nr = (int)((r + 1) % 3);  // idle this round; appended to next round
       p.xcnt[nr] = p.xcnt[3 + nr] = 0;
       p.pub[nr] = 0;
@@ -1853,19 +1861,19 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
         warp_flush<ALGO_WBFS>(p, wsm.stage, ws.scnt, 0, (int)r, nullptr, nullptr, p.cnt + xr);
         ws.scnt = 0;
       }
-      grid.sync();
+      team_sync<MG>(grid, p.bar, GBBS_NBLK);
       if (tid == 0) s.cnt = ld_relaxed64(p.cnt + xr);
       __syncthreads();
       const unsigned long long c = s.cnt;
       const long long f = (long long)(c >> p.ebits);
       const long long E = (long long)(c & ((1ull << p.ebits) - 1));
-      if (STATS && p.stats && r < p.stats_cap && blockIdx.x == 0 && tid == 0)
+      if (STATS && p.stats && r < p.stats_cap && GBBS_BID == 0 && tid == 0)
         p.stats[r].frontier_edges = E;
       if (f > 0)
         list_round<ALGO_WBFS, STATS, EMIT_LIST>(p, wsm, ws, 0, f, E, 0, (int)r, nullptr, nullptr,
                                                 gw, nw, p.wq + (r & 3));
     } else if (heavy_any) {  // hubs of this bucket, spread over all warps in list tiles
-      grid.sync();
+      team_sync<MG>(grid, p.bar, GBBS_NBLK);
       if (tid == 0) s.hcnt = ld_relaxed64(p.hcnt + (r & 1));
       __syncthreads();
       const unsigned long long hc = s.hcnt;
@@ -1896,11 +1904,25 @@ __global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS) wbfs_kernel(Params 
         atomicMax((unsigned long long *)&p.stats[r].t_flush_ns, t_flush);
       }
     }
-    grid.sync();
+    team_sync<MG>(grid, p.bar, GBBS_NBLK);
   }
-  if (STATS && blockIdx.x == 0 && tid == 0 && p.stats && r < p.stats_cap)
+  if (STATS && GBBS_BID == 0 && tid == 0 && p.stats && r < p.stats_cap)
     p.stats[r].t_start_ns = (long long)globaltimer_ns();
-  if (blockIdx.x == 0 && tid == 0) *p.rounds_out = r;
+  if (GBBS_BID == 0 && tid == 0) *p.rounds_out = r;
+}
+#undef GBBS_BID
+#undef GBBS_NBLK
+
+template <bool STATS>
+__global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS)
+    wbfs_kernel(const __grid_constant__ Params p) {
+  wbfs_body<STATS, false>(p, 1);
+}
+
+// G wBFS traversals in one cooperative launch (teams, as traverse_mg_kernel).
+__global__ void __launch_bounds__(BLOCK, GBBS_WBFS_MIN_CTAS)
+    wbfs_mg_kernel(const __grid_constant__ MultiParams mp) {
+  wbfs_body<false, true>(mp.ps[blockIdx.x % mp.G], mp.G);
 }
 
 }  // namespace gbbs_dev

@@ -28,7 +28,8 @@ EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_b
            "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
            "gbbs_widest_path_ex", "gbbs_wbfs", "gbbs_wbfs_ex", "gbbs_bellman_ford_signed",
            "gbbs_bellman_ford_signed_ex", "gbbs_bfs_batch", "gbbs_bellman_ford_batch",
-           "gbbs_bfs_batch_ex", "gbbs_bellman_ford_batch_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
+           "gbbs_bfs_batch_ex", "gbbs_bellman_ford_batch_ex", "gbbs_wbfs_batch",
+           "gbbs_wbfs_batch_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
            "gbbs_launch_info", "gbbs_last_error")
 
 
@@ -77,6 +78,8 @@ def _load():
     lib.gbbs_bfs_batch.argtypes = [p, p, i64, p, p, p]
     lib.gbbs_bellman_ford_batch.argtypes = [p, p, i64, p, p]
     lib.gbbs_bfs_batch_ex.argtypes = [p, p, i64, p, p, p, ctypes.POINTER(gbbs_opts)]
+    lib.gbbs_wbfs_batch.argtypes = [p, p, i64, p, p]
+    lib.gbbs_wbfs_batch_ex.argtypes = [p, p, i64, p, p, ctypes.POINTER(gbbs_opts)]
     lib.gbbs_bellman_ford_batch_ex.argtypes = [p, p, i64, p, p, ctypes.POINTER(gbbs_opts)]
     lib.gbbs_bellman_ford_signed.argtypes = [p, u32, p, p]
     lib.gbbs_bellman_ford_signed_ex.argtypes = [p, u32, p, p, ctypes.POINTER(gbbs_opts),
@@ -94,7 +97,7 @@ def _load():
               "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_wbfs",
               "gbbs_wbfs_ex", "gbbs_bellman_ford_signed", "gbbs_bellman_ford_signed_ex", "gbbs_bfs_batch",
               "gbbs_bellman_ford_batch", "gbbs_bfs_batch_ex", "gbbs_bellman_ford_batch_ex",
-              "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
+              "gbbs_wbfs_batch", "gbbs_wbfs_batch_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -225,6 +228,17 @@ def gbbs_bellman_ford_batch(handle, srcs, dist, stream=None, opts=None):
                                               st, ctypes.byref(opts)))
 
 
+def gbbs_wbfs_batch(handle, srcs, dist, stream=None, opts=None):
+    """dist: (k, n) device rows."""
+    s = np.ascontiguousarray(srcs, dtype=np.uint32)
+    st = _stream(stream, dist)
+    if opts is None:
+        _check(lib.gbbs_wbfs_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), st))
+    else:
+        _check(lib.gbbs_wbfs_batch_ex(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), st,
+                                      ctypes.byref(opts)))
+
+
 def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
     st = _stream(stream, delta)
     if stats is None:
@@ -327,6 +341,9 @@ class Graph:
 
     def bellman_ford_batch(self, srcs, dist, stream=None, opts=None):
         gbbs_bellman_ford_batch(self.handle, srcs, dist, stream, opts)
+
+    def wbfs_batch(self, srcs, dist, stream=None, opts=None):
+        gbbs_wbfs_batch(self.handle, srcs, dist, stream, opts)
 
     def bellman_ford_signed(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_bellman_ford_signed(self.handle, src, dist, stream, opts, stats)

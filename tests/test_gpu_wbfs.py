@@ -218,3 +218,23 @@ def test_errors(G):
         g.wbfs(0, d)
     assert e.value.code == -2
     g.close()
+
+
+@pytest.mark.parametrize("teams", [1, 2, 3, 5])
+def test_wbfs_batch_teams(G, teams):
+    """gbbs_wbfs_batch: teams of wBFS traversals per launch, each with its own bucket
+    ring; rows equal the oracle's Dijkstra (also with delta = 4, i.e. near lists)."""
+    off, tgt = graphgen.rmat_graph(16, 1 << 20, 44, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 3, 16)
+    g = G.Graph(off, tgt, w, symmetric=True)
+    srcs = graphgen.choose_sources(np.nonzero(np.diff(off) > 0)[0], 7, 17)
+    refs = [oracle.dijkstra(off, tgt, w, s)[0] for s in srcs]
+    for delta in (0, 4):
+        d = torch.empty((len(srcs), g.n), dtype=torch.int32, device="cuda")
+        g.wbfs_batch(srcs, d, opts=G.make_opts(teams=teams, delta=delta))
+        d = d.cpu().numpy().view(np.uint32)
+        for i in range(len(srcs)):
+            assert (d[i] == refs[i]).all(), (teams, delta, i)
+    with pytest.raises(G.GbbsError):
+        g.wbfs_batch(srcs, np.empty((len(srcs), g.n), np.uint32))   # host rows
+    g.close()

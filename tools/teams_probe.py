@@ -21,7 +21,8 @@ def main():
         dd = torch.empty((len(srcs), n), dtype=torch.int32, device="cuda")
         pp = torch.empty_like(dd)
         flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-        algos = ("bfs", "bf") if G["weights"] is not None else ("bfs",)
+        algos = tuple(os.environ.get("ALGOS", "bfs,bf,wbfs").split(",")) if G["weights"] is not None \
+            else ("bfs",)
         for algo in algos:
             base = None
             for teams in [int(x) for x in os.environ.get("TEAMS", "1,2,3,4").split(",")]:
@@ -33,6 +34,8 @@ def main():
                     e0.record()
                     if algo == "bfs":
                         g.bfs_batch(srcs, dd, pp, opts=opts)
+                    elif algo == "wbfs":
+                        g.wbfs_batch(srcs, dd, opts=opts)
                     else:
                         g.bellman_ford_batch(srcs, dd, opts=opts)
                     e1.record()
