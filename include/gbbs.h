@@ -253,6 +253,18 @@ int gbbs_bellman_ford_signed(const gbbs_graph *g, uint32_t src, int64_t *dist,
 int gbbs_wbfs_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
                     uint32_t *dist, void *cuda_stream);
 
+/*
+ * gbbs_betweenness_batch — k single-source betweenness computations (sources
+ * srcs[0..k), host array) into device rows delta[i*n .. (i+1)*n) (double),
+ * the same values as k gbbs_betweenness calls up to fp64 summation order.  The
+ * traversals run concurrently, teams per cooperative launch (gbbs_opts.teams
+ * in the _ex form; default 1: measured slower with teams, its levels are
+ * throughput-bound).
+ * Errors as gbbs_betweenness, plus GBBS_EINVAL for host rows.
+ */
+int gbbs_betweenness_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                           double *delta, void *cuda_stream);
+
 /* ---- extended calls (bench / tests) ------------------------------------ */
 
 /* Representation choice per round (threshold rule reading A10).
@@ -358,6 +370,9 @@ int gbbs_bellman_ford_signed_ex(const gbbs_graph *g, uint32_t src, int64_t *dist
  * NULL = defaults; ctas_per_sm must be 0). */
 int gbbs_wbfs_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
                        uint32_t *dist, void *cuda_stream, const gbbs_opts *opts);
+int gbbs_betweenness_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                              double *delta, void *cuda_stream,
+                              const gbbs_opts *opts);
 int gbbs_bfs_batch_ex(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
                       uint32_t *dist, uint32_t *parent, void *cuda_stream,
                       const gbbs_opts *opts);

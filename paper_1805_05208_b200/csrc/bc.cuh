@@ -53,6 +53,7 @@ struct BcParams {
   long long lvl_cap;
   unsigned long long *cnt;   // packed (count << ebits | edges) ring [4]
   unsigned long long *wq;    // [8] tile work-queue counters: forward ring [4], backward ring [4]
+  unsigned *bar;             // team barrier words (multi-traversal launches)
   int *status;
   long long *rounds_out;
   int ebits;
@@ -312,14 +313,23 @@ __device__ __forceinline__ void bc_level(const BcParams &p, BcWarpSmem &w, int &
   for (; t < t1; t++) i0 = bc_tile<BACK>(p, w, scnt, F, O, B, f, E, i0, t, l, qnext, ctr);
 }
 
-__global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
+template <bool MG>
+__device__ __forceinline__ void bc_body(const BcParams &p, int G) {
   __shared__ BcSmem s;
   cg::grid_group grid = cg::this_grid();
+  long long bid_ = 0, nblk_ = 0;  // MG: team-local index and size (as traverse_body)
+  if constexpr (MG) {
+    const int g = (int)(blockIdx.x % G);
+    bid_ = blockIdx.x / G;
+    nblk_ = ((long long)gridDim.x - g + G - 1) / G;
+  }
+#define GBBS_BID (MG ? bid_ : (long long)blockIdx.x)
+#define GBBS_NBLK (MG ? nblk_ : (long long)gridDim.x)
   const int tid = threadIdx.x, warp = tid >> 5;
-  const long long gtid = (long long)blockIdx.x * BLOCK + tid;
-  const long long gstride = (long long)gridDim.x * BLOCK;
-  const long long gw = (long long)blockIdx.x * NWARPS + warp;
-  const long long nw = (long long)gridDim.x * NWARPS;
+  const long long gtid = GBBS_BID * BLOCK + tid;
+  const long long gstride = GBBS_NBLK * BLOCK;
+  const long long gw = GBBS_BID * NWARPS + warp;
+  const long long nw = GBBS_NBLK * NWARPS;
   const uint32_t src = p.src;
   BcWarpSmem &w = s.w[warp];
 
@@ -328,7 +338,7 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
     p.sigma[i] = (i == src) ? 1.0 : 0.0;
     p.delta[i] = 0.0;
   }
-  if (blockIdx.x == 0 && tid == 0) {
+  if (GBBS_BID == 0 && tid == 0) {
     const long long a = p.off[src], d0 = p.off[src + 1] - a;
     p.cnt[1] = p.cnt[2] = p.cnt[3] = 0;
     if (d0 > 0) {
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
     *p.status = 0;
     for (int q = 0; q < 8; q++) p.wq[q] = 0;
   }
-  grid.sync();
+  team_sync<MG>(grid, p.bar, GBBS_NBLK);
 
   const unsigned long long emask = (1ull << p.ebits) - 1;
   long long start = 0;  // queue position of the current level
@@ -353,10 +363,10 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
     const long long f = (long long)(s.cnt >> p.ebits), E = (long long)(s.cnt & emask);
     if (f == 0) break;
     if (l >= p.lvl_cap) {
-      if (blockIdx.x == 0 && tid == 0) *p.status = 1;
+      if (GBBS_BID == 0 && tid == 0) *p.status = 1;
       break;
     }
-    if (blockIdx.x == 0 && tid == 0) {
+    if (GBBS_BID == 0 && tid == 0) {
       p.cnt[(l + 2) & 3] = 0;
       p.wq[(l + 2) & 3] = 0;
       p.lvl[3 * l] = start;
@@ -368,23 +378,39 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(BcParams p) {
                     p.wq + (l & 3));
     if (scnt > 0) bc_flush(p, w.stage, scnt, start + f, p.cnt + ((l + 1) & 3));
     start += f;
-    grid.sync();
+    team_sync<MG>(grid, p.bar, GBBS_NBLK);
   }
   const int L = l;  // levels with a non-empty list: 0 .. L-1
 #ifdef GBBS_DIAG_BC_FORWARD_ONLY  // measurement-only build
   if (L > 0) {
-    if (blockIdx.x == 0 && tid == 0) *p.rounds_out = L;
+    if (GBBS_BID == 0 && tid == 0) *p.rounds_out = L;
     return;
   }
 #endif
   for (int b = L - 1; b >= 1; b--) {
     const long long st0 = p.lvl[3 * b], f = p.lvl[3 * b + 1], E = p.lvl[3 * b + 2];
     int scnt = 0;
-    if (blockIdx.x == 0 && tid == 0) p.wq[4 + ((b - 2) & 3)] = 0;  // used two levels down
+    if (GBBS_BID == 0 && tid == 0) p.wq[4 + ((b - 2) & 3)] = 0;  // used two levels down
     bc_level<true>(p, w, scnt, st0, f, E, b, 0, nullptr, gw, nw, p.wq + 4 + (b & 3));
-    grid.sync();
+    team_sync<MG>(grid, p.bar, GBBS_NBLK);
   }
-  if (blockIdx.x == 0 && tid == 0) *p.rounds_out = L;
+  if (GBBS_BID == 0 && tid == 0) *p.rounds_out = L;
+}
+#undef GBBS_BID
+#undef GBBS_NBLK
+
+__global__ void __launch_bounds__(BLOCK) bc_kernel(const __grid_constant__ BcParams p) {
+  bc_body<false>(p, 1);
+}
+
+// G betweenness traversals in one cooperative launch (teams, as traverse_mg_kernel).
+constexpr int BC_GMAX = 8;
+struct MultiBcParams {
+  BcParams ps[BC_GMAX];
+  int G;
+};
+__global__ void __launch_bounds__(BLOCK) bc_mg_kernel(const __grid_constant__ MultiBcParams mp) {
+  bc_body<true>(mp.ps[blockIdx.x % mp.G], mp.G);
 }
 
 }  // namespace gbbs_dev

@@ -84,6 +84,7 @@ struct gbbs_graph {
   unsigned *bar0 = nullptr;          // team 0's barrier words
   int mg_grid[3] = {0, 0, 0};        // co-resident CTAs of traverse_mg_kernel<ALGO>
   int wb_mg_grid = 0;                // co-resident CTAs of wbfs_mg_kernel
+  int bc_mg_grid = 0;                // co-resident CTAs of bc_mg_kernel
   RoundStat *dstats = nullptr;
   long long dstats_cap = 0;
   unsigned long long *dcount = nullptr;
@@ -668,6 +669,10 @@ struct TeamScratch {
   uint32_t *tag = nullptr;
   int nbq = 0;
   unsigned long long qcap = 0;
+  // betweenness state of this team
+  uint32_t *bc_dist = nullptr;
+  double *bc_sigma = nullptr;
+  long long *bc_lvl = nullptr;
 };
 
 static void free_teams(gbbs_graph *g) {
@@ -687,6 +692,9 @@ static void free_teams(gbbs_graph *g) {
     cudaFree(x->wctr);
     for (int i = 0; i < 3; i++) cudaFree(x->xq[i]);
     cudaFree(x->tag);
+    cudaFree(x->bc_dist);
+    cudaFree(x->bc_sigma);
+    cudaFree(x->bc_lvl);
     delete x;
     g->team[t] = nullptr;
   }
@@ -1309,9 +1317,15 @@ static int run_wbfs_batch(const gbbs_graph *cg_, const uint32_t *srcs, int64_t k
       for (int i = 0; i < 3; i++) p.xq[i] = x->xq[i];
       p.tag = p0.tag ? x->tag : nullptr;
     }
-    void *args[] = {&mp};
-    CU(cudaLaunchCooperativeKernel((const void *)wbfs_mg_kernel, g->wb_mg_grid, BLOCK, args,
-                                   WBFS_DYN_SMEM, st));
+    if (mp.G == 1) {  // the plain kernel
+      void *a1[] = {&mp.ps[0]};
+      CU(cudaLaunchCooperativeKernel((const void *)wbfs_kernel<false>, g->wb->grid[0], BLOCK, a1,
+                                     WBFS_DYN_SMEM, st));
+    } else {
+      void *args[] = {&mp};
+      CU(cudaLaunchCooperativeKernel((const void *)wbfs_mg_kernel, g->wb_mg_grid, BLOCK, args,
+                                     WBFS_DYN_SMEM, st));
+    }
     for (int t = 0; t < mp.G; t++)
       CU(cudaMemcpyAsync(g->bstat + 2 * (i0 + t), mp.ps[t].status, 16, cudaMemcpyDeviceToDevice,
                          st));
@@ -1358,6 +1372,13 @@ extern "C" int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *
 // NEXT-3: single-source betweenness contributions (bc.cuh)
 // ---------------------------------------------------------------------------
 #include "bc.cuh"
+
+// default teams for betweenness batches: 1 — measured (tools/teams_probe.py) c2
+// 23.8 / 24.7 / 28.0 / 32.1 ms and c4 105 / 118 / 134 / 134 ms for 1 / 2 / 4 / 8
+// teams (fp64 fetch-and-adds and random loads: throughput-bound levels)
+#ifndef BC_TEAMS_AUTO
+#define BC_TEAMS_AUTO 1
+#endif
 
 struct BcScratch {
   uint32_t *dist = nullptr;
@@ -1464,6 +1485,108 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   }
   if (ctrl.status != 0) return fail(GBBS_EINTERNAL, "more than %lld BFS levels", b->lvl_cap);
   return GBBS_OK;
+}
+
+// Batch of betweenness traversals into device rows, G per launch (teams of
+// bc_mg_kernel, each with its own level, sigma, queue and counters).
+extern "C" int gbbs_betweenness_batch_ex(const gbbs_graph *cg_, const uint32_t *srcs, int64_t k,
+                                         double *delta, void *cuda_stream,
+                                         const gbbs_opts *opts) {
+  g_last_error.clear();
+  if (!cg_) return fail(GBBS_EINVAL, "g is NULL");
+  gbbs_graph *g = const_cast<gbbs_graph *>(cg_);
+  if (k < 0 || (k > 0 && (!srcs || !delta))) return fail(GBBS_EINVAL, "bad batch arguments");
+  for (int64_t i = 0; i < k; i++)
+    if ((long long)srcs[i] >= g->n) return fail(GBBS_EINVAL, "srcs[%lld] = %u >= n %lld",
+                                                 (long long)i, srcs[i], g->n);
+  if (k == 0) return GBBS_OK;
+  if (!is_device_ptr(delta)) return fail(GBBS_EINVAL, "gbbs_betweenness_batch writes device rows");
+  gbbs_opts o;
+  if (int rc0 = parse_opts(opts, OPTS_BATCH, o)) return rc0;
+  const int G = (int)(o.teams ? o.teams
+                              : ((g->n <= (1ll << 24) && g->m <= (1ll << 28)) ? BC_TEAMS_AUTO : 1));
+  if (G > BC_GMAX) return fail(GBBS_EINVAL, "teams %d > %d", G, BC_GMAX);
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  if (dev != g->device) CU(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const size_t n = (size_t)g->n;
+  int rc = GBBS_OK;
+  BcScratch *b = bc_scratch(g, &rc);
+  if (!b) return rc;
+  for (int t = 0; t < G; t++) {
+    if ((rc = team_scratch(g, t))) return rc;
+    TeamScratch *x = t ? g->team[t] : nullptr;
+    if (x && !x->bc_dist) {
+      CU(cudaMalloc(&x->bc_dist, n * 4));
+      CU(cudaMalloc(&x->bc_sigma, n * 8));
+      CU(cudaMalloc(&x->bc_lvl, (size_t)b->lvl_cap * 24));
+    }
+  }
+  if (g->bstat_cap < k) {
+    cudaFree(g->bstat);
+    g->bstat = nullptr;
+    g->bstat_cap = 0;
+    CU(cudaMalloc(&g->bstat, (size_t)k * 16));
+    g->bstat_cap = k;
+  }
+  if (!g->bc_mg_grid) {
+    int nsm = 0, per = 0;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bc_mg_kernel, BLOCK, 0));
+    if (per < 1) return fail(GBBS_ECUDA, "multi-traversal betweenness kernel cannot be resident");
+    g->bc_mg_grid = per * nsm;
+  }
+  for (int64_t i0 = 0; i0 < k; i0 += G) {
+    MultiBcParams mp;
+    memset(&mp, 0, sizeof mp);
+    mp.G = (int)((k - i0) < G ? (k - i0) : G);
+    for (int t = 0; t < mp.G; t++) {
+      BcParams &p = mp.ps[t];
+      TeamScratch *x = t ? g->team[t] : nullptr;
+      p.n = g->n;
+      p.m = g->m;
+      p.off = g->off;
+      p.tgt = g->tgt;
+      p.dist = x ? x->bc_dist : b->dist;
+      p.sigma = x ? x->bc_sigma : b->sigma;
+      p.delta = delta + (i0 + t) * n;
+      p.qv = x ? x->fv[0] : g->fv[0];
+      p.qo = x ? x->fo[0] : g->fo[0];
+      p.qb = x ? x->fb[0] : g->fb[0];
+      p.lvl = x ? x->bc_lvl : b->lvl;
+      p.lvl_cap = b->lvl_cap;
+      p.cnt = x ? x->cnt : g->cnt;
+      p.wq = p.cnt + 10;
+      p.status = (int *)(p.cnt + 4);
+      p.rounds_out = (long long *)(p.cnt + 5);
+      p.bar = x ? x->bar : g->bar0;
+      p.ebits = g->ebits;
+      p.src = srcs[i0 + t];
+    }
+    if (mp.G == 1) {  // the plain kernel (the team form costs ~15 % at G = 1)
+      void *a1[] = {&mp.ps[0]};
+      CU(cudaLaunchCooperativeKernel((const void *)bc_kernel, b->grid, BLOCK, a1, 0, st));
+    } else {
+      void *args[] = {&mp};
+      CU(cudaLaunchCooperativeKernel((const void *)bc_mg_kernel, g->bc_mg_grid, BLOCK, args, 0,
+                                     st));
+    }
+    for (int t = 0; t < mp.G; t++)
+      CU(cudaMemcpyAsync(g->bstat + 2 * (i0 + t), mp.ps[t].status, 16, cudaMemcpyDeviceToDevice,
+                         st));
+  }
+  std::vector<long long> hs((size_t)k * 2);
+  CU(cudaMemcpyAsync(hs.data(), g->bstat, (size_t)k * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < k; i++)
+    if (hs[2 * i] & 0xFFFFFFFF) return fail(GBBS_EINTERNAL, "more than %lld BFS levels", b->lvl_cap);
+  return GBBS_OK;
+}
+
+extern "C" int gbbs_betweenness_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
+                                      double *delta, void *cuda_stream) {
+  return gbbs_betweenness_batch_ex(g, srcs, k, delta, cuda_stream, nullptr);
 }
 
 extern "C" int gbbs_betweenness(const gbbs_graph *g, uint32_t src, double *delta,

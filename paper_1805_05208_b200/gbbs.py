@@ -29,7 +29,8 @@ EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_b
            "gbbs_widest_path_ex", "gbbs_wbfs", "gbbs_wbfs_ex", "gbbs_bellman_ford_signed",
            "gbbs_bellman_ford_signed_ex", "gbbs_bfs_batch", "gbbs_bellman_ford_batch",
            "gbbs_bfs_batch_ex", "gbbs_bellman_ford_batch_ex", "gbbs_wbfs_batch",
-           "gbbs_wbfs_batch_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
+           "gbbs_wbfs_batch_ex", "gbbs_betweenness_batch", "gbbs_betweenness_batch_ex",
+           "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
            "gbbs_launch_info", "gbbs_last_error")
 
 
@@ -79,6 +80,8 @@ def _load():
     lib.gbbs_bellman_ford_batch.argtypes = [p, p, i64, p, p]
     lib.gbbs_bfs_batch_ex.argtypes = [p, p, i64, p, p, p, ctypes.POINTER(gbbs_opts)]
     lib.gbbs_wbfs_batch.argtypes = [p, p, i64, p, p]
+    lib.gbbs_betweenness_batch.argtypes = [p, p, i64, p, p]
+    lib.gbbs_betweenness_batch_ex.argtypes = [p, p, i64, p, p, ctypes.POINTER(gbbs_opts)]
     lib.gbbs_wbfs_batch_ex.argtypes = [p, p, i64, p, p, ctypes.POINTER(gbbs_opts)]
     lib.gbbs_bellman_ford_batch_ex.argtypes = [p, p, i64, p, p, ctypes.POINTER(gbbs_opts)]
     lib.gbbs_bellman_ford_signed.argtypes = [p, u32, p, p]
@@ -97,7 +100,8 @@ def _load():
               "gbbs_bellman_ford_ex", "gbbs_widest_path", "gbbs_widest_path_ex", "gbbs_wbfs",
               "gbbs_wbfs_ex", "gbbs_bellman_ford_signed", "gbbs_bellman_ford_signed_ex", "gbbs_bfs_batch",
               "gbbs_bellman_ford_batch", "gbbs_bfs_batch_ex", "gbbs_bellman_ford_batch_ex",
-              "gbbs_wbfs_batch", "gbbs_wbfs_batch_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
+              "gbbs_wbfs_batch", "gbbs_wbfs_batch_ex", "gbbs_betweenness_batch",
+              "gbbs_betweenness_batch_ex", "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_launch_info"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -239,6 +243,17 @@ def gbbs_wbfs_batch(handle, srcs, dist, stream=None, opts=None):
                                       ctypes.byref(opts)))
 
 
+def gbbs_betweenness_batch(handle, srcs, delta, stream=None, opts=None):
+    """delta: (k, n) float64 device rows."""
+    s = np.ascontiguousarray(srcs, dtype=np.uint32)
+    st = _stream(stream, delta)
+    if opts is None:
+        _check(lib.gbbs_betweenness_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(delta), st))
+    else:
+        _check(lib.gbbs_betweenness_batch_ex(handle, s.ctypes.data, int(s.shape[0]), _ptr(delta),
+                                             st, ctypes.byref(opts)))
+
+
 def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
     st = _stream(stream, delta)
     if stats is None:
@@ -344,6 +359,9 @@ class Graph:
 
     def wbfs_batch(self, srcs, dist, stream=None, opts=None):
         gbbs_wbfs_batch(self.handle, srcs, dist, stream, opts)
+
+    def betweenness_batch(self, srcs, delta, stream=None, opts=None):
+        gbbs_betweenness_batch(self.handle, srcs, delta, stream, opts)
 
     def bellman_ford_signed(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_bellman_ford_signed(self.handle, src, dist, stream, opts, stats)

@@ -561,3 +561,20 @@ def test_batch_teams(G, teams):
         assert (dd[i] == oracle.bfs(doff, dtgt, s)[0]).all()
         assert oracle.check_bfs(doff, dtgt, s, dd[i], pp[i])[0]
     g.close()
+
+
+@pytest.mark.parametrize("teams", [1, 3, 8])
+def test_betweenness_batch_teams(G, teams):
+    """gbbs_betweenness_batch: teams of Brandes traversals per launch; every row
+    matches the oracle within the fp64 tolerance (reading B2)."""
+    off, tgt = graphgen.rmat_graph(15, 1 << 19, 55, 0.57, 0.19, 0.19)
+    g = G.Graph(off, tgt, symmetric=True)
+    srcs = graphgen.choose_sources(np.nonzero(np.diff(off) > 0)[0], 5, 23)
+    d = torch.empty((len(srcs), g.n), dtype=torch.float64, device="cuda")
+    g.betweenness_batch(srcs, d, opts=G.make_opts(teams=teams))
+    d = d.cpu().numpy()
+    for i, s in enumerate(srcs):
+        assert_bc_close(d[i], oracle.betweenness(off, tgt, s)[0])
+    with pytest.raises(G.GbbsError):
+        g.betweenness_batch(srcs, np.empty((len(srcs), g.n), np.float64))
+    g.close()

@@ -19,6 +19,7 @@ def main():
         srcs = G["sources"]
         n = G["n"]
         dd = torch.empty((len(srcs), n), dtype=torch.int32, device="cuda")
+        db = torch.empty((len(srcs), n), dtype=torch.float64, device="cuda")
         pp = torch.empty_like(dd)
         flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
         algos = tuple(os.environ.get("ALGOS", "bfs,bf,wbfs").split(",")) if G["weights"] is not None \
@@ -36,16 +37,18 @@ def main():
                         g.bfs_batch(srcs, dd, pp, opts=opts)
                     elif algo == "wbfs":
                         g.wbfs_batch(srcs, dd, opts=opts)
+                    elif algo == "bc":
+                        g.betweenness_batch(srcs, db, opts=opts)
                     else:
                         g.bellman_ford_batch(srcs, dd, opts=opts)
                     e1.record()
                     torch.cuda.synchronize()
                     if rep:
                         ts.append(e0.elapsed_time(e1))
-                out = dd.cpu().numpy()
+                out = (db if algo == "bc" else dd).cpu().numpy()
                 if base is None:
                     base = out
-                same = bool((out == base).all())
+                same = bool(np.allclose(out, base, rtol=1e-9)) if algo == "bc" else bool((out == base).all())
                 print(f"{name} {algo} teams={teams} step_ms={np.median(ts):.3f} rows_equal={same}",
                       flush=True)
         g.close()
