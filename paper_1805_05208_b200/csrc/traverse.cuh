@@ -1033,6 +1033,9 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #ifndef GBBS_PULL_DYNQ
 #define GBBS_PULL_DYNQ 1
 #endif
+#ifndef GBBS_PULL_SPEC_ODEG
+#define GBBS_PULL_SPEC_ODEG 1
+#endif
 #ifndef GBBS_LIST_DYNQ
 #define GBBS_LIST_DYNQ 1
 #endif
@@ -1095,7 +1098,11 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
         js[q] = ld_stream64(p.in_off + v[q]);
         rem[q] = (int)(ld_stream64(p.in_off + v[q] + 1) - js[q]);
       }
+      // the out-degree an acquired vertex adds to the next round's edge count:
+      // symmetric = in-degree; directed: loaded now, beside in_off, for every
+      // candidate (consecutive ids: coalesced) instead of a random load on acquire
       deg_in[q] = rem[q];
+      if (GBBS_PULL_SPEC_ODEG && !p.symmetric) deg_in[q] = (i < cnt) ? (int)__ldg(p.odeg + v[q]) : 0;
     }
     for (int step = 0; step < PULL_STEPS; step++) {
       uint4 g[PCH];
@@ -1214,7 +1221,8 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
         st_stream(p.dist + vq, (uint32_t)(r + 1));
         if (p.parent) st_stream(p.parent + vq, par[q]);
         atomicOr(&w.found[(vq >> 5) - (uint32_t)w0], 1u << (vq & 31));
-        const uint32_t dgo = p.symmetric ? (uint32_t)deg_in[q] : __ldg(p.odeg + vq);
+        const uint32_t dgo = (p.symmetric || GBBS_PULL_SPEC_ODEG) ? (uint32_t)deg_in[q]
+                                                                   : __ldg(p.odeg + vq);
         if (dgo > 0) {
           ws.K += 1;
           ws.D += dgo;
