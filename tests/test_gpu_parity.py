@@ -578,3 +578,35 @@ def test_betweenness_batch_teams(G, teams):
     with pytest.raises(G.GbbsError):
         g.betweenness_batch(srcs, np.empty((len(srcs), g.n), np.float64))
     g.close()
+
+
+def test_no_device_memory_leak_across_handles(G):
+    """Handles that used every scratch kind (teams, wBFS rings, betweenness, signed
+    BF staging, host-output batches) free it all on destroy: device memory in use
+    returns to its level after repeated create / run / destroy cycles."""
+    off, tgt = graphgen.rmat_graph(14, 1 << 17, 61, 0.57, 0.19, 0.19)
+    w = graphgen.pair_weights(off, tgt, 1, 14)
+    srcs = [0, 1, 2, 3, 4]
+
+    def cycle():
+        g = G.Graph(off, tgt, w, symmetric=True)
+        n = g.n
+        d = torch.empty((len(srcs), n), dtype=torch.int32, device="cuda")
+        g.bfs_batch(srcs, d, torch.empty_like(d), opts=G.make_opts(teams=5))
+        g.bellman_ford_batch(srcs, d)
+        g.wbfs_batch(srcs, d, opts=G.make_opts(teams=3))
+        g.betweenness_batch(srcs, torch.empty((len(srcs), n), dtype=torch.float64, device="cuda"),
+                            opts=G.make_opts(teams=2))
+        g.bellman_ford_signed(0, np.empty(n, np.int64))
+        g.bfs_batch(srcs, np.empty((len(srcs), n), np.uint32), np.empty((len(srcs), n), np.uint32))
+        g.close()
+        del d
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+    cycle()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(3):
+        cycle()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < (16 << 20), (free0, free1)
