@@ -203,14 +203,19 @@ int gbbs_betweenness(const gbbs_graph *g, uint32_t src, double *delta,
  * increasing order, each bucket one edgeMap round with the priority-write min
  * (PAPER.md:1826-1831), vertices whose distance dropped moved to their new
  * bucket.  With the default bucket width 1 and weights >= 1 every reached
- * vertex is expanded exactly once (O(m) work; rounds = number of distinct
- * finite distances).  gbbs_opts.delta > 1 selects Delta-stepping buckets.
+ * vertex is expanded exactly once (O(m) work) and every distinct finite
+ * distance is an extracted bucket (a bucket whose entries all moved to earlier
+ * buckets still costs a round).  gbbs_opts.delta > 1 selects Delta-stepping
+ * buckets with a near list.
  *
  * Weights, dist, stream and error conventions as gbbs_bellman_ford (including
  * GBBS_ERANGE), plus GBBS_EINVAL if floor((delta - 1 + maxw) / delta) >= 64
- * (the bucket ring holds 64 lists).  The bucket structure is allocated on the
- * first call and kept with the handle: 4 * nbq * 2^ceil(log2 n) bytes for the
- * bucket lists (nbq = the power of two above that span, <= 64) plus 16n bytes.
+ * (the bucket ring holds 64 lists), and GBBS_ENOMEM if a bucket list
+ * overflows its capacity.  The bucket structure is allocated on the first call
+ * and kept with the handle: nbq lists (the power of two above that span, <= 64)
+ * of 2^ceil(log2 n) vertex ids each — fewer when that would take over half of
+ * the free device memory — plus 16n bytes (near lists and round tags only when
+ * delta > 1 or a weight is 0).
  */
 int gbbs_wbfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
               void *cuda_stream);
@@ -319,8 +324,9 @@ typedef struct {
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */
 typedef struct {
   int32_t dense;          /* round kind: 0 = list push, 1 = dense pull,
-                             2 = bitmap-forward push, 3 = wBFS bucket
-                             list, 4 = wBFS near list (same bucket)       */
+                             2 = bitmap-forward push, 3 = pull-min (BF /
+                             widest path, GBBS_MODE_PULL) or, for wBFS, a
+                             bucket list, 4 = wBFS near list (same bucket) */
   int32_t bucket;         /* wBFS: the bucket the round processed; else 0 */
   int64_t frontier;       /* |U|: frontier vertices with out-degree > 0   */
   int64_t frontier_edges; /* sum of out-degrees of U                       */
