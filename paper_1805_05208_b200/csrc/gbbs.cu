@@ -866,10 +866,11 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
     int rc2 = wbfs_setup(g, o.delta, p);
     if (rc2) return rc2;
   }
-#ifdef GBBS_DBG_PHASE
+#if defined(GBBS_DBG_PHASE) || defined(GBBS_DIAG_TILE)
   static unsigned long long *dbg = nullptr;
-  if (!dbg) cudaMalloc(&dbg, 64 * 4 * 8);
-  cudaMemsetAsync(dbg, 0, 64 * 4 * 8, st);
+  constexpr size_t DBGW = 16 * 16384;
+  if (!dbg) cudaMalloc(&dbg, DBGW * 8);
+  cudaMemsetAsync(dbg, 0, DBGW * 8, st);
   p.dbg = dbg;
 #endif
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -930,6 +931,25 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
       }
     }
   }
+#ifdef GBBS_DIAG_TILE
+  {
+    std::vector<unsigned long long> hv(16 * 16384);
+    cudaMemcpy(hv.data(), dbg, hv.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long h[16] = {0};
+    for (size_t w = 0; w < 16384; w++)
+      for (int k = 0; k < 8; k++) {
+        h[k] += hv[16 * w + k];
+        h[8 + k] = std::max(h[8 + k], hv[16 * w + 8 + k]);
+      }
+    const char *nm[6] = {"search", "OBF", "tgt", "pre", "atom", "flush"};
+    for (int k = 0; k < 6; k++) {
+      const double c = (double)(k == 5 ? h[7] : h[6]);
+      fprintf(stderr, "diag %-6s mean %.2fus max %.2fus\n", nm[k], c ? h[k] / c / 1e3 : 0.0,
+              h[8 + k] / 1e3);
+    }
+    fprintf(stderr, "diag tiles %llu flushes %llu\n", h[6], h[7]);
+  }
+#endif
 #ifdef GBBS_DBG_PHASE
   {
     unsigned long long h[256];

@@ -66,6 +66,9 @@ namespace cg = cooperative_groups;
 constexpr int BLOCK = 256;            // threads per CTA
 constexpr int NWARPS = BLOCK / 32;
 constexpr int TE = 256;               // edges per warp tile (edgeMapBlocked bsize)
+#ifndef GBBS_SEARCH_EST
+#define GBBS_SEARCH_EST 1
+#endif
 #ifndef GBBS_NCH
 #define GBBS_NCH 4
 #endif
@@ -141,7 +144,7 @@ struct Params {
   // signed Bellman-Ford (sbf_kernel)
   long long *sdist;          // [n] int64 distances
   int neg_scope;             // 0: all -inf on a negative cycle, 1: its forward closure
-#ifdef GBBS_DBG_PHASE
+#if defined(GBBS_DBG_PHASE) || defined(GBBS_DIAG_TILE)
   unsigned long long *dbg;   // [64][4] per-round max phase durations (ns)
 #endif
 };
@@ -192,6 +195,9 @@ struct WarpState {
   unsigned long long pmask = 0;  // wBFS: bucket lists this lane appended to
   unsigned long long K = 0, D = 0;
   unsigned long long edges = 0, swept = 0, acquired = 0;
+#ifdef GBBS_DIAG_LIST  // diagnostic builds: list-round phase timestamps
+  unsigned long long t1 = 0, t2 = 0;
+#endif
 };
 
 // ---- small device helpers --------------------------------------------------
@@ -262,6 +268,21 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+#ifdef GBBS_DIAG_TILE
+// diagnostic builds: phase durations of BFS list tiles, p.dbg[0..5] sums,
+// [6] tiles, [7] flushes, [8..13] maxima (ns); dep() waits for a value
+#define GBBS_DEP(x) asm volatile("" ::"r"((uint32_t)(x)))
+__device__ __forceinline__ void diag_add(const unsigned long long *dbgc, int k,
+                                         unsigned long long dt) {
+  // one private 16-word slot per warp of the grid (no contention); host sums
+  unsigned long long *dbg = const_cast<unsigned long long *>(dbgc);
+  if ((threadIdx.x & 31) == 0 && dbg) {
+    unsigned long long *sl = dbg + 16 * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    sl[k] += dt;
+    sl[8 + k] = max(sl[8 + k], dt);
+  }
+}
+#endif
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -307,6 +328,26 @@ __device__ __forceinline__ long long warp_upper(const long long *O, long long lo
   const long long idx = lo + lane;
   const bool ok = idx < hi && __ldcg(O + idx) <= key;
   return lo + (31 - __clz(__ballot_sync(FULL, ok)));
+}
+
+// Owner search of edge `key` in a list of f entries holding E edges, with an
+// interpolation first probe: the 32 entries around key * f / E answer in one
+// round trip when the frontier's degrees are near-uniform (the torus: the plain
+// 32-ary search costs 4 dependent loads there at 10^5 entries); otherwise the
+// probe narrows the range to one side and warp_upper finishes.  Same result as
+// warp_upper(O, 0, f, key) (O non-decreasing, O[0] = 0 <= key).
+__device__ __forceinline__ long long warp_upper_est(const long long *O, long long f, long long E,
+                                                    long long key) {
+  if (GBBS_SEARCH_EST && f > 64) {
+    const int lane = threadIdx.x & 31;
+    const long long est = (long long)((double)key * (double)f / (double)E);
+    const long long base = min(max(est - 16, 0ll), f - 32);
+    const unsigned bb = __ballot_sync(FULL, __ldcg(O + base + lane) <= key);
+    if (bb == 0) return warp_upper(O, 0, base, key);
+    if (bb == FULL) return warp_upper(O, base + 31, f, key);
+    return base + 31 - __clz(bb);
+  }
+  return warp_upper(O, 0, f, key);
 }
 
 // Append the lanes' (v, a = offset(v), deg > 0) to list `nb` at positions and
@@ -556,9 +597,20 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
   const int lane = threadIdx.x & 31;
   bool win[NB];
   if (ALGO == ALGO_BFS) {
+#ifdef GBBS_DIAG_TILE
+    const unsigned long long tA0 = globaltimer_ns();
+#pragma unroll
+    for (int j = 0; j < NB; j++) GBBS_DEP(vv[j]);
+    const unsigned long long tA1 = globaltimer_ns();
+#endif
     uint32_t pre[NB];
 #pragma unroll
     for (int j = 0; j < NB; j++) pre[j] = act[j] ? prebits[vv[j] >> 5] : FULL;
+#ifdef GBBS_DIAG_TILE
+#pragma unroll
+    for (int j = 0; j < NB; j++) GBBS_DEP(pre[j]);
+    const unsigned long long tA2 = globaltimer_ns();
+#endif
 #pragma unroll
     for (int j = 0; j < NB; j++) {
       const uint32_t bit = 1u << (vv[j] & 31);
@@ -568,6 +620,16 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
         win[j] = !(old & bit);
       }
     }
+#ifdef GBBS_DIAG_TILE
+#pragma unroll
+    for (int j = 0; j < NB; j++) GBBS_DEP(win[j]);
+    const unsigned long long tA3 = globaltimer_ns();
+    if (EMIT == EMIT_LIST) {
+      diag_add(p.dbg, 2, tA1 - tA0);
+      diag_add(p.dbg, 3, tA2 - tA1);
+      diag_add(p.dbg, 4, tA3 - tA2);
+    }
+#endif
 #pragma unroll
     for (int j = 0; j < NB; j++) {
       if (win[j]) {
@@ -690,6 +752,9 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
   const long long *B = p.fb[lb];
   const uint32_t *F = p.fv[lb];
   if (STATS && lane == 0) ws.edges += (unsigned long long)(te - ts);
+#ifdef GBBS_DIAG_TILE
+  const unsigned long long tT0 = globaltimer_ns();
+#endif
 
   const long long k = i0 + lane;
   // O, base and vertex of the next 32 entries are loaded together (the base and
@@ -703,6 +768,13 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
   }
   const unsigned inb = __ballot_sync(FULL, Ok < te);  // owners with an edge in the tile
   const int n32 = __popc(inb);
+#ifdef GBBS_DIAG_TILE
+  GBBS_DEP(Bk); GBBS_DEP(Uk);
+  if (ALGO == ALGO_BFS) {
+    diag_add(p.dbg, 1, globaltimer_ns() - tT0);
+    diag_add(p.dbg, 6, 1);
+  }
+#endif
   if (n32 < 32) {
     // Register path: lane k holds owner i0+k; a chunk's owners come from a
     // ballot (owners starting at or before the chunk) plus an or-reduce of the
@@ -1361,7 +1433,7 @@ __device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpSta
       long long t = (long long)__shfl_sync(FULL, u, 0);
       if (t >= ntiles) break;
       const long long t1 = min(t + G, ntiles);
-      long long i0 = warp_upper(p.fo[lb], 0, f, t * TR);
+      long long i0 = warp_upper_est(p.fo[lb], f, E, t * TR);
       for (; t < t1; t++)
         i0 = push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, i0, t, f, E, nb, r, bits, prebits, TR);
     }
@@ -1372,9 +1444,23 @@ __device__ __forceinline__ void list_round(const Params &p, WarpSmem &w, WarpSta
   long long t = gw * per;
   const long long t1 = min(t + per, ntiles);
   if (t >= t1) return;
-  long long i0 = warp_upper(p.fo[lb], 0, f, t * TR);
-  for (; t < t1; t++)
+#ifdef GBBS_DIAG_TILE
+  const unsigned long long tS0 = globaltimer_ns();
+#endif
+  long long i0 = warp_upper_est(p.fo[lb], f, E, t * TR);
+#ifdef GBBS_DIAG_TILE
+  GBBS_DEP(i0);
+  if (ALGO == ALGO_BFS) diag_add(p.dbg, 0, globaltimer_ns() - tS0);
+#endif
+#ifdef GBBS_DIAG_LIST
+  if (STATS) ws.t1 = globaltimer_ns();
+#endif
+  for (; t < t1; t++) {
     i0 = push_tile<ALGO, STATS, EMIT>(p, w, ws, lb, i0, t, f, E, nb, r, bits, prebits, TR);
+#ifdef GBBS_DIAG_LIST
+    if (STATS && !ws.t2) ws.t2 = globaltimer_ns();
+#endif
+  }
 }
 
 // ---- teams: several traversals in one cooperative launch --------------------------
@@ -1621,14 +1707,26 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     if (STATS) t_work = globaltimer_ns();
     if (ws.scnt > 0) {
       if (STATS && lane == 0) ws.acquired += ws.scnt;
+#ifdef GBBS_DIAG_TILE
+      const unsigned long long tF0 = globaltimer_ns();
+#endif
       warp_flush<ALGO>(p, wsm.stage, ws.scnt, nb, (int)r,
                        (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nb], &t_work);
+#ifdef GBBS_DIAG_TILE
+      if (ALGO == ALGO_BFS && kind == 0) {
+        diag_add(p.dbg, 5, globaltimer_ns() - tF0);
+        diag_add(p.dbg, 7, 1);
+      }
+#endif
     }
     if (emit_count) {
       const unsigned long long K = warp_sum64((long long)ws.K), D = warp_sum64((long long)ws.D);
       if (lane == 0 && K) atomicAdd(p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
     }
     if (STATS) t_flush = globaltimer_ns();
+#ifdef GBBS_DIAG_LIST
+    if (STATS) { t_work = ws.t1; t_flush = ws.t2; ws.t1 = ws.t2 = 0; }
+#endif
     if (STATS && p.stats && r < p.stats_cap) {
       // one global atomic per CTA and counter
       if (tid < 5) s.sacc[tid] = 0;
