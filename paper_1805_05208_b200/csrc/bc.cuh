@@ -300,7 +300,7 @@ __device__ __forceinline__ void bc_level(const BcParams &p, BcWarpSmem &w, int &
       long long t = (long long)__shfl_sync(FULL, u, 0);
       if (t >= ntiles) break;
       const long long t1 = min(t + G, ntiles);
-      long long i0 = warp_upper(O, 0, f, t * TE);
+      long long i0 = warp_upper_est(O, f, E, t * TE);
       for (; t < t1; t++) i0 = bc_tile<BACK>(p, w, scnt, F, O, B, f, E, i0, t, l, qnext, ctr);
     }
     return;
@@ -309,7 +309,7 @@ __device__ __forceinline__ void bc_level(const BcParams &p, BcWarpSmem &w, int &
   long long t = gw * per;
   const long long t1 = min(t + per, ntiles);
   if (t >= t1) return;
-  long long i0 = warp_upper(O, 0, f, t * TE);
+  long long i0 = warp_upper_est(O, f, E, t * TE);
   for (; t < t1; t++) i0 = bc_tile<BACK>(p, w, scnt, F, O, B, f, E, i0, t, l, qnext, ctr);
 }
 

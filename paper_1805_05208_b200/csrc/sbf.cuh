@@ -62,7 +62,7 @@ __device__ __forceinline__ void sbf_tile(const Params &p, SbfWarpSmem &w, WarpSt
   const long long *B = p.fb[lb];
   const uint32_t *F = p.fv[lb];
   if (STATS && lane == 0) ws.edges += (unsigned long long)(te - ts);
-  const long long i0 = warp_upper(O, 0, f, ts);
+  const long long i0 = warp_upper_est(O, f, E, ts);
   {
     int4 *h4 = reinterpret_cast<int4 *>(w.head);
     h4[lane] = make_int4(0, 0, 0, 0);  // SBF_TE = 128 = 32 lanes x 4

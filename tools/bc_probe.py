@@ -3,7 +3,7 @@ sys.path.insert(0, os.getcwd())
 import torch, numpy as np
 from graphgen import device as gdev
 from paper_1805_05208_b200 import gbbs
-for name in ("c2", "c4"):
+for name in (sys.argv[1] if len(sys.argv) > 1 else "c2,c4").split(","):
     G = gdev.build_config(name, weights=False)
     g = gbbs.Graph(G["offsets"], G["targets"], None, symmetric=True)
     d = torch.empty(G["n"], dtype=torch.float64, device="cuda")
