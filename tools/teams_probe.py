@@ -26,8 +26,10 @@ def main():
             else ("bfs",)
         for algo in algos:
             base = None
-            for teams in [int(x) for x in os.environ.get("TEAMS", "1,2,3,4").split(",")]:
-                opts = gbbs.make_opts(teams=teams)
+            for teams, T, cps in [(int(a), int(b), int(c)) for a in os.environ.get("TEAMS", "1,2,3,4").split(",")
+                                  for b in os.environ.get("THRESH", "20").split(",")
+                                  for c in os.environ.get("CTAS", "0").split(",")]:
+                opts = gbbs.make_opts(teams=teams, threshold_den=T, ctas_per_sm=cps)
                 ts = []
                 for rep in range(4):
                     flush.fill_(1)
@@ -49,7 +51,7 @@ def main():
                 if base is None:
                     base = out
                 same = bool(np.allclose(out, base, rtol=1e-9)) if algo == "bc" else bool((out == base).all())
-                print(f"{name} {algo} teams={teams} step_ms={np.median(ts):.3f} rows_equal={same}",
+                print(f"{name} {algo} teams={teams} T={T} ctas={cps} step_ms={np.median(ts):.3f} rows_equal={same}",
                       flush=True)
         g.close()
         del G, g
