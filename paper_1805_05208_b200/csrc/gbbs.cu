@@ -184,11 +184,11 @@ __global__ void k_absmax_i32(const uint32_t *w, long long m, unsigned long long 
   if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
-// bit v set iff out-degree(v) > HEAVY (wBFS: insertions count the hubs of a bucket)
+// bit v set iff out-degree(v) > WBFS_HEAVY (wBFS: insertions count the hubs of a bucket)
 __global__ void k_heavy_bits(const long long *off, long long n, long long nwords, uint32_t *hv) {
   long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if ((v >> 5) >= nwords) return;
-  const bool h = v < n && off[v + 1] - off[v] > HEAVY;
+  const bool h = v < n && off[v + 1] - off[v] > WBFS_HEAVY;
   const unsigned b = __ballot_sync(0xffffffffu, h);
   if ((threadIdx.x & 31) == 0) hv[v >> 5] = b;
 }

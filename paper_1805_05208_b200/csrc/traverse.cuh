@@ -75,6 +75,14 @@ constexpr int TE = 256;               // edges per warp tile (edgeMapBlocked bsi
 constexpr int NCH = GBBS_NCH;         // 32-edge chunks in flight per batch
 constexpr int WCAP = 384;             // per-warp staging capacity (vertices)
 constexpr long long HEAVY = 512;      // bitmap-forward: deferred to heavy tiles above this
+// wBFS bucket sweeps: vertices above this many edges go to the heavy list and are
+// pushed in edge tiles by every warp after a barrier (a small bucket is swept one
+// vertex per lane by few warps; warp-serial pushes of its 33-512-edge vertices
+// made the rounds that expand rMAT's hubs the slowest of the run)
+#ifndef GBBS_WBFS_HEAVY
+#define GBBS_WBFS_HEAVY 32
+#endif
+constexpr long long WBFS_HEAVY = GBBS_WBFS_HEAVY;
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
@@ -132,12 +140,12 @@ struct Params {
   // wBFS (ALGO_WBFS) bucket structure, wbfs_kernel
   uint32_t *bq;              // [nb][qcap] ring of bucket lists (vertex ids, circular)
   unsigned long long *btail; // [nb] monotone append counters of the bucket lists
-  unsigned long long *bheavy;// [nb] monotone counters of heavy (deg > HEAVY) entries
+  unsigned long long *bheavy;// [nb] monotone counters of heavy (deg > WBFS_HEAVY) entries
   uint32_t *xq[3];           // near lists: re-insertions into the current bucket
   unsigned long long *xcnt;  // [3] their counters, [3] heavy counters after them
   unsigned long long *pub;   // [3] per-round masks of bucket lists that got entries
   uint32_t *tag;             // [n] round tag deduplicating near-list insertions
-  const uint32_t *hv;        // [nwords] out-degree > HEAVY
+  const uint32_t *hv;        // [nwords] out-degree > WBFS_HEAVY
   unsigned long long qcap;   // per-list capacity (power of two >= n)
   uint32_t delta;            // bucket width
   int nbq;                   // number of bucket lists (power of two)
@@ -493,6 +501,7 @@ constexpr uint32_t NOKEY = 0xFFFFFFFFu;
 // the list key of every staged vertex and a 65-bin histogram over the keys.
 struct WbfsWarpSmem {
   uint32_t hist[XKEY + 1];
+  uint32_t hh[XKEY + 1];  // heavy entries per key (one counter atomic per key and flush)
   uint8_t key[WCAP];
 };
 extern __shared__ __align__(16) unsigned char gbbs_dyn_smem[];
@@ -540,14 +549,22 @@ __device__ __forceinline__ void wbfs_flush(const Params &p, WarpState &ws, const
         p.xq[xr][pos] = v;
       } else
         p.bq[(unsigned long long)key * p.qcap + (pos & (p.qcap - 1))] = v;
-      if ((__ldg(p.hv + (v >> 5)) >> (v & 31)) & 1u)
-        atomicAdd(key == XKEY ? p.xcnt + 3 + xr : p.bheavy + key, 1ull);
+      if ((__ldg(p.hv + (v >> 5)) >> (v & 31)) & 1u) atomicAdd(&w.hh[key], 1u);
     }
+  }
+  __syncwarp();
+  {
+    const uint32_t gA = w.hh[lane], gB = w.hh[lane + 32];
+    if (gA) atomicAdd(p.bheavy + lane, (unsigned long long)gA);
+    if (gB) atomicAdd(p.bheavy + lane + 32, (unsigned long long)gB);
+    if (lane == 0 && w.hh[XKEY]) atomicAdd(p.xcnt + 3 + xr, (unsigned long long)w.hh[XKEY]);
   }
   __syncwarp();
   w.hist[lane] = 0;
   w.hist[lane + 32] = 0;
-  if (lane == 0) w.hist[XKEY] = 0;
+  w.hh[lane] = 0;
+  w.hh[lane + 32] = 0;
+  if (lane == 0) w.hist[XKEY] = w.hh[XKEY] = 0;
   if (STATS && lane == 0) ws.acquired += cnt;
   __syncwarp();
 }
@@ -974,7 +991,7 @@ __device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, Wa
                                               unsigned long long *hctr, int nb, int r,
                                               uint32_t *bits, const uint32_t *prebits) {
   const int lane = threadIdx.x & 31;
-  const bool heavy = dg > (int)HEAVY;
+  const bool heavy = dg > (int)(ALGO == ALGO_WBFS ? WBFS_HEAVY : HEAVY);
   warp_append(p, LIST_HEAVY, hctr, heavy, v, a, dg);
   unsigned med = __ballot_sync(FULL, dg > 32 && !heavy);
   while (med) {
@@ -1852,7 +1869,8 @@ __device__ __forceinline__ void wbfs_body(const Params &p, int G) {
   {
     WbfsWarpSmem &w = wbfs_smem();
     w.hist[lane] = w.hist[lane + 32] = 0;
-    if (lane == 0) w.hist[XKEY] = 0;
+    w.hh[lane] = w.hh[lane + 32] = 0;
+    if (lane == 0) w.hist[XKEY] = w.hh[XKEY] = 0;
   }
   team_sync<MG>(grid, p.bar, GBBS_NBLK);
 
