@@ -181,8 +181,12 @@ int gbbs_widest_path(const gbbs_graph *g, uint32_t src, uint32_t *width,
  * sigma_st(v) / sigma_st, Brandes' dependency of src on v, following
  * out-edges (the paper's input is undirected; pass a symmetric CSR).  The
  * forward pass counts shortest paths with an atomicCAS test-and-set on the
- * level and an fp64 fetch-and-add on sigma; the backward pass accumulates
- * delta level by level.  delta[src] = 0 and unreached vertices get 0
+ * level and an fp64 fetch-and-add on sigma, or, on a symmetric graph for a
+ * level where |U| + sum deg(U) > m/T and the unvisited vertices carry under a
+ * quarter of the frontier's edges, by pulling (each unvisited vertex sums
+ * sigma over its neighbours on the level; reading B3; _ex: opts.mode
+ * GBBS_MODE_SPARSE forces push, GBBS_MODE_DENSE pull); the backward pass
+ * accumulates delta level by level.  delta[src] = 0 and unreached vertices get 0
  * (reading B1).
  *
  * delta   double[n], caller-owned, host or device.  fp64 accumulation in a

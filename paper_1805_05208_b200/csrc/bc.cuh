@@ -12,6 +12,11 @@
 //           v lies on level r+1 (won or lost to a same-level writer), and the
 //           fetch-and-add is atomicAdd(sigma[v], sigma[u]) in fp64.  Winners are
 //           appended to a cumulative level queue (all levels kept, in order).
+//  dense    forward level on a symmetric graph (Ligra's dense edgeMap, P:1851-1874,
+//           reading B3): every unvisited vertex v sums sigma over its neighbours
+//           on level r (owner-computes, no atomics) and joins level r+1 iff the
+//           sum is positive; used when |U| + sum deg(U) > m/T and the unvisited
+//           vertices carry fewer edges than the frontier (no early exit here).
 //  backward levels L-1 .. 1: for every edge (u, v) of a level-l vertex u with
 //           dist[v] = l+1, delta[u] += sigma[u] / sigma[v] * (1 + delta[v])
 //           (Brandes' recurrence), a grid barrier between levels.
@@ -29,6 +34,12 @@
 #endif
 #ifndef GBBS_BC_SEG
 #define GBBS_BC_SEG 1
+#endif
+// Dense forward levels (reading B3) need the unvisited vertices' edges below
+// 1/RATIO of the frontier's: a pulled edge (lane-serial, no early exit) costs more
+// than a pushed one
+#ifndef GBBS_BC_PULL_RATIO
+#define GBBS_BC_PULL_RATIO 4
 #endif
 #ifndef GBBS_BC_DYNQ_FWD
 #define GBBS_BC_DYNQ_FWD 1
@@ -58,6 +69,8 @@ struct BcParams {
   long long *rounds_out;
   int ebits;
   uint32_t src;
+  long long dense_threshold;  // m / T
+  int dense_mode;             // 0: the rule above, 1: never (push), 2: always (pull)
 };
 
 struct BcWarpSmem {
@@ -281,6 +294,91 @@ __device__ __forceinline__ long long bc_tile(const BcParams &p, BcWarpSmem &w, i
   return onext == te ? i0 + nown : i0 + nown - 1;
 }
 
+// Dense forward level l (reading B3): units of BC_PULLV vertices from the level's
+// counter; a lane takes an unvisited vertex and sums sigma over its level-l
+// neighbours (4 edge loads in flight), vertices above 32 edges are summed by the
+// whole warp; winners get level l+1 and sigma with plain stores (each is written
+// by its owner only) and are appended to the level queue as in the push.
+constexpr int BC_PULLV = 1024;
+__device__ __forceinline__ void bc_pull_level(const BcParams &p, BcWarpSmem &w, int &scnt, int l,
+                                              long long qnext, unsigned long long *ctr,
+                                              unsigned long long *q) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lv = (uint32_t)l, nl = (uint32_t)(l + 1);
+  for (;;) {
+    unsigned long long u0 = 0;
+    if (lane == 0) u0 = atomicAdd(q, 1ull);
+    const long long v0 = (long long)__shfl_sync(FULL, u0, 0) * BC_PULLV;
+    if (v0 >= p.n) break;
+    const long long v1 = min(v0 + (long long)BC_PULLV, p.n);
+    for (long long vb = v0; vb < v1; vb += 32) {
+      const long long v = vb + lane;
+      long long a = 0;
+      int dg = 0;
+      if (v < v1 && ld_relaxed(p.dist + v) == INF) {
+        a = __ldg(p.off + v);
+        dg = (int)(__ldg(p.off + v + 1) - a);
+      }
+      double sum = 0.0;
+      unsigned big = __ballot_sync(FULL, dg > 32);
+      while (big) {
+        const int b = __ffs(big) - 1;
+        big &= big - 1;
+        const long long ba = __shfl_sync(FULL, a, b);
+        const int bd = __shfl_sync(FULL, dg, b);
+        double t = 0.0;
+        for (int e0 = 0; e0 < bd; e0 += 128) {
+          uint32_t u[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const int e = e0 + 32 * j + lane;
+            GBBS_CHECK(e >= bd || (ba + e >= 0 && ba + e < p.m));
+            u[j] = e < bd ? ld_stream(p.tgt + ba + e) : 0u;
+          }
+          uint32_t d[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) d[j] = (e0 + 32 * j + lane < bd) ? p.dist[u[j]] : INF;
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            if (d[j] == lv) t += p.sigma[u[j]];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+        if (lane == b) sum = t;
+      }
+      const int mine = dg <= 32 ? dg : 0;
+      int mx = mine;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+      for (int jj = 0; jj < mx; jj += 4) {
+        uint32_t u[4], d[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          GBBS_CHECK(jj + j >= mine || (a + jj + j >= 0 && a + jj + j < p.m));
+          u[j] = jj + j < mine ? ld_stream(p.tgt + a + jj + j) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) d[j] = jj + j < mine ? p.dist[u[j]] : INF;
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          if (d[j] == lv) sum += p.sigma[u[j]];
+      }
+      const bool win = sum > 0.0;
+      if (win) {
+        p.dist[v] = nl;
+        p.sigma[v] = sum;
+      }
+      const unsigned bw = __ballot_sync(FULL, win);
+      if (win) w.stage[scnt + __popc(bw & lanemask_lt())] = (uint32_t)v;
+      scnt += __popc(bw);
+      if (scnt > WCAP - 32) {
+        bc_flush(p, w.stage, scnt, qnext, ctr);
+        scnt = 0;
+      }
+    }
+  }
+}
+
 template <bool BACK>
 __device__ __forceinline__ void bc_level(const BcParams &p, BcWarpSmem &w, int &scnt,
                                          long long start, long long f, long long E, int l,
@@ -356,6 +454,7 @@ __device__ __forceinline__ void bc_body(const BcParams &p, int G) {
 
   const unsigned long long emask = (1ull << p.ebits) - 1;
   long long start = 0;  // queue position of the current level
+  long long seenE = 0;  // edges of the listed levels' vertices (so far and this one)
   int l = 0;
   for (;; l++) {
     if (tid == 0) s.cnt = ld_relaxed64(p.cnt + (l & 3));
@@ -374,8 +473,17 @@ __device__ __forceinline__ void bc_body(const BcParams &p, int G) {
       p.lvl[3 * l + 2] = E;
     }
     int scnt = 0;
-    bc_level<false>(p, w, scnt, start, f, E, l, start + f, p.cnt + ((l + 1) & 3), gw, nw,
-                    p.wq + (l & 3));
+    seenE += E;
+    // dense iff the paper's rule holds and the pull (every edge of every unvisited
+    // vertex: m - seenE on a symmetric graph) reads fewer edges than the push (E)
+    const bool dense = p.dense_mode == 2 ||
+                       (p.dense_mode == 0 && f + E > p.dense_threshold &&
+                        GBBS_BC_PULL_RATIO * (p.m - seenE) < E);
+    if (dense)
+      bc_pull_level(p, w, scnt, l, start + f, p.cnt + ((l + 1) & 3), p.wq + (l & 3));
+    else
+      bc_level<false>(p, w, scnt, start, f, E, l, start + f, p.cnt + ((l + 1) & 3), gw, nw,
+                      p.wq + (l & 3));
     if (scnt > 0) bc_flush(p, w.stage, scnt, start + f, p.cnt + ((l + 1) & 3));
     start += f;
     team_sync<MG>(grid, p.bar, GBBS_NBLK);

@@ -1437,6 +1437,15 @@ static BcScratch *bc_scratch(gbbs_graph *g, int *rc) {
   return b;
 }
 
+// Forward-level direction (reading B3): pull only on symmetric graphs; opts.mode
+// SPARSE = always push, DENSE = always pull, else the rule in bc_body.
+static void bc_dense(const gbbs_graph *g, const gbbs_opts &o, BcParams &p) {
+  p.dense_threshold = g->m / (long long)o.threshold_den;
+  if (!(g->flags & GBBS_SYMMETRIC) || o.mode == GBBS_MODE_SPARSE) p.dense_mode = 1;
+  else if (o.mode == GBBS_MODE_DENSE) p.dense_mode = 2;
+  else p.dense_mode = 0;
+}
+
 static void free_bc(gbbs_graph *g) {
   if (!g->bc) return;
   cudaFree(g->bc->dist); cudaFree(g->bc->sigma); cudaFree(g->bc->delta); cudaFree(g->bc->lvl);
@@ -1478,6 +1487,7 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   p.rounds_out = g->rounds;
   p.ebits = g->ebits;
   p.src = src;
+  bc_dense(g, o, p);
   void *args[] = {&p};
   if (stats) {
     if (!g->ev[0]) {
@@ -1583,6 +1593,7 @@ extern "C" int gbbs_betweenness_batch_ex(const gbbs_graph *cg_, const uint32_t *
       p.bar = x ? x->bar : g->bar0;
       p.ebits = g->ebits;
       p.src = srcs[i0 + t];
+      bc_dense(g, o, p);
     }
     if (mp.G == 1) {  // the plain kernel (the team form costs ~15 % at G = 1)
       void *a1[] = {&mp.ps[0]};

@@ -254,12 +254,14 @@ def gbbs_betweenness_batch(handle, srcs, delta, stream=None, opts=None):
                                              st, ctypes.byref(opts)))
 
 
-def gbbs_betweenness(handle, src, delta, stream=None, stats=None):
+def gbbs_betweenness(handle, src, delta, stream=None, stats=None, opts=None):
     st = _stream(stream, delta)
-    if stats is None:
+    if stats is None and opts is None:
         _check(lib.gbbs_betweenness(handle, int(src), _ptr(delta), st))
     else:
-        _check(lib.gbbs_betweenness_ex(handle, int(src), _ptr(delta), st, None, ctypes.byref(stats)))
+        _check(lib.gbbs_betweenness_ex(handle, int(src), _ptr(delta), st,
+                                       None if opts is None else ctypes.byref(opts),
+                                       None if stats is None else ctypes.byref(stats)))
 
 
 def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0, neg_scope=0, bsize=0,
@@ -366,5 +368,5 @@ class Graph:
     def bellman_ford_signed(self, src, dist, stream=None, opts=None, stats=None):
         gbbs_bellman_ford_signed(self.handle, src, dist, stream, opts, stats)
 
-    def betweenness(self, src, delta, stream=None, stats=None):
-        gbbs_betweenness(self.handle, src, delta, stream, stats)
+    def betweenness(self, src, delta, stream=None, stats=None, opts=None):
+        gbbs_betweenness(self.handle, src, delta, stream, stats, opts)

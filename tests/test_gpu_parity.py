@@ -359,13 +359,14 @@ def test_widest_c1_and_torus(G):
 
 # ---- NEXT-3 single-source betweenness -----------------------------------------------
 
-def run_bc(G, g, src, host=False):
+def run_bc(G, g, src, host=False, mode=None):
+    opts = None if mode is None else G.make_opts(mode=mode)
     if host:
         d = np.empty(g.n, np.float64)
-        g.betweenness(src, d)
+        g.betweenness(src, d, opts=opts)
         return d
     d = torch.empty(g.n, dtype=torch.float64, device="cuda")
-    g.betweenness(src, d)
+    g.betweenness(src, d, opts=opts)
     return d.cpu().numpy()
 
 
@@ -407,6 +408,30 @@ def test_bc_random_and_rmat(G, seed):
     off, tgt = graphgen.rmat_graph(15, 1 << 19, 80 + seed, 0.57, 0.19, 0.19)
     g = G.Graph(off, tgt, symmetric=True)
     assert_bc_close(run_bc(G, g, 0), oracle.betweenness(off, tgt, 0)[0])
+    g.close()
+
+
+@pytest.mark.parametrize("mode", ["sparse", "dense", "auto"])
+def test_bc_forward_directions(G, mode):
+    """Reading B3: forward levels pushed (CAS + fp64 FA), pulled (owner-computes sum
+    over level-l neighbours, symmetric graphs), or chosen per level; every form
+    gives Brandes' dependencies.  The star from a leaf pulls its 499-edge hub with
+    the whole warp at level 0; a directed graph ignores DENSE (push only)."""
+    md = {"sparse": G.GBBS_MODE_SPARSE, "dense": G.GBBS_MODE_DENSE, "auto": G.GBBS_MODE_AUTO}[mode]
+    cases = [graphgen.random_graph(900, 0.006, 91, symmetric=True),
+             graphgen.rmat_graph(14, 1 << 18, 92, 0.57, 0.19, 0.19),
+             graphgen.torus3d(10),
+             graphgen.from_edge_list(500, [(0, i) for i in range(1, 500)]),
+             graphgen.from_edge_list(2000, path_graph(2000))]
+    for off, tgt in cases:
+        g = G.Graph(off, tgt, symmetric=True)
+        for src in (0, 7, len(off) - 2):
+            assert_bc_close(run_bc(G, g, src, mode=md), oracle.betweenness(off, tgt, src)[0])
+        g.close()
+    off, tgt = graphgen.random_graph(700, 0.01, 93, symmetric=False)
+    g = G.Graph(off, tgt, symmetric=False)
+    for src in (0, 5):
+        assert_bc_close(run_bc(G, g, src, mode=md), oracle.betweenness(off, tgt, src)[0])
     g.close()
 
 
