@@ -65,7 +65,10 @@ namespace cg = cooperative_groups;
 
 constexpr int BLOCK = 256;            // threads per CTA
 constexpr int NWARPS = BLOCK / 32;
-constexpr int TE = 256;               // edges per warp tile (edgeMapBlocked bsize)
+#ifndef GBBS_TE
+#define GBBS_TE 256
+#endif
+constexpr int TE = GBBS_TE;           // edges per warp tile (edgeMapBlocked bsize)
 #ifndef GBBS_SEARCH_EST
 #define GBBS_SEARCH_EST 1
 #endif
@@ -73,7 +76,15 @@ constexpr int TE = 256;               // edges per warp tile (edgeMapBlocked bsi
 #define GBBS_NCH 4
 #endif
 constexpr int NCH = GBBS_NCH;         // 32-edge chunks in flight per batch
-constexpr int WCAP = 384;             // per-warp staging capacity (vertices)
+#ifndef GBBS_WCAP
+#define GBBS_WCAP 192
+#endif
+// per-warp staging capacity (vertices).  192 rather than 384: the kernels' static
+// shared memory drops from 46 to 40 KB per CTA, so four CTAs fit the 164 KB
+// shared-memory carve-out and L1 grows from ~60 to ~92 KB per SM (BFS c2/c4/c5
+// -2 to -3.5 %, BF -3.7 %, 8-team BFS batch -3.3 %); adding 2 KB per CTA instead
+// (a 228 KB carve-out, ~28 KB of L1) cost 20 %
+constexpr int WCAP = GBBS_WCAP;
 constexpr long long HEAVY = 512;      // bitmap-forward: deferred to heavy tiles above this
 // wBFS bucket sweeps: vertices above this many edges go to the heavy list and are
 // pushed in edge tiles by every warp after a barrier (a small bucket is swept one
@@ -157,7 +168,10 @@ struct Params {
 #endif
 };
 
-constexpr int SWEEP_WORDS = 32;        // max bitmap words gathered per warp step (sweeps)
+#ifndef GBBS_SWEEP_WORDS
+#define GBBS_SWEEP_WORDS 32
+#endif
+constexpr int SWEEP_WORDS = GBBS_SWEEP_WORDS;  // max bitmap words gathered per warp step (sweeps)
 // Sweep unit (words per warp step, a power of two <= SWEEP_WORDS) is chosen per
 // traversal so that every warp gets at least this many units: on small graphs a
 // 32-word unit per warp leaves the round waiting on the slowest unit.
@@ -1136,6 +1150,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #ifndef GBBS_PULL_SW
 #define GBBS_PULL_SW 32
 #endif
+static_assert(GBBS_PULL_SW <= SWEEP_WORDS, "pull units are gathered into SweepSmem");
 #ifndef GBBS_PULL_STEPS
 #define GBBS_PULL_STEPS 2
 #endif
