@@ -390,6 +390,7 @@ def run_ours(args, rank, world, local):
                                            else None),
                          "peak_source": peak_src, "copy_gbs_same_run": round(copy_gbs, 1),
                          "frac_of_copy_same_run": round(achieved / copy_gbs, 4),
+                         "frac_of_nominal_8tbs": round(achieved / 8000.0, 4),
                          "kernel": kname, "teams": teams,
                          "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": round(step_ms, 4),
                          "single_traversal_kernel_ms_per_step": round(kernel_ms, 4),
@@ -405,6 +406,9 @@ def run_ours(args, rank, world, local):
                     "note": "gbbs_bfs_batch (one call per step) into pinned host dist/parent "
                             "rows; the library's D2H copy of traversal i overlaps traversal i+1; "
                             "h2d = the source ids (host array, passed as kernel arguments)"},
+            # Graph500-style undirected TEPS (m_reach / 2) on symmetric graphs
+            "graph500_undirected_gteps": (round(edges_job / 2 / (step_ms * 1e-3) / 1e9, 3)
+                                          if cfg.symmetric else None),
             "gpu_launches": args.steps * launches,
             "clocks": clocks,
             "per_source": [{"src": s, **per_src[(args.algo, s)]} for s in sources],

@@ -1,6 +1,6 @@
 """All BASELINE configs x algorithms on one B200 (dev/report tool, not the bench):
 per source the kernel time (CUDA events around the persistent launch, L2 flushed
-before each timed call, median of 3), GTEPS (reading A20), the contract's
+before each timed call, median of 5 after a warm-up call; all samples kept), GTEPS (reading A20), the contract's
 roofline fraction (algorithmic bytes / time / measured peak, bench.algorithmic_bytes)
 and the edge-traffic fraction (4 B per reached edge, reading A21b).
 python tools/results_table.py [c1,c2,c3,c4,c5] > profiles/r01_results_all_configs.json"""
@@ -56,7 +56,7 @@ def main():
                 reach = int((off[1:] - off[:-1])[(d != 0) if base == "wp" else (d != -1)].sum())
                 relax = sum(r["edges_examined"] for r in recs)
                 ts = []
-                for _ in range(3):
+                for _ in range(5):
                     flush.fill_(1)
                     s2 = gbbs.make_stats(0)
                     call(s, s2)
@@ -65,9 +65,14 @@ def main():
                 row = {"config": name, "algo": algo, "src": s, "ms": round(ms, 3),
                        "rounds": st.rounds, "m_reach": reach,
                        "gteps": round(reach / (ms * 1e-3) / 1e9, 2),
+                       # Graph500-style undirected TEPS on symmetric graphs
+                       "gteps_undirected": (round(reach / 2 / (ms * 1e-3) / 1e9, 2)
+                                            if G["symmetric"] else None),
+                       "samples_ms": [round(x, 4) for x in ts],
                        "relax_per_s_G": round(relax / (ms * 1e-3) / 1e9, 2),
                        "alg_GBps": round(alg / (ms * 1e-3) / 1e9, 1),
                        "roofline_frac": round(alg / (ms * 1e-3) / 1e9 / peak, 4),
+                       "roofline_frac_nominal_8TBs": round(alg / (ms * 1e-3) / 1e9 / 8000.0, 4),
                        "edge_traffic_frac": round(4 * reach / (ms * 1e-3) / 1e9 / peak, 4)}
                 rows.append(row)
                 print(json.dumps(row), flush=True)
