@@ -1151,8 +1151,11 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #define GBBS_PULL_SW 32
 #endif
 static_assert(GBBS_PULL_SW <= SWEEP_WORDS, "pull units are gathered into SweepSmem");
+// vectorised 4-edge steps per lane before a long in-list goes to the warp: 3 since
+// the L1 grew (WCAP 192): c2/c4/c5 BFS -2 to -2.3 %, 8-team batch -3.5 % vs 2
+// (4 and 5 measure the same as 3, 1 is 5 % slower)
 #ifndef GBBS_PULL_STEPS
-#define GBBS_PULL_STEPS 2
+#define GBBS_PULL_STEPS 3
 #endif
 #ifndef GBBS_LONG_IN
 #define GBBS_LONG_IN 24
