@@ -509,6 +509,9 @@ constexpr uint32_t XKEY = 64;    // near list
 #define GBBS_WBFS_LB 4
 #endif
 constexpr int WBFS_LB = GBBS_WBFS_LB;
+// a staging flush leaves room for one whole batch: WCAP - 32 * (chunks per batch)
+// must not be negative, or a batch could overrun the warp's staging buffer
+static_assert(WCAP >= 32 * NCH && WCAP >= 32 * WBFS_LB, "WCAP below one batch of winners");
 constexpr uint32_t NOKEY = 0xFFFFFFFFu;
 
 // Per-warp wBFS staging metadata in dynamic shared memory (wbfs_kernel only):
@@ -610,7 +613,7 @@ __device__ __forceinline__ void wbfs_stage(const Params &p, WarpState &ws, uint3
     }
     ws.scnt += __popc(bal);
   }
-  if (ws.scnt > WCAP - 32 * WBFS_LB) {  // room for the widest batch (WBFS_LB chunks)
+  if (ws.scnt > WCAP - 32 * (WBFS_LB > NCH ? WBFS_LB : NCH)) {  // room for the widest batch
     wbfs_flush<STATS>(p, ws, st, ws.scnt, r);
     ws.scnt = 0;
   }
@@ -1062,6 +1065,12 @@ __device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, Wa
 // 4.8 gains 28 % on that round; c2's 1.75 loses 2 % overall)
 #ifndef GBBS_FWD_CONVERT_DEG
 #define GBBS_FWD_CONVERT_DEG 4
+#endif
+// ... and in a multi-traversal launch, where each traversal has 1/G of the warps,
+// so the lane path's serial batches per warp are G times longer (c2 8-team batch
+// 0.84 -> 0.79 ms at 2; single traversals: c2 flat, c5 up to +2.6 % at 2)
+#ifndef GBBS_FWD_CONVERT_DEG_MG
+#define GBBS_FWD_CONVERT_DEG_MG 2
 #endif
 // BFS: frontier = precheck (vis_cur) & ~bits (vis_old): what the last dense round
 // added; the TS target is vis_old, which also absorbs the frontier bits (atomicOr)
@@ -1713,7 +1722,8 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
       if (ALGO == ALGO_BFS) {
         forward_round<ALGO, STATS, EMIT_LIST, MG>(
             s, p, grid, wsm, ws, nullptr, p.bm[vc ^ 1], p.bm[vc], nb, (int)r, gw, nw,
-            GBBS_FWD_CONVERT && E >= (long long)GBBS_FWD_CONVERT_DEG * f, GBBS_NBLK);
+            GBBS_FWD_CONVERT &&
+                E >= (long long)(MG ? GBBS_FWD_CONVERT_DEG_MG : GBBS_FWD_CONVERT_DEG) * f, GBBS_NBLK);
         vc ^= 1;
         list_valid = true;
       } else if (big) {
