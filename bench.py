@@ -3,13 +3,15 @@
 
 Contract (task README + DESIGN.md §Measurement):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2] [--algo bfs|bf]
+                  [--workload c5] [--bf-workload c4] [--algo bfs|bf]
 One step = one pass of the hot path over the workload's batch: BFS (direction-
 optimising, T=20) from each of the config's seeded sources on the resident graph
-(default c2: 8 sources in the largest component of the medium rMAT graph), issued
-as one gbbs_bfs_batch call into device rows.  The
-Bellman-Ford leg of the metric is measured in the same run on the same graph with
-weights in [1, floor(log2 n)] (reading A6) and reported under "bellman_ford".
+(default c5, the largest single-GPU config: 8 sources with out-degree >= 1 on the
+directed 2^26-vertex rMAT graph), issued as one gbbs_bfs_batch call into device
+rows.  The Bellman-Ford leg of the metric is measured in the same run on c4 (BJ's
+atomicMin config: 4 seeded LCC sources, weights in [1, 25], reading A6) and
+reported under "bellman_ford", beside the NEXT rows on the same graph and a c2 BFS
+leg.
 Multi-GPU: every rank holds its own copy of the graph and
 traverses its own shard of the source sample (rank r: sources 8r .. 8r+7 of the
 config's sequential seeded sample, so rank 0's are the N=1 sources; configs with
@@ -41,12 +43,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default="c5",
+                    help="headline config (default c5: the largest single-GPU config, BJ's "
+                         "large rMAT direction-optimising BFS)")
     ap.add_argument("--algo", default="bfs", choices=["bfs", "bf"])
+    ap.add_argument("--bf-workload", default="c4",
+                    help="config of the Bellman-Ford leg (default c4: BJ's atomicMin config)")
     ap.add_argument("--threshold", type=int, default=20)
-    ap.add_argument("--no-bf-leg", action="store_true")
+    ap.add_argument("--rules", type=int, default=0, help="gbbs_opts.rules (1 = paper's m/T only)")
+    ap.add_argument("--no-legs", action="store_true", help="headline only (no BF / NEXT / c2 legs)")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
-    ap.add_argument("--profile", action="store_true", help="short run for ncu (no cpu baseline)")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no legs, no cpu baseline)")
     return ap.parse_args()
 
 
@@ -134,32 +141,20 @@ def copy_bandwidth(torch):
 
 
 def algorithmic_bytes(recs, n, m, algo):
-    """SURVEY §8(d) algorithmic bytes of offsets + targets + weights + frontier, per
-    traversal, from the per-round records:
-      list push   : frontier entries read 20 B (v 4 + O 8 + base 8), targets 4 B/edge
-                    (+ weights 4 B/edge for BF), each emitted vertex 16 B of offsets
-                    read + 20 B entry written;
-      dense pull  : in-offsets 8 B per swept vertex + 8, in-edges 4 B per edge loaded,
-                    visited bitmap n/8 read + n/8 written;
-      bitmap fwd  : frontier bitmap(s) swept (n/8, x2 for BFS), offsets 16 B per
-                    frontier vertex, targets (+weights) per edge, emitted entries;
-      wBFS bucket : 24 B per bucket entry swept (id, dist, two offsets), 8 B per
-                    edge (target + weight), 4 B per insertion.
-    Probes of the L2-resident bitmaps and dist/parent state are not counted (state
-    bytes are returned separately)."""
-    alg = 0
-    wb = (n + 7) // 8
-    per_edge = 4 if algo == "bfs" else 8
-    for r in recs:
-        emit = 36 * r["acquired"]
-        if r["dense"] == 1:
-            alg += 8 * r["vertices_swept"] + 8 + 4 * r["edges_examined"] + 2 * wb
-        elif r["dense"] in (3, 4):  # wBFS bucket round: entry id + dist + offsets, edges, inserts
-            alg += 24 * r["vertices_swept"] + 8 * r["edges_examined"] + 4 * r["acquired"]
-        elif r["dense"] == 2:
-            alg += (2 if algo == "bfs" else 1) * wb + 16 * r["vertices_swept"] + per_edge * r["edges_examined"] + emit
-        else:
-            alg += 20 * r["frontier"] + per_edge * r["frontier_edges"] + emit
+    """SURVEY §8(d) algorithmic bytes of one traversal: offsets (and per-vertex pull
+    records), targets, weights and frontier (lists and bitmap words), at the
+    granularity the kernels load them — a 16-byte in-edge vector load counts 16 B
+    even after an early exit.  BFS / Bellman-Ford / widest path: the kernels' own
+    counters (gbbs_round_stat.alg_bytes, summed by the STATS instantiation at every
+    load site).  wBFS has no counters: 24 B per bucket entry swept (id, dist, two
+    offsets), 8 B per edge (target + weight), 4 B per insertion.  Probes of the
+    L2-resident bitmaps and the dist / parent state are not counted; the state
+    bytes (per-run init) are returned separately."""
+    if algo in ("bfs", "bf", "wp"):
+        alg = sum(r["alg_bytes"] for r in recs)
+    else:
+        alg = sum(24 * r["vertices_swept"] + 8 * r["edges_examined"] + 4 * r["acquired"]
+                  for r in recs)
     state = 8 * n if algo == "bfs" else 4 * n
     return alg, state
 
@@ -220,6 +215,7 @@ def shard_sources(sources, rank, world, per_rank):
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist_mod
+    from graphgen import CONFIGS
     from graphgen import device as gdev
     from paper_1805_05208_b200 import gbbs
 
@@ -227,70 +223,75 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     if world > 1:
         dist_mod.init_process_group("nccl", device_id=dev)
-
-    t0 = time.time()
-    want_w = (args.algo == "bf") or not args.no_bf_leg
-    from graphgen import CONFIGS
-    per_rank = CONFIGS[args.workload].nsources
-    G = gdev.build_config(args.workload, weights=want_w, nsources=per_rank * world)
-    cfg = G["cfg"]
-    n, m = G["n"], G["m"]
-    g = gbbs.Graph(G["offsets"], G["targets"], G["weights"], symmetric=G["symmetric"])
-    setup_s = time.time() - t0
-    sources = shard_sources(G["sources"], rank, world, per_rank)
-    off = G["offsets"]
-    dist = torch.empty(n, dtype=torch.int32, device=dev)
-    par = torch.empty(n, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    opts = gbbs.make_opts(args.threshold, gbbs.GBBS_MODE_AUTO)
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    peak, peak_src = measured_peaks()
 
-    def one(src, algo, stats=None):
+    def load(name, weights):
+        t0 = time.time()
+        per_rank = CONFIGS[name].nsources
+        G = gdev.build_config(name, weights=weights, nsources=per_rank * world)
+        G["g"] = gbbs.Graph(G["offsets"], G["targets"], G["weights"], symmetric=G["symmetric"])
+        G["mine"] = shard_sources(G["sources"], rank, world, per_rank)
+        G["setup_s"] = round(time.time() - t0, 2)
+        return G
+
+    def drop(G):
+        G["g"].close()
+        G.clear()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+    def one(G, algo, src, dist, par, opts=None, stats=None):
+        g = G["g"]
         if algo == "bfs":
             g.bfs(src, dist, par, stream=stream, opts=opts, stats=stats)
         elif algo == "bf":
-            g.bellman_ford(src, dist, stream=stream, stats=stats)
+            g.bellman_ford(src, dist, stream=stream, opts=opts, stats=stats)
         elif algo == "wbfs":
-            g.wbfs(src, dist, stream=stream, stats=stats)
+            g.wbfs(src, dist, stream=stream, opts=opts, stats=stats)
         else:
-            g.widest_path(src, dist, stream=stream, stats=stats)
+            g.widest_path(src, dist, stream=stream, opts=opts, stats=stats)
 
-    algos = [args.algo] + (["bf", "wbfs", "wp"] if (want_w and args.algo == "bfs" and not args.profile)
-                           else [])
-    # per-source traversed edges (TEPS numerator, reading A20) and algorithmic bytes
-    per_src = {}
-    for algo in algos:
-        for s in sources:
+    def profile(G, algo, opts):
+        """Per source: TEPS numerator (reading A20), rounds, algorithmic bytes (the
+        kernels' counters, STATS instantiation, untimed) and relaxations."""
+        n, off = G["n"], G["offsets"]
+        dist = torch.empty(n, dtype=torch.int32, device=dev)
+        par = torch.empty_like(dist)
+        out = {}
+        for s in G["mine"]:
             st = gbbs.make_stats(1 << 16)
-            one(s, algo, stats=st)
+            one(G, algo, s, dist, par, opts, st)
             recs = gbbs.round_records(st)
-            alg, state = algorithmic_bytes(recs, n, m, algo)
+            alg, state = algorithmic_bytes(recs, n, G["m"], algo)
             reach = reached_edges(torch, off, dist) if algo != "wp" else \
                 int((off[1:] - off[:-1])[dist != 0].sum())
-            per_src[(algo, s)] = dict(m_reach=reach, rounds=st.rounds,
-                                      dense_rounds=st.dense_rounds, alg_bytes=alg, state_bytes=state,
-                                      relax=sum(r["edges_examined"] for r in recs))
+            out[s] = dict(m_reach=reach, rounds=st.rounds, dense_rounds=st.dense_rounds,
+                          alg_bytes=alg, state_bytes=state,
+                          relax=sum(r["edges_examined"] for r in recs),
+                          kinds="".join("SDFPB"[min(r["dense"], 4)] for r in recs))
+        return out
 
-    # one step = the batch call over this rank's sources into device rows (the k
-    # launches are enqueued back to back, one synchronisation per step); the NEXT
-    # legs use the per-source calls
-    drows = torch.empty((len(sources), n), dtype=torch.int32, device=dev)
-    prows = torch.empty_like(drows) if args.algo == "bfs" else None
+    def timed(G, algo, opts, steps, warmup, rows, prows):
+        """One step = the batch call over this rank's sources into device rows (the
+        launches are enqueued back to back, one synchronisation per step); the step
+        time is the slowest rank's.  Also the kernel-only time summed over sources
+        (CUDA events libgbbs records around each persistent launch)."""
+        srcs = G["mine"]
 
-    def step(algo):
-        if algo == "bfs":
-            g.bfs_batch(sources, drows, prows, stream=stream, opts=opts)
-        elif algo == "bf":
-            g.bellman_ford_batch(sources, drows, stream=stream)
-        elif algo == "wbfs":
-            g.wbfs_batch(sources, drows, stream=stream)
-        else:
-            for s in sources:
-                one(s, algo)
-
-    def timed(algo, steps, warmup):
+        def step():
+            if algo == "bfs":
+                G["g"].bfs_batch(srcs, rows, prows, stream=stream, opts=opts)
+            elif algo == "bf":
+                G["g"].bellman_ford_batch(srcs, rows, stream=stream, opts=opts)
+            elif algo == "wbfs":
+                G["g"].wbfs_batch(srcs, rows, stream=stream, opts=opts)
+            else:
+                for i, s in enumerate(srcs):
+                    one(G, algo, s, rows[i], None, opts)
         for _ in range(warmup):
-            step(algo)
+            step()
         if world > 1:
             dist_mod.barrier()
         torch.cuda.synchronize()
@@ -301,39 +302,48 @@ def run_ours(args, rank, world, local):
             flush_buf.fill_(1)  # L2 flush between timed steps (outside the events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step(algo)
+            step()
             e1.record(stream)
             evs.append((e0, e1))
         torch.cuda.synchronize()
         ck = clocks.stop()
         if world > 1:
             dist_mod.barrier()
-        ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+        ms = float(np.mean([x.elapsed_time(y) for x, y in evs]))
         tmax = replica_max(ms, world, dist_mod, dev)
-        # kernel-only time of the persistent traversal kernel: CUDA events that libgbbs
-        # records on `stream` around its cooperative launch (gbbs_stats.kernel_ms)
         kms = []
-        for s in sources:
+        for i, s in enumerate(srcs):
             flush_buf.fill_(1)
             st = gbbs.make_stats(0)
-            one(s, algo, stats=st)
+            one(G, algo, s, rows[i], prows[i] if prows is not None else None, opts, st)
             kms.append(st.kernel_ms)
         return tmax, ck, float(np.sum(kms))
 
-    res = {algo: timed(algo, args.steps if algo == args.algo else max(2, args.steps // 2),
-                       args.warmup if algo == args.algo else 1) for algo in algos}
-    step_ms, clocks, kernel_ms = res[args.algo]
-    edges_step = sum(per_src[(args.algo, s)]["m_reach"] for s in sources)
-    edges_job = replica_sum(edges_step, world, dist_mod, dev)
-    # every leg's edges summed over ranks (all ranks take part in the reduction)
-    leg_edges = {a: replica_sum(sum(per_src[(a, s)]["m_reach"] for s in sources), world, dist_mod, dev)
-                 for a in algos}
-    value = replica_value(edges_job, step_ms)
+    def leg(G, algo, opts, steps, warmup, with_parent=False):
+        per = profile(G, algo, opts)
+        rows = torch.empty((len(G["mine"]), G["n"]), dtype=torch.int32, device=dev)
+        prows = torch.empty_like(rows) if with_parent else None
+        t, ck, kms = timed(G, algo, opts, steps, warmup, rows, prows)
+        edges = replica_sum(sum(v["m_reach"] for v in per.values()), world, dist_mod, dev)
+        alg = sum(v["alg_bytes"] for v in per.values())
+        del rows, prows
+        return dict(per=per, ms=t, clocks=ck, kernel_ms=kms, edges=edges, alg=alg,
+                    value=replica_value(edges, t))
 
-    # e2e: the public batch API with pinned host output rows on every rank: one
-    # gbbs_bfs_batch call per step, whose device->host copies of dist/parent
-    # (8n bytes per source) overlap the next traversal (sources are a host
-    # array); the step time is the slowest rank's (median over steps)
+    # ---- headline: c5 direction-optimising BFS (default) --------------------------
+    H = load(args.workload, weights=args.algo == "bf")
+    cfg, n, m = H["cfg"], H["n"], H["m"]
+    sources = H["mine"]
+    opts = gbbs.make_opts(args.threshold, gbbs.GBBS_MODE_AUTO, rules=args.rules)
+    hl = leg(H, args.algo, opts, args.steps, args.warmup, with_parent=args.algo == "bfs")
+    step_ms, clocks, kernel_ms = hl["ms"], hl["clocks"], hl["kernel_ms"]
+    per_src, edges_job, alg_bytes = hl["per"], hl["edges"], hl["alg"]
+    edges_step = sum(v["m_reach"] for v in per_src.values())
+    value = hl["value"]
+
+    # e2e: the public batch API with pinned host output rows: one gbbs_bfs_batch call
+    # per step, whose device->host copies of dist/parent (8n bytes per source)
+    # overlap the next traversal (sources are a host array)
     hd = torch.empty((len(sources), n), dtype=torch.int32, pin_memory=True)
     hp = torch.empty((len(sources), n), dtype=torch.int32, pin_memory=True)
     hdn, hpn = hd.numpy(), hp.numpy()
@@ -344,26 +354,23 @@ def run_ours(args, rank, world, local):
             dist_mod.barrier()
         t = time.perf_counter()
         if args.algo == "bfs":
-            gbbs.gbbs_bfs_batch(g.handle, sources, hdn, hpn, stream=stream)
+            gbbs.gbbs_bfs_batch(H["g"].handle, sources, hdn, hpn, stream=stream, opts=opts)
         else:
-            gbbs.gbbs_bellman_ford_batch(g.handle, sources, hdn, stream=stream)
+            gbbs.gbbs_bellman_ford_batch(H["g"].handle, sources, hdn, stream=stream)
         e2e.append(replica_max(time.perf_counter() - t, world, dist_mod, dev))
     e2e_s = float(np.median(e2e))
+    del hd, hp, hdn, hpn
 
+    teams = min(8, len(sources)) if (args.algo == "bfs" and n <= (1 << 24) and m <= (1 << 28)) else 1
+    launches = -(-len(sources) // teams)
     out = None
     if rank == 0:
-        peak, peak_src = measured_peaks()
         copy_gbs = copy_bandwidth(torch)
-        alg_bytes = sum(per_src[(args.algo, s)]["alg_bytes"] for s in sources)
-        # the step's launches: G traversals each (gbbs_opts.teams auto rule, gbbs.h)
-        teams = min(8, len(sources)) if (args.algo == "bfs" and n <= (1 << 24)
-                                         and m <= (1 << 28)) else 1
-        launches = -(-len(sources) // teams)
         kname = ("gbbs_dev::traverse_mg_kernel<BFS> (persistent; %d traversals per launch, "
                  "%d launches per step)" % (teams, launches)) if teams > 1 else \
-            "gbbs_dev::traverse_kernel (persistent; one launch per traversal)"
-        # achieved = algorithmic bytes of the step / the step's device time (CUDA events
-        # around exactly those launches on their stream)
+            "gbbs_dev::traverse_kernel<%s> (persistent; one launch per traversal)" % args.algo.upper()
+        # achieved = algorithmic bytes of the step (kernel counters) / the step's device
+        # time (CUDA events around exactly those launches on their stream)
         achieved = alg_bytes / (step_ms * 1e-3) / 1e9
         traffic = ncu_traffic(cfg.name, args.algo)
         d2h = len(sources) * n * (8 if args.algo == "bfs" else 4)
@@ -375,19 +382,16 @@ def run_ours(args, rank, world, local):
             "data": "synthetic (seeded counter-based rMAT/torus generators, DESIGN.md §Input recipe)",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "algo": args.algo,
                        "n": n, "m": m, "sources": sources, "threshold_T": args.threshold,
-                       "traversals_per_step": len(sources), "edges_per_step": edges_step,
+                       "rules": args.rules, "traversals_per_step": len(sources),
+                       "edges_per_step": edges_step,
                        "l2": "flushed (256 MB write) before every timed step; graph > L2",
                        "parallelism": f"source-sharded replicas x{world}",
                        "edges_per_step_all_ranks": edges_job},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "traffic_unit": "bytes per launch of the kernel below",
-                         # context: the DRAM utilisation ncu measured for that launch
-                         # (cold-cache, serialised replay; its duration, not this run's)
-                         "ncu_dram_frac": (round(traffic / (ncu_traffic(cfg.name, args.algo, "us")
-                                                           * 1e-6) / 1e9 / peak, 4)
-                                           if traffic and ncu_traffic(cfg.name, args.algo, "us")
-                                           else None),
+                         "traffic_vs_alg_bytes": (round(traffic / (alg_bytes / len(sources)), 3)
+                                                  if traffic else None),
                          "peak_source": peak_src, "copy_gbs_same_run": round(copy_gbs, 1),
                          "frac_of_copy_same_run": round(achieved / copy_gbs, 4),
                          "frac_of_nominal_8tbs": round(achieved / 8000.0, 4),
@@ -395,82 +399,99 @@ def run_ours(args, rank, world, local):
                          "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": round(step_ms, 4),
                          "single_traversal_kernel_ms_per_step": round(kernel_ms, 4),
                          "single_traversal_gteps": round(edges_step / (kernel_ms * 1e-3) / 1e9, 3),
-                         # reading A21b: the edge-traffic roofline of a BFS is
-                         # 4 B per reached edge at peak; a direction-optimising BFS that
-                         # skips edges can exceed it (frac > 1)
-                         "edge_traffic": {"bytes_per_edge": 4,
-                                          "achieved": round(4 * edges_step / (step_ms * 1e-3) / 1e9, 1),
-                                          "frac": round(4 * edges_step / (step_ms * 1e-3) / 1e9 / peak, 4)}},
+                         # context only, not the gate: 4 B per reached edge at peak (a
+                         # dense-equivalent count; an early-exit pull never reads most
+                         # of those bytes, so this can exceed 1)
+                         "dense_equivalent_context": {
+                             "bytes_per_reached_edge": 4,
+                             "frac": round(4 * edges_step / (step_ms * 1e-3) / 1e9 / peak, 4)}},
             "e2e": {"value": round(edges_job / e2e_s / 1e9, 3), "unit": "GTEPS",
                     "h2d_bytes_per_step": 4 * len(sources) * world, "d2h_bytes_per_step": d2h * world,
                     "note": "gbbs_bfs_batch (one call per step) into pinned host dist/parent "
                             "rows; the library's D2H copy of traversal i overlaps traversal i+1; "
                             "h2d = the source ids (host array, passed as kernel arguments)"},
-            # Graph500-style undirected TEPS (m_reach / 2) on symmetric graphs
             "graph500_undirected_gteps": (round(edges_job / 2 / (step_ms * 1e-3) / 1e9, 3)
                                           if cfg.symmetric else None),
             "gpu_launches": args.steps * launches,
             "clocks": clocks,
-            "per_source": [{"src": s, **per_src[(args.algo, s)]} for s in sources],
-            "setup_s": round(setup_s, 2),
+            "per_source": [{"src": s, **per_src[s]} for s in sources],
+            "setup_s": H["setup_s"],
         }
-        if "bf" in algos and args.algo == "bfs":
-            bt, bclk, bkms = res["bf"]
-            be = leg_edges["bf"]
-            brel = sum(per_src[("bf", s)]["relax"] for s in sources)
-            balg = sum(per_src[("bf", s)]["alg_bytes"] for s in sources)
-            out["bellman_ford"] = {
-                "value": round(be / (bt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective, reading A20)",
-                "relaxations_per_s_G": round(brel / (bt * 1e-3) / 1e9, 3), "ms_per_step": round(bt, 4),
-                "weights": f"[1,{cfg.W}] pair-hash (readings A5, A6)",
-                "roofline_frac": round(balg / (bkms * 1e-3) / 1e9 / peak, 4),
-                # every relaxation probes the 16-bit distance shadow at a random address;
-                # tools/gather_bench.cu measured 270 G random 2-byte L2 gathers/s and
-                # 110 G random atomicMin/s on this B200 (profiles/r01_gather_bench.txt)
-                "relax_vs_l2_gather_ceiling": round(brel / (bkms * 1e-3) / 1e9 / 270.0, 4),
-                "kernel_ms_per_step": round(bkms, 4), "clocks": bclk,
-                "rounds": [per_src[("bf", s)]["rounds"] for s in sources]}
-        if "wbfs" in algos and args.algo == "bfs":
-            wt, wclk, wkms = res["wbfs"]
-            we = leg_edges["wbfs"]
-            out["wbfs"] = {
-                "value": round(we / (wt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective)",
-                "ms_per_step": round(wt, 4), "kernel_ms_per_step": round(wkms, 4),
-                "note": "NEXT-2: integral-weight SSSP over distance buckets (bucket width 1), "
-                        "same graph and weights as the Bellman-Ford leg; one gbbs_wbfs_batch call "
-                        "per step (teams of traversals per launch)",
-                "rounds": [per_src[("wbfs", s)]["rounds"] for s in sources]}
-        if "wp" in algos and args.algo == "bfs":
-            wt, wclk, wkms = res["wp"]
-            we = leg_edges["wp"]
-            walg = sum(per_src[("wp", s)]["alg_bytes"] for s in sources)
-            out["widest_path"] = {
-                "value": round(we / (wt * 1e-3) / 1e9, 3), "unit": "GTEPS (effective)",
-                "ms_per_step": round(wt, 4), "kernel_ms_per_step": round(wkms, 4),
-                "roofline_frac": round(walg / (wkms * 1e-3) / 1e9 / peak, 4),
-                "note": "NEXT-1: Bellman-Ford over the (max, min) semiring, same graph and weights",
-                "rounds": [per_src[("wp", s)]["rounds"] for s in sources]}
-        if want_w and args.algo == "bfs" and not args.profile:
-            # NEXT-3: single-source betweenness on the same graph (8 sources per step)
-            delta = torch.empty((len(sources), n), dtype=torch.float64, device=dev)
-            g.betweenness_batch(sources[:2], delta[:2], stream=stream)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            flush_buf.fill_(1)
-            e0.record(stream)
-            g.betweenness_batch(sources, delta, stream=stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            bt = e0.elapsed_time(e1)
-            out["betweenness"] = {
-                "value": round(edges_step / (bt * 1e-3) / 1e9, 3),
-                "unit": "GTEPS (m_reach of the BFS per source / time; rank 0's shard)",
-                "ms_per_step": round(bt, 4),
-                "note": "NEXT-3: Brandes dependencies, forward CAS + fp64 fetch-and-add, backward per "
-                        "level; one gbbs_betweenness_batch call into device rows"}
         if not args.profile:
-            out["cpu_baseline"] = cpu_baseline(args, G["offsets"], G["targets"], sources, cfg)
-    g.close()
+            out["cpu_baseline"] = cpu_baseline(args, H["offsets"], H["targets"], sources, cfg)
+    drop(H)
+    if args.no_legs or args.profile:
+        if world > 1:
+            dist_mod.destroy_process_group()
+        return out
+
+    # ---- legs: Bellman-Ford (the metric's second half) + NEXT rows on c4 ------------
+    B = load(args.bf_workload, weights=True)
+    bcfg = B["cfg"]
+    legs = {}
+    for algo, key in (("bf", "bellman_ford"), ("wbfs", "wbfs"), ("wp", "widest_path")):
+        r = leg(B, algo, None, max(2, args.steps // 2), 1)
+        legs[key] = r
+    # NEXT-3: single-source betweenness on the same graph, this rank's sources per step
+    srcs = B["mine"]
+    delta = torch.empty((len(srcs), B["n"]), dtype=torch.float64, device=dev)
+    B["g"].betweenness_batch(srcs[:1], delta[:1], stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush_buf.fill_(1)
+    e0.record(stream)
+    B["g"].betweenness_batch(srcs, delta, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    bc_ms = replica_max(e0.elapsed_time(e1), world, dist_mod, dev)
+    bc_edges = legs["bellman_ford"]["edges"]
+    del delta
+    bsrc = B["mine"]
+    drop(B)
+    # ---- leg: c2 BFS (the medium config; teams of traversals per launch) -------------
+    C = load("c2", weights=False)
+    c2 = leg(C, "bfs", opts, args.steps, args.warmup, with_parent=True)
+    c2src = C["mine"]
+    drop(C)
+
+    if rank == 0:
+        bf = legs["bellman_ford"]
+        bf_relax = sum(v["relax"] for v in bf["per"].values())
+        out["bellman_ford"] = {
+            "workload": f"{bcfg.name}: {bcfg.note}", "sources": bsrc,
+            "value": round(bf["value"], 3), "unit": "GTEPS (effective, reading A20)",
+            "relaxations_per_s_G": round(bf_relax / (bf["ms"] * 1e-3) / 1e9, 3),
+            "ms_per_step": round(bf["ms"], 4), "kernel_ms_per_step": round(bf["kernel_ms"], 4),
+            "weights": f"[1,{bcfg.W}] pair-hash (readings A5, A6)",
+            "alg_bytes_per_step": bf["alg"],
+            "roofline_frac": round(bf["alg"] / (bf["kernel_ms"] * 1e-3) / 1e9 / peak, 4),
+            # every relaxation probes the 16-bit distance shadow at a random address;
+            # tools/gather_bench.cu measured 270 G random 2-byte L2 gathers/s on this B200
+            "relax_vs_l2_gather_ceiling": round(bf_relax / (bf["kernel_ms"] * 1e-3) / 1e9 / 270.0, 4),
+            "clocks": bf["clocks"], "rounds": [v["rounds"] for v in bf["per"].values()]}
+        for key, note in (("wbfs", "NEXT-2: integral-weight SSSP over distance buckets (bucket width "
+                                   "1), same graph and weights as the Bellman-Ford leg"),
+                          ("widest_path", "NEXT-1: Bellman-Ford over the (max, min) semiring, same "
+                                          "graph and weights")):
+            r = legs[key]
+            out[key] = {"value": round(r["value"], 3), "unit": "GTEPS (effective)",
+                        "ms_per_step": round(r["ms"], 4), "kernel_ms_per_step": round(r["kernel_ms"], 4),
+                        "roofline_frac": round(r["alg"] / (r["kernel_ms"] * 1e-3) / 1e9 / peak, 4),
+                        "note": note, "rounds": [v["rounds"] for v in r["per"].values()]}
+        out["betweenness"] = {
+            "value": round(bc_edges / (bc_ms * 1e-3) / 1e9, 3),
+            "unit": "GTEPS (m_reach of the BFS per source / time)", "ms_per_step": round(bc_ms, 4),
+            "note": "NEXT-3: Brandes dependencies on the Bellman-Ford leg's graph and sources, one "
+                    "gbbs_betweenness_batch call into device rows"}
+        out["c2_bfs"] = {
+            "workload": "c2: " + CONFIGS["c2"].note, "sources": c2src,
+            "value": round(c2["value"], 3), "unit": "GTEPS",
+            "graph500_undirected_gteps": round(c2["edges"] / 2 / (c2["ms"] * 1e-3) / 1e9, 3),
+            "ms_per_step": round(c2["ms"], 4),
+            "roofline_frac": round(c2["alg"] / (c2["ms"] * 1e-3) / 1e9 / peak, 4),
+            "note": "the medium config: one gbbs_bfs_batch call per step (8 traversals as teams "
+                    "of one cooperative launch)",
+            "rounds": [v["rounds"] for v in c2["per"].values()]}
     if world > 1:
         dist_mod.destroy_process_group()
     return out

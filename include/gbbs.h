@@ -153,10 +153,14 @@ int gbbs_bellman_ford_batch(const gbbs_graph *g, const uint32_t *srcs,
  * dist    uint32[n], caller-owned, host or device: shortest weighted
  *         distance from src, GBBS_INF if unreachable.
  * Same stream/synchronization/error conventions as gbbs_bfs, plus
- * GBBS_ERANGE if some relaxation candidate d(u) + w reached 2^32 - 1 (the
- * distances do not fit below the uint32 sentinel; detected during the run,
- * dist is then incomplete), and GBBS_EINTERNAL if more than n+1 rounds run
- * (impossible with w >= 0).
+ * GBBS_ERANGE iff some reachable vertex's shortest distance is >= 2^32 - 1
+ * (it does not fit below the uint32 sentinel): candidates d(u) + w reaching
+ * 2^32 - 1 are dropped as "no improvement" during the run, so every finite
+ * distance returned is exact; when the run dropped one, an O(m) check after
+ * it returns GBBS_ERANGE only if an edge (u, v) has finite d(u),
+ * d(u) + w >= 2^32 - 1 and d(v) = GBBS_INF (dist then holds the exact finite
+ * distances and GBBS_INF for the vertices that do not fit).  GBBS_EINTERNAL
+ * if more than n+1 rounds run (impossible with w >= 0).
  */
 int gbbs_bellman_ford(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                       void *cuda_stream);
@@ -278,7 +282,11 @@ int gbbs_betweenness_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
 
 /* Representation choice per round (threshold rule reading A10).
  * BFS AUTO: a round is dense (pull over in-edges, early exit) iff
- *   |U| + sum_{u in U} outdeg(u) > m / T, else sparse (push).
+ *   |U| + sum_{u in U} outdeg(u) > m / T (reading A10), or —
+ *   reading A10b, unless gbbs_opts.rules has GBBS_RULE_PAPER_ONLY — the
+ *   previous round was dense (the frontier is a bitmap) and the pull's
+ *   remaining work, the vertices with in-edges not yet visited, is at most
+ *   |U| + sum deg(U); else sparse (push).
  * Bellman-Ford AUTO: always list push; DENSE forces the bitmap-forward push
  *   (the frontier as a bitmap, reading A11), kept as the measured alternative. */
 #define GBBS_MODE_AUTO 0
@@ -322,8 +330,13 @@ typedef struct {
                              Teams 1-7 allocate their own scratch (~60n
                              bytes of lists each) on first use.  Other
                              calls ignore it.                              */
-  uint32_t reserved[1];   /* must be zero                                  */
+  uint32_t rules;         /* direction-rule flags: GBBS_RULE_PAPER_ONLY
+                             (BFS AUTO takes the paper's m/T test alone,
+                             without reading A10b's stay-dense test).
+                             Other bits must be zero.                      */
 } gbbs_opts;
+
+#define GBBS_RULE_PAPER_ONLY 0x1
 
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */
 typedef struct {
@@ -343,6 +356,14 @@ typedef struct {
                              end time when rounds_cap allows             */
   int64_t t_work_ns;      /* latest end of edge work over all CTAs      */
   int64_t t_flush_ns;     /* latest end of the final flush over all CTAs */
+  int64_t alg_bytes;      /* algorithmic bytes the round loaded or stored
+                             at the granularity of its loads:
+                             offsets and per-vertex pull records, targets,
+                             weights, frontier lists and bitmap words
+                             swept; probes of the L2-resident bitmaps and
+                             dist / parent state are not counted          */
+  int64_t head_hits;      /* dense pull: vertices acquired by their first
+                             in-edge (the inline record, no in-list load) */
 } gbbs_round_stat;
 
 typedef struct {
@@ -363,7 +384,7 @@ void gbbs_default_opts(gbbs_opts *o);
 /* As gbbs_bfs / gbbs_bellman_ford with options (NULL = defaults) and optional
  * statistics (NULL = none).  Collecting per-round records adds counters to
  * the kernels; do not time runs that collect them.  GBBS_EINVAL also for a
- * bad mode or nonzero reserved fields. */
+ * bad mode or unknown rules bits. */
 int gbbs_bfs_ex(const gbbs_graph *g, uint32_t src, uint32_t *dist,
                 uint32_t *parent, void *cuda_stream, const gbbs_opts *opts,
                 gbbs_stats *stats);

@@ -50,6 +50,10 @@ extern "C" const char *gbbs_last_error(void) { return g_last_error.c_str(); }
 // ---------------------------------------------------------------------------
 // the handle
 // ---------------------------------------------------------------------------
+// control words per traversal scratch: packed counter ring [4], status, rounds,
+// count, -, heavy-list counters [2], work queues [8], acquisition ring [4]
+constexpr int CNT_WORDS = 22;
+
 struct gbbs_graph {
   int device = 0;
   long long n = 0, m = 0;
@@ -60,7 +64,9 @@ struct gbbs_graph {
   uint32_t *tgt = nullptr;
   uint32_t *wgt = nullptr;
   bool own_off = true, own_tgt = true, own_wgt = true;
-  uint32_t *odeg = nullptr;  // out-degrees, directed graphs only
+  uint2 *pin = nullptr;      // pull records (first in-neighbour, out-degree)
+  uint32_t *nin = nullptr;   // no-in-edge mask (+ padding)
+  long long ncand = 0;       // vertices with at least one in-edge
   uint16_t *shadow = nullptr;  // 16-bit distance shadow (BF / widest path)
   long long *in_off = nullptr;  // alias of off when symmetric
   uint32_t *in_tgt = nullptr;
@@ -98,6 +104,29 @@ struct gbbs_graph {
   int sgrid[2] = {0, 0};
 };
 
+// Every entry point that touches a handle runs on the handle's device and restores
+// the caller's current device on return (PyTorch and other callers keep theirs).
+struct DeviceGuard {
+  int prev = -1;
+  int rc = GBBS_OK;
+  explicit DeviceGuard(int want) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+    if (prev != want) {
+      const cudaError_t e = cudaSetDevice(want);
+      if (e != cudaSuccess) rc = fail(GBBS_ECUDA, "cudaSetDevice(%d): %s", want, cudaGetErrorString(e));
+    }
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard &) = delete;
+  DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+
 static void free_bc(gbbs_graph *g);
 static void free_wbfs(gbbs_graph *g);
 static void free_teams(gbbs_graph *g);
@@ -107,7 +136,8 @@ static void free_graph(gbbs_graph *g) {
   if (g->own_off) cudaFree(g->off);
   if (g->own_tgt) cudaFree(g->tgt);
   if (g->own_wgt) cudaFree(g->wgt);
-  cudaFree(g->odeg);
+  cudaFree(g->pin);
+  cudaFree(g->nin);
   cudaFree(g->shadow);
   if (g->in_off && g->in_off != g->off) cudaFree(g->in_off);
   if (g->in_tgt && g->in_tgt != g->tgt) cudaFree(g->in_tgt);
@@ -237,9 +267,28 @@ __global__ void k_isolated(const long long *off, const long long *in_off, long l
   if ((threadIdx.x & 31) == 0) iso[v >> 5] = b;
 }
 
-__global__ void k_out_degree(const long long *off, long long n, uint32_t *deg) {
+// Pull records and the no-in-edge mask (a8): pin[v] = (first in-neighbour of v
+// in CSC order or INF, out-degree of v saturated to 32 bits); bit v of nin set
+// iff v has no in-edges (or v >= n): such a vertex can never be acquired by a
+// pull, so dense rounds do not sweep it (it cannot be marked visited instead:
+// visited vertices act as the frontier, reading R2).  *ncand counts the others.
+__global__ void k_pull_records(const long long *off, const long long *in_off,
+                               const uint32_t *in_tgt, long long n, long long nwords, uint2 *pin,
+                               uint32_t *nin, unsigned long long *ncand) {
   long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < n) deg[v] = (uint32_t)(off[v + 1] - off[v]);
+  if ((v >> 5) >= nwords) return;
+  bool none = true;
+  if (v < n) {
+    const long long a = in_off[v], b = in_off[v + 1];
+    const long long od = off[v + 1] - off[v];
+    none = a == b;
+    pin[v] = make_uint2(none ? INF : in_tgt[a], (uint32_t)min(od, 0xFFFFFFFFll));
+  }
+  const unsigned bb = __ballot_sync(0xffffffffu, none);
+  if ((threadIdx.x & 31) == 0) {
+    nin[v >> 5] = bb;
+    atomicAdd(ncand, (unsigned long long)(32 - __popc(bb)));
+  }
 }
 
 static int bits_for(unsigned long long x) {  // bits needed to represent x (>= 1)
@@ -404,17 +453,19 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
     CU(cudaMalloc(&g->fo[i], (size_t)n * 8));
     CU(cudaMalloc(&g->fb[i], (size_t)n * 8));
   }
-  if (!(flags & GBBS_SYMMETRIC)) {
-    CU(cudaMalloc(&g->odeg, (size_t)n * 4));
-    k_out_degree<<<(unsigned)((n + 255) / 256), 256>>>(g->off, n, g->odeg);
-    CU(cudaGetLastError());
-  }
   CU(cudaMalloc(&g->shadow, (size_t)n * 2));
   CU(cudaMalloc(&g->iso, (size_t)g->nwords * 4));
   k_isolated<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->in_off, n, g->nwords, g->iso);
   CU(cudaGetLastError());
-  CU(cudaMalloc(&g->cnt, 18 * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8]
-  CU(cudaMemset(g->cnt, 0, 18 * 8));
+  CU(cudaMalloc(&g->cnt, CNT_WORDS * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8], acq[4]
+  CU(cudaMemset(g->cnt, 0, CNT_WORDS * 8));
+  CU(cudaMalloc(&g->pin, (size_t)n * 8));
+  CU(cudaMalloc(&g->nin, (size_t)g->nwords * 4));
+  k_pull_records<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->in_off, g->in_tgt, n,
+                                                                    g->nwords, g->pin, g->nin,
+                                                                    g->cnt + 6);
+  CU(cudaGetLastError());
+  CU(cudaMemcpy(&g->ncand, g->cnt + 6, 8, cudaMemcpyDeviceToHost));
   g->status = (int *)(g->cnt + 4);
   g->rounds = (long long *)(g->cnt + 5);
   g->dcount = g->cnt + 6;
@@ -450,7 +501,11 @@ extern "C" int gbbs_graph_create(int64_t n, int64_t m, const int64_t *offsets,
   return GBBS_OK;
 }
 
-extern "C" void gbbs_graph_destroy(gbbs_graph *g) { free_graph(g); }
+extern "C" void gbbs_graph_destroy(gbbs_graph *g) {
+  if (!g) return;
+  DeviceGuard dguard(g->device);
+  free_graph(g);
+}
 
 extern "C" int gbbs_graph_info(const gbbs_graph *g, int64_t *n, int64_t *m, uint32_t *flags) {
   if (!g) return fail(GBBS_EINVAL, "g is NULL");
@@ -638,8 +693,8 @@ static int parse_opts(const gbbs_opts *opts, OptsKind kind, gbbs_opts &o) {
   if (!opts) return GBBS_OK;
   o = *opts;
   if (o.threshold_den == 0) o.threshold_den = 20;
-  for (int i = 0; i < 1; i++)
-    if (o.reserved[i]) return fail(GBBS_EINVAL, "opts.reserved must be zero");
+  if (o.rules & ~(uint32_t)GBBS_RULE_PAPER_ONLY)
+    return fail(GBBS_EINVAL, "unknown opts.rules bits 0x%x", o.rules);
   const int max_mode = (kind == OPTS_BATCH) ? 2 : 3;
   if (o.mode < 0 || o.mode > max_mode) return fail(GBBS_EINVAL, "bad mode %d", o.mode);
   if (o.bsize && (o.bsize < 32 || o.bsize > (uint32_t)TE || (o.bsize & (o.bsize - 1))))
@@ -659,7 +714,7 @@ struct TeamScratch {
   uint32_t *fv[3] = {nullptr, nullptr, nullptr};
   long long *fo[3] = {nullptr, nullptr, nullptr};
   long long *fb[3] = {nullptr, nullptr, nullptr};
-  unsigned long long *cnt = nullptr;  // same layout as the handle's (18 words)
+  unsigned long long *cnt = nullptr;  // same layout as the handle's (CNT_WORDS words)
   uint16_t *shadow = nullptr;
   unsigned *bar = nullptr;
   // wBFS bucket structure of this team (hv is shared with team 0's)
@@ -721,8 +776,8 @@ static int team_scratch(gbbs_graph *g, int t) {
     CU(cudaMalloc(&x->fo[i], n * 8));
     CU(cudaMalloc(&x->fb[i], n * 8));
   }
-  CU(cudaMalloc(&x->cnt, 18 * 8));
-  CU(cudaMemset(x->cnt, 0, 18 * 8));
+  CU(cudaMalloc(&x->cnt, CNT_WORDS * 8));
+  CU(cudaMemset(x->cnt, 0, CNT_WORDS * 8));
   CU(cudaMalloc(&x->shadow, n * 2));
   CU(cudaMalloc(&x->bar, 8));
   CU(cudaMemset(x->bar, 0, 8));
@@ -752,6 +807,7 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   p.cnt = g->cnt;
   p.hcnt = g->cnt + 8;
   p.wq = g->cnt + 10;
+  p.acq = g->cnt + 18;
   p.status = g->status;
   p.rounds_out = g->rounds;
   p.nwords = g->nwords;
@@ -759,7 +815,10 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   p.max_rounds = g->n + 1;
   p.ebits = g->ebits;
   p.iso = g->iso;
-  p.odeg = g->odeg;
+  p.nin = g->nin;
+  p.pin = g->pin;
+  p.ncand = g->ncand;
+  p.rules = (int)o.rules;
   p.shadow = g->shadow;
   p.symmetric = (g->flags & GBBS_SYMMETRIC) ? 1 : 0;
   p.mode = o.mode;
@@ -786,6 +845,7 @@ static void fill_params_team(gbbs_graph *g, int algo, uint32_t src, uint32_t *dd
   p.cnt = x->cnt;
   p.hcnt = x->cnt + 8;
   p.wq = x->cnt + 10;
+  p.acq = x->cnt + 18;
   p.status = (int *)(x->cnt + 4);
   p.rounds_out = (long long *)(x->cnt + 5);
   p.shadow = x->shadow;
@@ -807,13 +867,53 @@ static int launch_mg(gbbs_graph *g, MultiParams &mp, cudaStream_t st) {
   return GBBS_OK;
 }
 
+// Exact range check (status bit 2: a relaxation candidate d(u) + w reached 2^32 - 1).
+// The kernels drop such a candidate as "no improvement", so every finite distance
+// they return is exact; the true distance of a vertex does not fit the uint32 output
+// iff some edge (u, v) has finite d(u), d(u) + w >= 2^32 - 1 and d(v) = INF.  One
+// warp per source vertex; run only when the kernel raised the flag.
+__global__ void k_range_check(const long long *off, const uint32_t *tgt, const uint32_t *wgt,
+                              long long n, const uint32_t *dist, unsigned long long *bad) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long u = warp; u < n; u += nwarps) {
+    const uint32_t du = dist[u];
+    if (du == INF) continue;
+    for (long long e = off[u] + lane; e < off[u + 1]; e += 32) {
+      const unsigned long long c = (unsigned long long)du + (wgt ? wgt[e] : 1u);
+      if (c >= INF && dist[tgt[e]] == INF) atomicOr(bad, 1ull);
+    }
+  }
+}
+
+// Clears status bit 2 when the check above finds every distance representable.
+// dist: n entries, host or device.
+static int range_recheck(gbbs_graph *g, const uint32_t *dist, cudaStream_t st, int *status) {
+  if (!(*status & 2)) return GBBS_OK;
+  const uint32_t *dd = dist;
+  if (!is_device_ptr(dist)) {
+    if (!g->tmp_dist) CU(cudaMalloc(&g->tmp_dist, (size_t)g->n * 4));
+    CU(cudaMemcpyAsync(g->tmp_dist, dist, (size_t)g->n * 4, cudaMemcpyHostToDevice, st));
+    dd = g->tmp_dist;
+  }
+  CU(cudaMemsetAsync(g->dcount, 0, 8, st));
+  k_range_check<<<1184, 256, 0, st>>>(g->off, g->tgt, g->wgt, g->n, dd, g->dcount);
+  CU(cudaGetLastError());
+  unsigned long long bad = 0;
+  CU(cudaMemcpyAsync(&bad, g->dcount, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (!bad) *status &= ~2;
+  return GBBS_OK;
+}
+
 static int status_error(const gbbs_graph *g, int status, long long max_rounds) {
   if (status & 4)
     return fail(GBBS_ENOMEM, "wbfs: a bucket list exceeded its capacity of %llu entries "
                 "(device memory was short at first use; a larger delta needs fewer)",
                 g->wb ? g->wb->qcap : 0ull);
-  if (status & 2)  // a relaxation candidate reached 2^32 - 1 (uint32 distances)
-    return fail(GBBS_ERANGE, "a distance candidate reached 2^32-1 (max weight %u): "
+  if (status & 2)  // a reachable vertex's distance is >= 2^32 - 1 (k_range_check)
+    return fail(GBBS_ERANGE, "a reachable vertex's distance is >= 2^32-1 (max weight %u): "
                 "distances do not fit the uint32 output", g->maxw);
   if (status != 0)
     return fail(GBBS_EINTERNAL, "round cap (%lld rounds) exceeded", max_rounds);
@@ -829,9 +929,8 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   gbbs_opts o;
   if (int rc0 = parse_opts(opts, OPTS_TRAVERSE, o)) return rc0;
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
-  if (dev != g->device) CU(cudaSetDevice(g->device));
+  DeviceGuard dguard(g->device);
+  if (dguard.rc) return dguard.rc;
   cudaStream_t st = (cudaStream_t)stream;
 
   const bool dist_dev = is_device_ptr(dist);
@@ -959,6 +1058,7 @@ static int run(const gbbs_graph *cg_, int algo, uint32_t src, uint32_t *dist, ui
               h[4 * i] / 1e3, h[4 * i + 1] / 1e3, h[4 * i + 2] / 1e3, h[4 * i + 3]);
   }
 #endif
+  if (int rc3 = range_recheck(g, ddist, st, &ctrl.status)) return rc3;
   return status_error(g, ctrl.status, p.max_rounds);
 }
 
@@ -978,9 +1078,8 @@ static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int6
     if ((long long)srcs[i] >= g->n) return fail(GBBS_EINVAL, "srcs[%lld] = %u >= n %lld",
                                                  (long long)i, srcs[i], g->n);
   if (k == 0) return GBBS_OK;
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
-  if (dev != g->device) CU(cudaSetDevice(g->device));
+  DeviceGuard dguard(g->device);
+  if (dguard.rc) return dguard.rc;
   const size_t n = (size_t)g->n;
   const bool dist_dev = is_device_ptr(dist);
   const bool par_dev = parent ? is_device_ptr(parent) : true;
@@ -1064,7 +1163,9 @@ static int run_batch(const gbbs_graph *cg_, int algo, const uint32_t *srcs, int6
   CU(cudaStreamSynchronize(st));
   if (host_out) CU(cudaStreamSynchronize(g->cstream));
   for (int64_t i = 0; i < k; i++) {
-    const int rc = status_error(g, (int)(hs[2 * i] & 0xFFFFFFFF), g->n + 1);
+    int sti = (int)(hs[2 * i] & 0xFFFFFFFF);
+    if (int rc3 = range_recheck(g, dist + i * n, st, &sti)) return rc3;
+    const int rc = status_error(g, sti, g->n + 1);
     if (rc) return rc;
   }
   return GBBS_OK;
@@ -1141,9 +1242,8 @@ extern "C" int gbbs_bellman_ford_signed_ex(const gbbs_graph *cg_, uint32_t src, 
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   gbbs_opts o;
   if (int rc0 = parse_opts(opts, OPTS_SIGNED, o)) return rc0;
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
-  if (dev != g->device) CU(cudaSetDevice(g->device));
+  DeviceGuard dguard(g->device);
+  if (dguard.rc) return dguard.rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   if (g->smaxabs < 0) {
     g->smaxabs = 1;
@@ -1263,9 +1363,8 @@ static int run_wbfs_batch(const gbbs_graph *cg_, const uint32_t *srcs, int64_t k
   if (!is_device_ptr(dist)) return fail(GBBS_EINVAL, "gbbs_wbfs_batch writes device rows");
   gbbs_opts o;
   if (int rc0 = parse_opts(opts, OPTS_BATCH, o)) return rc0;
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
-  if (dev != g->device) CU(cudaSetDevice(g->device));
+  DeviceGuard dguard(g->device);
+  if (dguard.rc) return dguard.rc;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t n = (size_t)g->n;
   // teams: default 8 on graphs with n <= 2^24 and m <= 2^28, else 1 — measured
@@ -1354,7 +1453,9 @@ static int run_wbfs_batch(const gbbs_graph *cg_, const uint32_t *srcs, int64_t k
   CU(cudaMemcpyAsync(hs.data(), g->bstat, (size_t)k * 16, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   for (int64_t i = 0; i < k; i++) {
-    const int rc = status_error(g, (int)(hs[2 * i] & 0xFFFFFFFF), -1);
+    int sti = (int)(hs[2 * i] & 0xFFFFFFFF);
+    if (int rc3 = range_recheck(g, dist + i * (size_t)g->n, st, &sti)) return rc3;
+    const int rc = status_error(g, sti, -1);
     if (rc) return rc;
   }
   return GBBS_OK;
@@ -1462,6 +1563,8 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   if ((long long)src >= g->n) return fail(GBBS_EINVAL, "src %u >= n %lld", src, g->n);
   gbbs_opts o;
   if (int rc0 = parse_opts(opts, OPTS_OTHER, o)) return rc0;
+  DeviceGuard dguard(g->device);
+  if (dguard.rc) return dguard.rc;
   int rc = GBBS_OK;
   BcScratch *b = bc_scratch(g, &rc);
   if (!b) return rc;
@@ -1536,9 +1639,8 @@ extern "C" int gbbs_betweenness_batch_ex(const gbbs_graph *cg_, const uint32_t *
   const int G = (int)(o.teams ? o.teams
                               : ((g->n <= (1ll << 24) && g->m <= (1ll << 28)) ? BC_TEAMS_AUTO : 1));
   if (G > BC_GMAX) return fail(GBBS_EINVAL, "teams %d > %d", G, BC_GMAX);
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
-  if (dev != g->device) CU(cudaSetDevice(g->device));
+  DeviceGuard dguard(g->device);
+  if (dguard.rc) return dguard.rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const size_t n = (size_t)g->n;
   int rc = GBBS_OK;

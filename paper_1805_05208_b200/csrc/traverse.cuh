@@ -113,6 +113,8 @@ struct RoundStat {           // mirrors gbbs_round_stat
   long long t_start_ns;
   long long t_work_ns;
   long long t_flush_ns;
+  long long alg_bytes;       // algorithmic bytes at load granularity (STATS builds)
+  long long head_hits;       // dense pull: acquired by the inline first in-edge
 };
 
 struct Params {
@@ -123,7 +125,9 @@ struct Params {
   const long long *in_off;   // in-CSC (alias of CSR when symmetric)
   const uint32_t *in_tgt;
   const uint32_t *iso;       // [nwords] isolated-vertex (+padding) mask
-  const uint32_t *odeg;      // out-degrees (directed graphs; nullptr if symmetric)
+  const uint32_t *nin;       // [nwords] no in-edges (+padding): never a pull candidate
+  const uint2 *pin;          // [n] pull record: (first in-neighbour or INF, out-degree)
+  long long ncand;           // vertices with at least one in-edge
   uint32_t *dist;            // [n]
   uint16_t *shadow;          // [n] BF/WP: 16-bit conservative copy of dist
   uint32_t *parent;          // [n] or nullptr
@@ -143,8 +147,10 @@ struct Params {
   long long nwords;
   long long dense_threshold; // dense iff |U| + sum deg(U) > dense_threshold
   long long max_rounds;
+  unsigned long long *acq;   // BFS: ring [4] of per-round acquisition counts (reading A10b)
   int ebits;
   int mode;                  // 0 auto, 1 sparse, 2 dense, 3 pull
+  int rules;                 // gbbs_opts.rules (GBBS_RULE_PAPER_ONLY = 1)
   int bsize;                 // list-push tile edges (power of two in [32, TE]); 0 = adaptive
   int symmetric;
   uint32_t src;
@@ -205,8 +211,8 @@ struct WarpSmem {             // one per warp; nothing here is shared across war
 
 struct Smem {
   WarpSmem w[NWARPS];
-  unsigned long long sacc[5];
-  unsigned long long cnt, hcnt;
+  unsigned long long sacc[7];
+  unsigned long long cnt, hcnt, acq;
 };
 
 // Per-warp round state kept in registers: staging count, emitted (K, D) for
@@ -216,7 +222,9 @@ struct WarpState {
   unsigned long long bk = 0;     // wBFS: bucket being processed
   unsigned long long pmask = 0;  // wBFS: bucket lists this lane appended to
   unsigned long long K = 0, D = 0;
+  unsigned long long A = 0;      // BFS: vertices acquired this round (warp-uniform)
   unsigned long long edges = 0, swept = 0, acquired = 0;
+  unsigned long long ab = 0, hh = 0;  // STATS: algorithmic bytes, pull head hits
 #ifdef GBBS_DIAG_LIST  // diagnostic builds: list-round phase timestamps
   unsigned long long t1 = 0, t2 = 0;
 #endif
@@ -404,7 +412,8 @@ template <int ALGO>
 __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, int cnt, int nb,
                                            int r, uint32_t *bits_next,
                                            unsigned long long *tmark = nullptr,
-                                           unsigned long long *ctr = nullptr) {
+                                           unsigned long long *ctr = nullptr,
+                                           unsigned long long *abp = nullptr) {
   constexpr int FL = 4;
   const int lane = threadIdx.x & 31;
 #ifdef GBBS_DBG_PHASE
@@ -422,6 +431,7 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
         const uint32_t v = st[i];
         lo[u] = __ldg(p.off + v);
         hi[u] = __ldg(p.off + v + 1);
+        if (abp) *abp += 16;  // STATS: the offset pair
       }
     }
 #pragma unroll
@@ -471,6 +481,7 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
       const long long o = (long long)d + dex;
       if (keep) {
         GBBS_CHECK(pos < (unsigned long long)p.n);
+        if (abp) *abp += 20;  // STATS: the entry (v, O, base)
         fv[pos] = vv[u];
         fo[pos] = o;
         fb[pos] = lo[u] - o;
@@ -758,10 +769,11 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
       if (win[j]) st[ws.scnt + __popc(b & lanemask_lt())] = vv[j];
       ws.scnt += __popc(b);
+      if (ALGO == ALGO_BFS) ws.A += __popc(b);
     }
     if (ws.scnt > WCAP - 32 * NB) {
       if (STATS && lane == 0) ws.acquired += ws.scnt;
-      warp_flush<ALGO>(p, st, ws.scnt, nb, r, bits);
+      warp_flush<ALGO>(p, st, ws.scnt, nb, r, bits, nullptr, nullptr, STATS ? &ws.ab : nullptr);
       ws.scnt = 0;
     }
   }
@@ -785,7 +797,10 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
   const long long *O = p.fo[lb];
   const long long *B = p.fb[lb];
   const uint32_t *F = p.fv[lb];
-  if (STATS && lane == 0) ws.edges += (unsigned long long)(te - ts);
+  if (STATS && lane == 0) {
+    ws.edges += (unsigned long long)(te - ts);
+    ws.ab += (unsigned long long)(te - ts) * ((ALGO != ALGO_BFS && p.wgt) ? 8 : 4);
+  }
 #ifdef GBBS_DIAG_TILE
   const unsigned long long tT0 = globaltimer_ns();
 #endif
@@ -799,6 +814,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
     Ok = __ldcg(O + k);
     Bk = __ldcg(B + k);
     Uk = __ldcg(F + k);
+    if (STATS) ws.ab += 20;  // frontier entry (v, O, base)
   }
   const unsigned inb = __ballot_sync(FULL, Ok < te);  // owners with an edge in the tile
   const int n32 = __popc(inb);
@@ -885,6 +901,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
         o2[h] = __ldcg(O + kk);
         b2[h] = __ldcg(B + kk);
         u2[h] = __ldcg(F + kk);
+        if (STATS) ws.ab += 20;
       }
     }
     int cnt_h[2];
@@ -1017,7 +1034,10 @@ __device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, Wa
     const long long la = __shfl_sync(FULL, a, l);
     const int ld = __shfl_sync(FULL, dg, l);
     const uint32_t lx = __shfl_sync(FULL, x, l);
-    if (STATS && lane == 0) ws.edges += ld;
+    if (STATS && lane == 0) {
+      ws.edges += ld;
+      ws.ab += (unsigned long long)ld * ((ALGO != ALGO_BFS && p.wgt) ? 8 : 4);
+    }
     for (int cs = 0; cs < ld; cs += 32 * NCH) {
       uint32_t vv[NCH], ww[NCH], uu[NCH];
       bool act[NCH];
@@ -1034,7 +1054,10 @@ __device__ __forceinline__ void push_vertices(const Params &p, WarpSmem &wsm, Wa
     }
   }
   const int mine = dg <= 32 ? dg : 0;
-  if (STATS) ws.edges += mine;
+  if (STATS) {
+    ws.edges += mine;
+    ws.ab += (unsigned long long)mine * ((ALGO != ALGO_BFS && p.wgt) ? 8 : 4);
+  }
   int mx = mine;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
@@ -1094,6 +1117,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
       fw = fr[word];
       if (fw) fr[word] = 0;
     }
+    if (STATS) ws.ab += (ALGO == ALGO_BFS ? 8 : 4) + (fw ? 4 : 0);  // bitmap words swept / updated
   }
   if (!__any_sync(FULL, fw != 0)) return;
   const int cnt = warp_gather(w, w0, fw);
@@ -1109,7 +1133,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
       ws.scnt += __popc(bal);
       if (ws.scnt > WCAP - 32) {
         warp_flush<ALGO>(p, wsm.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr,
-                         p.hcnt + (r & 1));
+                         p.hcnt + (r & 1), STATS ? &ws.ab : nullptr);
         ws.scnt = 0;
       }
     }
@@ -1124,6 +1148,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
     if (valid) {
       a = __ldg(p.off + v);
       dg = (int)(__ldg(p.off + v + 1) - a);
+      if (STATS) ws.ab += 16;
     }
     uint32_t x = v;
     if (ALGO != ALGO_BFS) x = dg > 0 ? ld_relaxed(p.dist + v) : 0u;
@@ -1144,9 +1169,6 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #endif
 #ifndef GBBS_PULL_DYNQ
 #define GBBS_PULL_DYNQ 1
-#endif
-#ifndef GBBS_PULL_SPEC_ODEG
-#define GBBS_PULL_SPEC_ODEG 1
 #endif
 #ifndef GBBS_LIST_DYNQ
 #define GBBS_LIST_DYNQ 1
@@ -1169,9 +1191,6 @@ static_assert(GBBS_PULL_SW <= SWEEP_WORDS, "pull units are gathered into SweepSm
 #ifndef GBBS_LONG_IN
 #define GBBS_LONG_IN 24
 #endif
-#ifndef GBBS_LONG_UNROLL
-#define GBBS_LONG_UNROLL 1
-#endif
 constexpr int PULL_STEPS = GBBS_PULL_STEPS;
 constexpr int LONG_IN = GBBS_LONG_IN;
 constexpr int PCH = GBBS_PCH;
@@ -1182,76 +1201,123 @@ __device__ __forceinline__ bool vbit(const uint32_t *vis, uint32_t u) {
   return (vis[u >> 5] >> (u & 31)) & 1u;
 }
 
-template <bool STATS>
+// Pull record of a candidate: (first in-neighbour, out-degree) in one 8-byte load.
+__device__ __forceinline__ uint2 ld_stream_v2(const uint2 *a) {
+  uint2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+      : "=r"(v.x), "=r"(v.y)
+      : "l"(a), "l"(ef_policy()));
+  return v;
+}
+
+// Candidates = the unit's vertices that are unvisited and have in-edges (the
+// no-in-edge mask nin removes vertices no pull can ever acquire).  A candidate's
+// first in-edge comes from its 8-byte pull record, loaded beside its in-offsets:
+// rMAT in-lists are sorted by source, so the first in-neighbour is the lowest
+// id — the likeliest hub, visited early — and most acquisitions are decided
+// without touching the in-edge array.  The scan then continues from the second
+// in-edge in CSC order (same edges, same order, same early exit: P:1870-1874).
+// LISTOUT (light pulls, below): acquisitions with out-edges are also staged and
+// flushed into frontier list nb with their edge prefixes, so the next round can
+// push from a list instead of sweeping the bitmap.
+template <bool STATS, bool LISTOUT = false>
 __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
                                            const uint32_t *vis, uint32_t *vis_next, int r,
-                                           WarpState &ws) {
+                                           WarpState &ws, int nb = 0) {
   const int lane = threadIdx.x & 31;
   SweepSmem &w = wsm.u.s;
   const long long word = w0 + lane;
   const bool mine = lane < sw && word < p.nwords;
   const uint32_t vw = mine ? vis[word] : FULL;
-  if (!__any_sync(FULL, vw != FULL)) {  // all visited: carry the words over
-    if (mine) vis_next[word] = FULL;
+  const uint32_t skip = mine ? (vw | __ldg(p.nin + word)) : FULL;
+  if (STATS && mine) ws.ab += 12;  // visited + no-in words read, next visited word written
+  if (!__any_sync(FULL, skip != FULL)) {  // nothing to pull: carry the words over
+    if (mine) vis_next[word] = vw;
     return;
   }
-  const int cnt = warp_gather(w, w0, ~vw);
+  const int cnt = warp_gather(w, w0, ~skip);
   w.found[lane] = 0;
   __syncwarp();
   if (STATS && lane == 0) ws.swept += cnt;
   for (int c0 = 0; c0 < cnt; c0 += 32 * PCH) {
-    uint32_t v[PCH], par[PCH];
+    uint32_t v[PCH], par[PCH], dgo[PCH];
     long long js[PCH];
-    int rem[PCH], deg_in[PCH];
+    int rem[PCH];
+    uint2 rec[PCH];
+    long long o0[PCH], o1[PCH];
 #pragma unroll
     for (int q = 0; q < PCH; q++) {
       const int i = c0 + 32 * q + lane;
       v[q] = i < cnt ? w.cand[i] : 0;
+      rec[q] = make_uint2(INF, 0);
+      o0[q] = o1[q] = 0;
+      if (i < cnt) {
+        rec[q] = ld_stream_v2(p.pin + v[q]);
+        o0[q] = ld_stream64(p.in_off + v[q]);
+        o1[q] = ld_stream64(p.in_off + v[q] + 1);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      const int i = c0 + 32 * q + lane;
+      par[q] = INF;
       js[q] = 0;
       rem[q] = 0;
-      par[q] = INF;
+      dgo[q] = rec[q].y;  // out-degree an acquisition adds to the next round's edges
       if (i < cnt) {
-        js[q] = ld_stream64(p.in_off + v[q]);
-        rem[q] = (int)(ld_stream64(p.in_off + v[q] + 1) - js[q]);
+        if (STATS) {
+          ws.ab += 24;  // pull record + in-offset pair
+          ws.edges += 1;
+        }
+        if (rec[q].x != INF && vbit(vis, rec[q].x)) {
+          par[q] = rec[q].x;
+          if (STATS) ws.hh += 1;
+        } else {
+          js[q] = o0[q] + 1;
+          rem[q] = (int)(o1[q] - js[q]);
+        }
       }
-      // the out-degree an acquired vertex adds to the next round's edge count:
-      // symmetric = in-degree; directed: loaded now, beside in_off, for every
-      // candidate (consecutive ids: coalesced) instead of a random load on acquire
-      deg_in[q] = rem[q];
-      if (GBBS_PULL_SPEC_ODEG && !p.symmetric) deg_in[q] = (i < cnt) ? (int)__ldg(p.odeg + v[q]) : 0;
     }
-    for (int step = 0; step < PULL_STEPS; step++) {
-      uint4 g[PCH];
+    bool anyrem = false;
 #pragma unroll
-      for (int q = 0; q < PCH; q++)
-        if (rem[q] > 0) {
-          GBBS_CHECK(js[q] >= 0 && js[q] < p.m);
-          g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+    for (int q = 0; q < PCH; q++) anyrem |= rem[q] > 0;
+    if (__any_sync(FULL, anyrem)) {
+      for (int step = 0; step < PULL_STEPS; step++) {
+        uint4 g[PCH];
+#pragma unroll
+        for (int q = 0; q < PCH; q++)
+          if (rem[q] > 0) {
+            GBBS_CHECK(js[q] >= 0 && js[q] < p.m);
+            g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+          }
+        bool live = false;
+#pragma unroll
+        for (int q = 0; q < PCH; q++) {
+          if (rem[q] <= 0) continue;
+          const int lo = (int)(js[q] & 3);
+          const int hi = min(4, lo + rem[q]);
+          const uint32_t e[4] = {g[q].x, g[q].y, g[q].z, g[q].w};
+          bool b[4];
+#pragma unroll
+          for (int k = 0; k < 4; k++) b[k] = (k >= lo && k < hi) ? vbit(vis, e[k]) : false;
+          uint32_t hit = INF;
+#pragma unroll
+          for (int k = 3; k >= 0; k--)
+            if (b[k]) hit = e[k];
+          if (STATS) {
+            ws.edges += hi - lo;
+            ws.ab += 16;
+          }
+          js[q] += hi - lo;
+          rem[q] -= hi - lo;
+          if (hit != INF) {
+            par[q] = hit;
+            rem[q] = 0;
+          }
+          live |= rem[q] > 0;
         }
-      bool live = false;
-#pragma unroll
-      for (int q = 0; q < PCH; q++) {
-        if (rem[q] <= 0) continue;
-        const int lo = (int)(js[q] & 3);
-        const int hi = min(4, lo + rem[q]);
-        const uint32_t e[4] = {g[q].x, g[q].y, g[q].z, g[q].w};
-        bool b[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) b[k] = (k >= lo && k < hi) ? vbit(vis, e[k]) : false;
-        uint32_t hit = INF;
-#pragma unroll
-        for (int k = 3; k >= 0; k--)
-          if (b[k]) hit = e[k];
-        if (STATS) ws.edges += hi - lo;
-        js[q] += hi - lo;
-        rem[q] -= hi - lo;
-        if (hit != INF) {
-          par[q] = hit;
-          rem[q] = 0;
-        }
-        live |= rem[q] > 0;
+        if (!__any_sync(FULL, live)) break;
       }
-      if (!__any_sync(FULL, live)) break;
     }
     // short remainders: per lane; long remainders: the whole warp, one vertex at a time
 #pragma unroll
@@ -1269,7 +1335,10 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
 #pragma unroll
           for (int k = 3; k >= 0; k--)
             if (k >= lo && k < hi && vbit(vis, e[k])) hit = e[k];
-          if (STATS) ws.edges += hi - lo;
+          if (STATS) {
+            ws.edges += hi - lo;
+            ws.ab += 16;
+          }
           js[q] += hi - lo;
           rem[q] -= hi - lo;
           if (hit != INF) {
@@ -1285,43 +1354,27 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
         long long a = __shfl_sync(FULL, js[q], l);
         const long long e_end = a + __shfl_sync(FULL, rem[q], l);
         uint32_t found = INF;
-        // GBBS_LONG_UNROLL groups of 128 in-edges per step: all loads, then all
-        // probes, so a step keeps UNROLL x 16 B per lane in flight
+        // groups of 128 in-edges per step: a 16-byte load per lane, then the probes
         while (a < e_end) {
           const long long a0 = a & ~3ll;
-          uint4 g[GBBS_LONG_UNROLL];
+          const long long gk = a0 + 4 * lane;
+          uint32_t hit = INF;
+          if (gk < e_end) {
+            GBBS_CHECK(gk >= 0 && gk < p.m);
+            const uint4 g = ldg_v4(p.in_tgt + gk);
+            const uint32_t e[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-          for (int u = 0; u < GBBS_LONG_UNROLL; u++) {
-            const long long gk = a0 + 128 * u + 4 * lane;
-            if (gk < e_end) {
-              GBBS_CHECK(gk >= 0 && gk < p.m);
-              g[u] = ldg_v4(p.in_tgt + gk);
-            }
+            for (int k = 3; k >= 0; k--)
+              if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit = e[k];
+            if (STATS) ws.ab += 16;
           }
-          uint32_t hit[GBBS_LONG_UNROLL];
-#pragma unroll
-          for (int u = 0; u < GBBS_LONG_UNROLL; u++) {
-            const long long gk = a0 + 128 * u + 4 * lane;
-            hit[u] = INF;
-            if (gk < e_end) {
-              const uint32_t e[4] = {g[u].x, g[u].y, g[u].z, g[u].w};
-#pragma unroll
-              for (int k = 3; k >= 0; k--)
-                if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit[u] = e[k];
-            }
+          if (STATS && lane == 0) ws.edges += min(a0 + 128, e_end) - a;
+          const unsigned hb = __ballot_sync(FULL, hit != INF);  // first hit in CSC order
+          if (hb) {
+            found = __shfl_sync(FULL, hit, __ffs(hb) - 1);
+            break;
           }
-          if (STATS && lane == 0) ws.edges += min(a0 + 128 * GBBS_LONG_UNROLL, e_end) - a;
-          bool done = false;
-#pragma unroll
-          for (int u = 0; u < GBBS_LONG_UNROLL; u++) {  // first hit in CSC order
-            const unsigned hb = __ballot_sync(FULL, hit[u] != INF);
-            if (hb && !done) {
-              found = __shfl_sync(FULL, hit[u], __ffs(hb) - 1);
-              done = true;
-            }
-          }
-          if (done) break;
-          a = a0 + 128 * GBBS_LONG_UNROLL;
+          a = a0 + 128;
         }
         if (lane == l) {
           rem[q] = 0;
@@ -1331,24 +1384,95 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
     }
 #pragma unroll
     for (int q = 0; q < PCH; q++) {
+      ws.A += __popc(__ballot_sync(FULL, par[q] != INF));
       if (par[q] != INF) {
         const uint32_t vq = v[q];
-        if (STATS) ws.acquired += 1;
+        if (STATS && (!LISTOUT || dgo[q] == 0)) ws.acquired += 1;  // LISTOUT: staged ones at flush
+#ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
         st_stream(p.dist + vq, (uint32_t)(r + 1));
         if (p.parent) st_stream(p.parent + vq, par[q]);
+#endif
         atomicOr(&w.found[(vq >> 5) - (uint32_t)w0], 1u << (vq & 31));
-        const uint32_t dgo = (p.symmetric || GBBS_PULL_SPEC_ODEG) ? (uint32_t)deg_in[q]
-                                                                   : __ldg(p.odeg + vq);
-        if (dgo > 0) {
+        if (!LISTOUT && dgo[q] > 0) {
           ws.K += 1;
-          ws.D += dgo;
+          ws.D += dgo[q];
         }
+      }
+    }
+    if (LISTOUT) {
+#pragma unroll
+      for (int q = 0; q < PCH; q++) {
+        const bool stg = par[q] != INF && dgo[q] > 0;
+        const unsigned b = __ballot_sync(FULL, stg);
+        GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
+        if (stg) wsm.stage[ws.scnt + __popc(b & lanemask_lt())] = v[q];
+        ws.scnt += __popc(b);
+      }
+      if (ws.scnt > WCAP - 32 * PCH) {
+        if (STATS && (threadIdx.x & 31) == 0) ws.acquired += ws.scnt;
+        warp_flush<ALGO_BFS>(p, wsm.stage, ws.scnt, nb, r, nullptr, nullptr, nullptr,
+                             STATS ? &ws.ab : nullptr);
+        ws.scnt = 0;
       }
     }
   }
   __syncwarp();
   if (mine) vis_next[word] = vw | w.found[lane];
   __syncwarp();
+}
+
+// ---- light pull: a dense round with few candidates left -----------------------------
+// When at most GBBS_LIGHT candidates per warp remain (the tail of a direction-
+// optimising BFS, reading A10b), most 32-word groups have nothing to pull.  Warps
+// take contiguous blocks of 128 words (static, no work queue), read the visited and
+// no-in-edge words as 16-byte vectors, carry dead groups over with vector stores and
+// run pull_words only on groups with candidates, emitting a frontier list for the
+// next round (LISTOUT) so that a small next frontier is pushed from a list instead
+// of swept as a bitmap.
+#ifndef GBBS_LIGHT
+#define GBBS_LIGHT 128
+#endif
+template <bool STATS>
+__device__ __forceinline__ void light_pull(const Params &p, WarpSmem &wsm, WarpState &ws,
+                                           const uint32_t *vis, uint32_t *vis_next, int r, int nb,
+                                           long long gw, long long nw) {
+  const int lane = threadIdx.x & 31;
+  const long long steps = (p.nwords + 127) / 128;
+  const long long per = (steps + nw - 1) / nw;
+  const long long s1 = min(steps, (gw + 1) * per);
+  for (long long st = gw * per; st < s1; st++) {
+    const long long w0 = st * 128;
+    const long long wl = w0 + 4 * lane;
+    uint4 a = make_uint4(FULL, FULL, FULL, FULL), b = a;
+    if (wl + 3 < p.nwords) {
+      a = __ldcg(reinterpret_cast<const uint4 *>(vis + wl));
+      b = __ldg(reinterpret_cast<const uint4 *>(p.nin + wl));
+    } else {
+      if (wl < p.nwords) { a.x = vis[wl]; b.x = p.nin[wl]; }
+      if (wl + 1 < p.nwords) { a.y = vis[wl + 1]; b.y = p.nin[wl + 1]; }
+      if (wl + 2 < p.nwords) { a.z = vis[wl + 2]; b.z = p.nin[wl + 2]; }
+    }
+    if (STATS) ws.ab += 8 * 4;
+    const bool has = ((a.x | b.x) & (a.y | b.y) & (a.z | b.z) & (a.w | b.w)) != FULL;
+    const unsigned hb = __ballot_sync(FULL, has);
+    if (!((hb >> (lane & ~7)) & 0xFFu)) {  // this lane's 32-word group is dead: carry over
+      if (STATS) ws.ab += 16;
+      if (wl + 3 < p.nwords) {
+        *reinterpret_cast<uint4 *>(vis_next + wl) = a;
+      } else {
+        if (wl < p.nwords) vis_next[wl] = a.x;
+        if (wl + 1 < p.nwords) vis_next[wl + 1] = a.y;
+        if (wl + 2 < p.nwords) vis_next[wl + 2] = a.z;
+      }
+    }
+#pragma unroll 1
+    for (int g = 0; g < 4; g++)
+      if ((hb >> (8 * g)) & 0xFFu) {
+        // pull_words counts its words' visited / no-in reads again: counted above
+        if (STATS && lane == 0) ws.ab -= 8 * min(32ll, max(0ll, p.nwords - (w0 + 32 * g)));
+        pull_words<STATS, true>(p, wsm, w0 + 32 * g, 32, vis, vis_next, r, ws, nb);
+      }
+  }
 }
 
 // ---- dense pull-min (Bellman-Ford / widest path, GBBS_MODE_PULL) ---------------------
@@ -1563,7 +1687,8 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
       forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, sw, fr, bits, precheck, nb, r, convert);
   }
   if (ALGO == ALGO_BFS && convert && ws.scnt > 0) {
-    warp_flush<ALGO>(p, w.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr, p.hcnt + (r & 1));
+    warp_flush<ALGO>(p, w.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr, p.hcnt + (r & 1),
+                     STATS ? &ws.ab : nullptr);
     ws.scnt = 0;
   }
   team_sync<MG>(grid, p.bar, nblk);  // heavy list complete
@@ -1626,7 +1751,11 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     }
   }
   const long long a0 = p.off[src], d0 = p.off[src + 1] - a0;
+  // reading A10b: vertices with in-edges acquired so far (the source counts if it has any)
+  long long acq_total = 0;
+  if (ALGO == ALGO_BFS) acq_total = ((__ldg(p.nin + (src >> 5)) >> (src & 31)) & 1u) ? 0 : 1;
   if (GBBS_BID == 0 && tid == 0) {
+    if (ALGO == ALGO_BFS) p.acq[0] = p.acq[1] = p.acq[2] = p.acq[3] = 0;
     p.cnt[1] = p.cnt[2] = p.cnt[3] = 0;
     p.hcnt[0] = p.hcnt[1] = 0;
     for (int q = 0; q < 8; q++) p.wq[q] = 0;
@@ -1647,11 +1776,15 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
   bool list_valid = true;  // is this round's frontier materialised as a list?
   long long r = 0;
   for (;; r++) {
-    if (tid == 0) s.cnt = ld_relaxed64(p.cnt + (r & 3));
+    if (tid == 0) {
+      s.cnt = ld_relaxed64(p.cnt + (r & 3));
+      if (ALGO == ALGO_BFS) s.acq = ld_relaxed64(p.acq + (r & 3));
+    }
     __syncthreads();
     const unsigned long long c = s.cnt;
     const long long f = (long long)(c >> p.ebits);
     const long long E = (long long)(c & emask);
+    if (ALGO == ALGO_BFS) acq_total += (long long)s.acq;
     if (STATS && GBBS_BID == 0 && tid == 0 && p.stats && r < p.stats_cap)
       p.stats[r].t_start_ns = (long long)globaltimer_ns();
     if (f == 0) break;
@@ -1664,9 +1797,17 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     // forces bitmap-forward rounds (reading A11: measured slower on rMAT).
     // mode 3 (GBBS_MODE_PULL): BFS as auto; BF / widest path take a pull-min
     // round (kind 3, symmetric graphs) when |U| + sum deg(U) > m/T
+    // Reading A10b (BFS AUTO): after a dense round the frontier is a bitmap, and
+    // the next round stays dense while the pull's remaining work — the vertices
+    // with in-edges not visited yet (ncand - acquired so far) — is at most the
+    // push's |U| + sum deg(U): a pull then sweeps few candidates, while a push
+    // would expand the whole frontier (Beamer's bottom-up -> top-down switch in
+    // work terms).  GBBS_RULE_PAPER_ONLY keeps the paper's m/T test alone.
     const bool over = f + E > p.dense_threshold;
+    const bool stay = ALGO == ALGO_BFS && !list_valid && !(p.rules & 1) &&
+                      p.ncand - acq_total <= f + E;
     const bool big = (ALGO == ALGO_BFS)
-                         ? (p.mode == 2 || ((p.mode == 0 || p.mode == 3) && over))
+                         ? (p.mode == 2 || ((p.mode == 0 || p.mode == 3) && (over || stay)))
                          : (p.mode == 2 || (p.mode == 3 && over));
     int kind;
     if (ALGO == ALGO_BFS) kind = big ? 1 : (list_valid ? 0 : 2);
@@ -1674,6 +1815,7 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     else kind = (big || !list_valid) ? 2 : 0;
     if (GBBS_BID == 0 && tid == 0) {
       p.cnt[(r + 2) & 3] = 0;
+      if (ALGO == ALGO_BFS) p.acq[(r + 2) & 3] = 0;
       p.wq[(r + 2) & 3] = 0;
       p.wq[4 + ((r + 2) & 3)] = 0;
       p.hcnt[(r + 1) & 1] = 0;
@@ -1686,7 +1828,11 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     const int cb = (int)(r & 1), nb = cb ^ 1;
     WarpState ws;
     bool emit_count = false;
-    if (kind == 1) {  // dense pull (BFS)
+    if (kind == 1 && ALGO == ALGO_BFS && p.ncand - acq_total <= (long long)GBBS_LIGHT * nw) {
+      light_pull<STATS>(p, wsm, ws, p.bm[vc], p.bm[vc ^ 1], (int)r, nb, gw, nw);
+      vc ^= 1;
+      list_valid = true;  // the acquisitions were also emitted as list nb
+    } else if (kind == 1) {  // dense pull (BFS)
       const uint32_t *vis = p.bm[vc];
       uint32_t *vis_next = p.bm[vc ^ 1];
       if (GBBS_PULL_DYNQ) {
@@ -1756,7 +1902,8 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
       const unsigned long long tF0 = globaltimer_ns();
 #endif
       warp_flush<ALGO>(p, wsm.stage, ws.scnt, nb, (int)r,
-                       (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nb], &t_work);
+                       (ALGO == ALGO_BFS) ? p.bm[vc] : p.bm[nb], &t_work, nullptr,
+                       STATS ? &ws.ab : nullptr);
 #ifdef GBBS_DIAG_TILE
       if (ALGO == ALGO_BFS && kind == 0) {
         diag_add(p.dbg, 5, globaltimer_ns() - tF0);
@@ -1768,23 +1915,28 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
       const unsigned long long K = warp_sum64((long long)ws.K), D = warp_sum64((long long)ws.D);
       if (lane == 0 && K) atomicAdd(p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
     }
+    if (ALGO == ALGO_BFS && lane == 0 && ws.A) atomicAdd(p.acq + ((r + 1) & 3), ws.A);
     if (STATS) t_flush = globaltimer_ns();
 #ifdef GBBS_DIAG_LIST
     if (STATS) { t_work = ws.t1; t_flush = ws.t2; ws.t1 = ws.t2 = 0; }
 #endif
     if (STATS && p.stats && r < p.stats_cap) {
       // one global atomic per CTA and counter
-      if (tid < 5) s.sacc[tid] = 0;
+      if (tid < 7) s.sacc[tid] = 0;
       __syncthreads();
       const unsigned long long e = warp_sum64((long long)ws.edges);
       const unsigned long long sw = warp_sum64((long long)ws.swept);
       const unsigned long long aq = warp_sum64((long long)ws.acquired);
+      const unsigned long long ab = warp_sum64((long long)ws.ab);
+      const unsigned long long hh = warp_sum64((long long)ws.hh);
       if (lane == 0) {
         atomicAdd(&s.sacc[0], e);
         atomicAdd(&s.sacc[1], sw);
         atomicAdd(&s.sacc[2], aq);
         atomicMax(&s.sacc[3], t_work);
         atomicMax(&s.sacc[4], t_flush);
+        atomicAdd(&s.sacc[5], ab);
+        atomicAdd(&s.sacc[6], hh);
       }
       __syncthreads();
       if (tid == 0) {
@@ -1793,6 +1945,8 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
         atomicAdd((unsigned long long *)&p.stats[r].acquired, s.sacc[2]);
         atomicMax((unsigned long long *)&p.stats[r].t_work_ns, s.sacc[3]);
         atomicMax((unsigned long long *)&p.stats[r].t_flush_ns, s.sacc[4]);
+        atomicAdd((unsigned long long *)&p.stats[r].alg_bytes, s.sacc[5]);
+        atomicAdd((unsigned long long *)&p.stats[r].head_hits, s.sacc[6]);
       }
     }
     team_sync<MG>(grid, p.bar, GBBS_NBLK);

@@ -23,6 +23,7 @@ GBBS_DIST_INF = np.iinfo(np.int64).max
 GBBS_DIST_NEGINF = np.iinfo(np.int64).min
 GBBS_SYMMETRIC, GBBS_BORROW, GBBS_NO_VALIDATE = 0x1, 0x2, 0x4
 GBBS_MODE_AUTO, GBBS_MODE_SPARSE, GBBS_MODE_DENSE, GBBS_MODE_PULL = 0, 1, 2, 3
+GBBS_RULE_PAPER_ONLY = 0x1
 
 EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_bfs",
            "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
@@ -40,11 +41,18 @@ class GbbsError(RuntimeError):
         self.code = code
 
 
+class GbbsArgError(GbbsError, ValueError):
+    """An argument rejected by the binding before it reaches C (code GBBS_EINVAL)."""
+
+    def __init__(self, msg):
+        super().__init__(GBBS_EINVAL, msg)
+
+
 class gbbs_opts(ctypes.Structure):
     _fields_ = [("threshold_den", ctypes.c_uint32), ("mode", ctypes.c_int32),
                 ("ctas_per_sm", ctypes.c_uint32), ("delta", ctypes.c_uint32),
                 ("neg_scope", ctypes.c_uint32), ("bsize", ctypes.c_uint32),
-                ("teams", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 1)]
+                ("teams", ctypes.c_uint32), ("rules", ctypes.c_uint32)]
 
 
 class gbbs_round_stat(ctypes.Structure):
@@ -52,7 +60,8 @@ class gbbs_round_stat(ctypes.Structure):
                 ("frontier", ctypes.c_int64), ("frontier_edges", ctypes.c_int64),
                 ("acquired", ctypes.c_int64), ("edges_examined", ctypes.c_int64),
                 ("vertices_swept", ctypes.c_int64), ("t_start_ns", ctypes.c_int64),
-                ("t_work_ns", ctypes.c_int64), ("t_flush_ns", ctypes.c_int64)]
+                ("t_work_ns", ctypes.c_int64), ("t_flush_ns", ctypes.c_int64),
+                ("alg_bytes", ctypes.c_int64), ("head_hits", ctypes.c_int64)]
 
 
 class gbbs_stats(ctypes.Structure):
@@ -135,6 +144,41 @@ def _ptr(a):
     raise TypeError(f"unsupported array type {type(a)}")
 
 
+def _shape(a):
+    """(element size in bytes, element count, is-integer, is-float) of an array, or None
+    for a raw address (int), which is passed through unchecked."""
+    if a is None or isinstance(a, int):
+        return None
+    if isinstance(a, np.ndarray):
+        return a.dtype.itemsize, a.size, a.dtype.kind in "iu", a.dtype.kind == "f"
+    if hasattr(a, "element_size"):
+        return (a.element_size(), a.numel(), not (a.is_floating_point() or a.is_complex()),
+                a.is_floating_point())
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _want(a, name, itemsize, count, kind="int", exact=False):
+    """Check an argument before its address goes to C: element size, integer or float
+    elements, and at least (exactly, if exact) `count` elements.  The library reads
+    and writes fixed widths, so a mismatch would be an out-of-bounds access."""
+    sh = _shape(a)
+    if sh is None:
+        return
+    isz, cnt, is_int, is_float = sh
+    if isz != itemsize or (kind == "int" and not is_int) or (kind == "float" and not is_float):
+        raise GbbsArgError(f"{name}: expected {itemsize}-byte {kind} elements, got {isz}-byte "
+                         f"{'int' if is_int else 'float' if is_float else 'other'}")
+    if (cnt != count) if exact else (cnt < count):
+        raise GbbsArgError(f"{name}: expected {'exactly' if exact else 'at least'} {count} "
+                         f"elements, got {cnt}")
+
+
+def _graph_n(handle):
+    n = ctypes.c_int64()
+    _check(lib.gbbs_graph_info(handle, ctypes.byref(n), None, None))
+    return n.value
+
+
 def _stream(stream, *arrays):
     if stream is not None:
         return stream if isinstance(stream, int) else stream.cuda_stream
@@ -149,6 +193,10 @@ def _stream(stream, *arrays):
 
 def gbbs_graph_create(n, m, offsets, targets, weights=None, flags=0):
     """Returns an opaque handle (int).  See gbbs.h for ownership and errors."""
+    if 1 <= int(n) <= 0xFFFFFFFE and int(m) >= 0:  # else the library rejects n / m unread
+        _want(offsets, "offsets", 8, int(n) + 1, exact=True)
+        _want(targets, "targets", 4, int(m), exact=True)
+        _want(weights, "weights", 4, int(m), exact=True)
     h = ctypes.c_void_p()
     _check(lib.gbbs_graph_create(int(n), int(m), _ptr(offsets), _ptr(targets), _ptr(weights),
                                  int(flags), ctypes.byref(h)))
@@ -160,6 +208,9 @@ def gbbs_graph_destroy(handle):
 
 
 def gbbs_bfs(handle, src, dist, parent=None, stream=None, opts=None, stats=None):
+    n = _graph_n(handle)
+    _want(dist, "dist", 4, n)
+    _want(parent, "parent", 4, n)
     st = _stream(stream, dist, parent)
     if opts is None and stats is None:
         _check(lib.gbbs_bfs(handle, int(src), _ptr(dist), _ptr(parent), st))
@@ -170,6 +221,7 @@ def gbbs_bfs(handle, src, dist, parent=None, stream=None, opts=None, stats=None)
 
 
 def gbbs_bellman_ford(handle, src, dist, stream=None, opts=None, stats=None):
+    _want(dist, "dist", 4, _graph_n(handle))
     st = _stream(stream, dist)
     if opts is None and stats is None:
         _check(lib.gbbs_bellman_ford(handle, int(src), _ptr(dist), st))
@@ -180,6 +232,7 @@ def gbbs_bellman_ford(handle, src, dist, stream=None, opts=None, stats=None):
 
 
 def gbbs_widest_path(handle, src, width, stream=None, opts=None, stats=None):
+    _want(width, "width", 4, _graph_n(handle))
     st = _stream(stream, width)
     if opts is None and stats is None:
         _check(lib.gbbs_widest_path(handle, int(src), _ptr(width), st))
@@ -190,6 +243,7 @@ def gbbs_widest_path(handle, src, width, stream=None, opts=None, stats=None):
 
 
 def gbbs_wbfs(handle, src, dist, stream=None, opts=None, stats=None):
+    _want(dist, "dist", 4, _graph_n(handle))
     st = _stream(stream, dist)
     if opts is None and stats is None:
         _check(lib.gbbs_wbfs(handle, int(src), _ptr(dist), st))
@@ -201,6 +255,7 @@ def gbbs_wbfs(handle, src, dist, stream=None, opts=None, stats=None):
 
 def gbbs_bellman_ford_signed(handle, src, dist, stream=None, opts=None, stats=None):
     """dist: int64[n] (numpy or torch, host or device)."""
+    _want(dist, "dist", 8, _graph_n(handle))
     st = _stream(stream, dist)
     if opts is None and stats is None:
         _check(lib.gbbs_bellman_ford_signed(handle, int(src), _ptr(dist), st))
@@ -213,6 +268,9 @@ def gbbs_bellman_ford_signed(handle, src, dist, stream=None, opts=None, stats=No
 def gbbs_bfs_batch(handle, srcs, dist, parent=None, stream=None, opts=None):
     """dist/parent: (k, n) uint32 arrays (row i = source i), host or device."""
     s = np.ascontiguousarray(srcs, dtype=np.uint32)
+    n = _graph_n(handle)
+    _want(dist, "dist", 4, s.shape[0] * n)
+    _want(parent, "parent", 4, s.shape[0] * n)
     st = _stream(stream, dist, parent)
     if opts is None:
         _check(lib.gbbs_bfs_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), _ptr(parent),
@@ -224,6 +282,7 @@ def gbbs_bfs_batch(handle, srcs, dist, parent=None, stream=None, opts=None):
 
 def gbbs_bellman_ford_batch(handle, srcs, dist, stream=None, opts=None):
     s = np.ascontiguousarray(srcs, dtype=np.uint32)
+    _want(dist, "dist", 4, s.shape[0] * _graph_n(handle))
     st = _stream(stream, dist)
     if opts is None:
         _check(lib.gbbs_bellman_ford_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), st))
@@ -235,6 +294,7 @@ def gbbs_bellman_ford_batch(handle, srcs, dist, stream=None, opts=None):
 def gbbs_wbfs_batch(handle, srcs, dist, stream=None, opts=None):
     """dist: (k, n) device rows."""
     s = np.ascontiguousarray(srcs, dtype=np.uint32)
+    _want(dist, "dist", 4, s.shape[0] * _graph_n(handle))
     st = _stream(stream, dist)
     if opts is None:
         _check(lib.gbbs_wbfs_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(dist), st))
@@ -246,6 +306,7 @@ def gbbs_wbfs_batch(handle, srcs, dist, stream=None, opts=None):
 def gbbs_betweenness_batch(handle, srcs, delta, stream=None, opts=None):
     """delta: (k, n) float64 device rows."""
     s = np.ascontiguousarray(srcs, dtype=np.uint32)
+    _want(delta, "delta", 8, s.shape[0] * _graph_n(handle), kind="float")
     st = _stream(stream, delta)
     if opts is None:
         _check(lib.gbbs_betweenness_batch(handle, s.ctypes.data, int(s.shape[0]), _ptr(delta), st))
@@ -255,6 +316,7 @@ def gbbs_betweenness_batch(handle, srcs, delta, stream=None, opts=None):
 
 
 def gbbs_betweenness(handle, src, delta, stream=None, stats=None, opts=None):
+    _want(delta, "delta", 8, _graph_n(handle), kind="float")
     st = _stream(stream, delta)
     if stats is None and opts is None:
         _check(lib.gbbs_betweenness(handle, int(src), _ptr(delta), st))
@@ -265,7 +327,7 @@ def gbbs_betweenness(handle, src, delta, stream=None, stats=None, opts=None):
 
 
 def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0, neg_scope=0, bsize=0,
-              teams=0):
+              teams=0, rules=0):
     o = gbbs_opts()
     lib.gbbs_default_opts(ctypes.byref(o))
     o.threshold_den = threshold_den
@@ -275,6 +337,7 @@ def make_opts(threshold_den=20, mode=GBBS_MODE_AUTO, ctas_per_sm=0, delta=0, neg
     o.neg_scope = neg_scope
     o.bsize = bsize
     o.teams = teams
+    o.rules = rules
     return o
 
 
@@ -301,7 +364,8 @@ def round_records(stats):
         us = (raw[i + 1].t_start_ns - r.t_start_ns) / 1e3 if i + 1 < len(raw) else None
         out.append(dict(dense=r.dense, bucket=r.bucket, frontier=r.frontier, frontier_edges=r.frontier_edges,
                         acquired=r.acquired, edges_examined=r.edges_examined,
-                        vertices_swept=r.vertices_swept, us=us,
+                        vertices_swept=r.vertices_swept, us=us, alg_bytes=r.alg_bytes,
+                        head_hits=r.head_hits,
                         work_us=(r.t_work_ns - r.t_start_ns) / 1e3,
                         flush_us=(r.t_flush_ns - r.t_start_ns) / 1e3))
     return out

@@ -94,3 +94,22 @@ def test_product_does_not_touch_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 s = open(os.path.join(dp, f)).read()
                 assert "oracle" not in s.lower().replace("no oracle", ""), f
+
+
+def test_binding_validates_arrays_without_gpu(built):
+    """The ctypes binding checks element width and length before an address reaches
+    C, which reads and writes fixed widths (int64 offsets, uint32 targets/weights)."""
+    import numpy as np
+    from paper_1805_05208_b200 import gbbs
+    off = np.array([0, 1, 2], np.int64)
+    tgt = np.array([1, 0], np.uint32)
+    bad = [(off.astype(np.int32), tgt, None),              # 4-byte offsets
+           (off[:2], tgt, None),                           # offsets shorter than n + 1
+           (off, tgt.astype(np.uint64), None),             # 8-byte targets
+           (off, tgt[:1], None),                           # fewer than m targets
+           (off, tgt, np.ones(2, np.float32)),             # float weights
+           (off, tgt, np.ones(3, np.uint32))]              # weights longer than m
+    for o, t, w in bad:
+        with pytest.raises(gbbs.GbbsArgError) as e:
+            gbbs.gbbs_graph_create(2, 2, o, t, w)
+        assert e.value.code == gbbs.GBBS_EINVAL and isinstance(e.value, ValueError)

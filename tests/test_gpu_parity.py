@@ -523,6 +523,34 @@ def test_pull_min_bf_and_widest(G, T):
         g.close()
 
 
+def test_bf_dense_bitmap_forward_default_kernel(G):
+    """GBBS_MODE_DENSE on the default Bellman-Ford / widest-path kernel (the
+    bitmap-forward push of reading A11, a9: the frontier is the TS bitmap, swept
+    by warps) on symmetric rMATs and a directed graph: every round is a bitmap
+    round and distances / widths equal the oracle's."""
+    cfg = graphgen.CONFIGS["c1"]
+    off, tgt = graphgen.rmat_graph(cfg.levels, 1 << cfg.log_edges, cfg.graph_seed, *cfg.abc)
+    cases = [(off, tgt, graphgen.pair_weights(off, tgt, cfg.weight_seed, cfg.W), True)]
+    roff, rtgt = graphgen.rmat_graph(16, 1 << 20, 5, 0.57, 0.19, 0.19)
+    cases.append((roff, rtgt, graphgen.pair_weights(roff, rtgt, 9, 16), True))
+    doff, dtgt = graphgen.rmat_graph(14, 1 << 18, 8, 0.6, 0.15, 0.15, symmetric=False)
+    cases.append((doff, dtgt, graphgen.pair_weights(doff, dtgt, 4, 14), False))
+    for o, t, ww, sym in cases:
+        g = G.Graph(o, t, ww, symmetric=sym)
+        opts = G.make_opts(20, G.GBBS_MODE_DENSE)
+        srcs = [0] + list(graphgen.choose_sources(np.nonzero(np.diff(o) > 0)[0], 2, 31))
+        for src in srcs:
+            d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+            st = G.make_stats(4096)
+            g.bellman_ford(src, d, opts=opts, stats=st)
+            assert (d.cpu().numpy().view(np.uint32) == oracle.dijkstra(o, t, ww, src)[0]).all(), src
+            recs = G.round_records(st)
+            assert recs and all(r["dense"] == 2 for r in recs)
+            g.widest_path(src, d, opts=opts)
+            assert (d.cpu().numpy().view(np.uint32) == oracle.widest_path(o, t, ww, src)).all(), src
+        g.close()
+
+
 def test_block_size_option(G):
     """gbbs_opts.bsize (edgeMapBlocked's block size): every fixed tile size gives the
     same distances as the adaptive default; invalid sizes are rejected."""

@@ -101,6 +101,32 @@ def test_bfs_disconnected_and_directed():
     assert list(p) == [INF, 1, 1, INF, INF]
 
 
+def test_reached_edges_closed_forms():
+    """oracle_reached_edges (the TEPS numerator of reading A20) pinned by closed forms:
+    on a connected symmetric graph (star, path, 3D torus) every vertex is reached, so
+    it equals m; on a disjoint union it equals the source component's degree sum,
+    i.e. twice its undirected edge count; a directed path reached from vertex i
+    carries exactly the n-1-i edges out of i..n-2; an all-INF dist gives 0."""
+    n = 12
+    for edges in ([(0, i) for i in range(1, n)], path_graph(n)):
+        off, tgt = graphgen.from_edge_list(n, edges)
+        d, _ = oracle.bfs(off, tgt, 5)
+        assert oracle.reached_edges(off, d) == tgt.shape[0] == 2 * (n - 1)
+    off, tgt = graphgen.torus3d(4)
+    assert oracle.reached_edges(off, oracle.bfs(off, tgt, 0)[0]) == 6 * 4 ** 3
+    # K_4 on {0..3} (6 edges) + path on {4..9} (5 edges) + isolated 10, 11
+    edges = [(i, j) for i in range(4) for j in range(i + 1, 4)] + [(i, i + 1) for i in range(4, 9)]
+    off, tgt = graphgen.from_edge_list(12, edges)
+    assert oracle.reached_edges(off, oracle.bfs(off, tgt, 2)[0]) == 12
+    assert oracle.reached_edges(off, oracle.bfs(off, tgt, 7)[0]) == 10
+    assert oracle.reached_edges(off, oracle.bfs(off, tgt, 11)[0]) == 0
+    # directed path 0 -> 1 -> ... -> n-1 from vertex i: edges i..n-2 are reached
+    off, tgt = graphgen.from_edge_list(n, path_graph(n), symmetric=False)
+    for i in (0, 4, n - 1):
+        assert oracle.reached_edges(off, oracle.bfs(off, tgt, i)[0]) == n - 1 - i
+    assert oracle.reached_edges(off, np.full(n, INF, np.uint32)) == 0
+
+
 # ---- BFS vs brute force / Floyd–Warshall ------------------------------------------
 
 def test_bfs_all_graphs_on_4_vertices_brute_force():

@@ -11,12 +11,15 @@ import time
 
 import numpy as np
 
+NOPARENT = False
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
 def run_algo(g, algo, s, d, p, opts, st):
-    if algo == "bfs":
+    if algo == "bfs" and NOPARENT:
+        g.bfs(s, d, None, opts=opts, stats=st)
+    elif algo == "bfs":
         g.bfs(s, d, p, opts=opts, stats=st)
     elif algo == "bf":
         g.bellman_ford(s, d, opts=opts, stats=st)
@@ -37,7 +40,11 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--rounds", action="store_true", help="print every round")
     ap.add_argument("--check", action="store_true", help="certify against the oracle certificate")
+    ap.add_argument("--noparent", action="store_true", help="BFS without the parent output")
+    ap.add_argument("--rules", type=int, default=0, help="gbbs_opts.rules (1 = paper's m/T rule only)")
     a = ap.parse_args()
+    global NOPARENT
+    NOPARENT = a.noparent
     import torch
     from graphgen import device as gdev
     from paper_1805_05208_b200 import gbbs
@@ -55,7 +62,7 @@ def main():
         for algo in a.algos.split(","):
             for s in G["sources"][: a.nsrc]:
                 st = gbbs.make_stats(1 << 17)
-                opts = gbbs.make_opts(a.T, mode, delta=a.delta)
+                opts = gbbs.make_opts(a.T, mode, delta=a.delta, rules=a.rules)
                 run_algo(g, algo, s, d, p, opts, st)
                 recs = gbbs.round_records(st)
                 mreach = int((off[1:] - off[:-1])[d != -1].sum())
@@ -66,7 +73,7 @@ def main():
                     kms.append(s2.kernel_ms)
                 km = float(np.median(kms))
                 tot_us = sum(r["us"] or 0 for r in recs)
-                print(f"-- {algo} src={s} rounds={st.rounds} dense={st.dense_rounds} reached={st.reached} "
+                print(f"-- {algo} src={s} alg_bytes={sum(r['alg_bytes'] for r in recs) / 1e6:.1f}MB rounds={st.rounds} dense={st.dense_rounds} reached={st.reached} "
                       f"m_reach={mreach} kernel={km * 1e3:.1f}us (stats run rounds sum {tot_us:.1f}us) "
                       f"GTEPS={mreach / km / 1e6:.1f}", flush=True)
                 if a.rounds or st.rounds <= 40:
@@ -74,7 +81,8 @@ def main():
                         print(f"   r{i:<4d} {'SDFPB'[r['dense']] if r['dense'] < 3 or a.algos.find('wbfs') < 0 else 'BN'[r['dense'] - 3]} k={r['bucket']:<6d} U={r['frontier']:>10d} "
                               f"E={r['frontier_edges']:>11d} acq={r['acquired']:>9d} "
                               f"ex={r['edges_examined']:>11d} sw={r['vertices_swept']:>9d} "
-                              f"{(r['us'] or 0):9.1f}us  work<{r['work_us']:.1f} flush<{r['flush_us']:.1f}")
+                              f"{(r['us'] or 0):9.1f}us  work<{r['work_us']:.1f} flush<{r['flush_us']:.1f} "
+                              f"ab={r['alg_bytes'] / 1e6:.1f}MB hh={r['head_hits']}")
                 else:
                     us = np.array([r["us"] or 0 for r in recs])
                     fr = np.array([r["frontier"] for r in recs])
