@@ -48,6 +48,9 @@ def _nvcc(spec, force=False, log=None):
     res = subprocess.run(cmd, capture_output=True, text=True)
     if log is not None:
         log.write(res.stderr)
+    os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    with open(os.path.join(ROOT, "build", os.path.basename(spec["out"]) + ".ptxas.log"), "w") as f:
+        f.write(res.stderr)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed for {spec['out']}")

@@ -287,8 +287,11 @@ int gbbs_betweenness_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
  *   previous round was dense (the frontier is a bitmap) and the pull's
  *   remaining work, the vertices with in-edges not yet visited, is at most
  *   |U| + sum deg(U); else sparse (push).
- * Bellman-Ford AUTO: always list push; DENSE forces the bitmap-forward push
- *   (the frontier as a bitmap, reading A11), kept as the measured alternative. */
+ * Bellman-Ford AUTO / SPARSE: every round converts the frontier bitmap into a
+ *   list carrying each vertex's distance and pushes it in edge tiles with
+ *   fire-and-forget priority-writes (round kind 5); DENSE forces the
+ *   bitmap-forward push (the frontier as a bitmap, reading A11), kept as the
+ *   measured alternative. */
 #define GBBS_MODE_AUTO 0
 #define GBBS_MODE_SPARSE 1 /* always push                                 */
 #define GBBS_MODE_DENSE 2  /* BFS: always pull; BF: bitmap-forward push   */
@@ -343,7 +346,10 @@ typedef struct {
   int32_t dense;          /* round kind: 0 = list push, 1 = dense pull,
                              2 = bitmap-forward push, 3 = pull-min (BF /
                              widest path, GBBS_MODE_PULL) or, for wBFS, a
-                             bucket list, 4 = wBFS near list (same bucket) */
+                             bucket list, 4 = wBFS near list (same bucket),
+                             5 = Bellman-Ford red round (bitmap -> list with
+                             distances, then a push whose priority-writes
+                             are reductions; frontier = the marked bitmap) */
   int32_t bucket;         /* wBFS: the bucket the round processed; else 0 */
   int64_t frontier;       /* |U|: frontier vertices with out-degree > 0   */
   int64_t frontier_edges; /* sum of out-degrees of U                       */

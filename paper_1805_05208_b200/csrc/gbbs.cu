@@ -64,7 +64,8 @@ struct gbbs_graph {
   uint32_t *tgt = nullptr;
   uint32_t *wgt = nullptr;
   bool own_off = true, own_tgt = true, own_wgt = true;
-  uint2 *pin = nullptr;      // pull records (first in-neighbour, out-degree)
+  uint4 *phot = nullptr;     // pull records: (in0, in1, in2, out-degree)
+  uint4 *pcold = nullptr;    //               (in3, in4, tail)
   uint32_t *nin = nullptr;   // no-in-edge mask (+ padding)
   long long ncand = 0;       // vertices with at least one in-edge
   uint16_t *shadow = nullptr;  // 16-bit distance shadow (BF / widest path)
@@ -136,7 +137,8 @@ static void free_graph(gbbs_graph *g) {
   if (g->own_off) cudaFree(g->off);
   if (g->own_tgt) cudaFree(g->tgt);
   if (g->own_wgt) cudaFree(g->wgt);
-  cudaFree(g->pin);
+  cudaFree(g->phot);
+  cudaFree(g->pcold);
   cudaFree(g->nin);
   cudaFree(g->shadow);
   if (g->in_off && g->in_off != g->off) cudaFree(g->in_off);
@@ -267,22 +269,38 @@ __global__ void k_isolated(const long long *off, const long long *in_off, long l
   if ((threadIdx.x & 31) == 0) iso[v >> 5] = b;
 }
 
-// Pull records and the no-in-edge mask (a8): pin[v] = (first in-neighbour of v
-// in CSC order or INF, out-degree of v saturated to 32 bits); bit v of nin set
-// iff v has no in-edges (or v >= n): such a vertex can never be acquired by a
-// pull, so dense rounds do not sweep it (it cannot be marked visited instead:
-// visited vertices act as the frontier, reading R2).  *ncand counts the others.
+// Pull records and the no-in-edge mask (a8).  The early-exit pull
+// examines v's in-edges in CSC order and stops at the first visited one; on rMAT
+// almost every candidate stops within its first few in-edges (sorted by source,
+// the hubs come first), so those are stored inline and a candidate is decided
+// without first loading its in-offsets and then its in-edges (two dependent HBM
+// round trips per candidate):
+//   hot[v]  = (in0, in1, in2, out-degree)   16 B, read for every candidate
+//   cold[v] = (in3, in4, tail)              16 B, read only when in0..in2 miss
+// where in_k is v's k-th in-neighbour in CSC order (INF past the in-degree) and
+// tail = (in_off[v] + 5) << 24 | min(indeg - 5, 2^24 - 1) (0 if indeg <= 5; a
+// saturated count means: read in_off[v + 1]).  Same edges, same order, same
+// early exit as scanning in_tgt from in_off[v].  Bit v of nin is set iff v has no
+// in-edges (or v >= n): such a vertex can never be acquired by a pull, so dense
+// rounds do not sweep it (it cannot be marked visited instead: visited vertices
+// act as the frontier, reading R2).  *ncand counts the others.
 __global__ void k_pull_records(const long long *off, const long long *in_off,
-                               const uint32_t *in_tgt, long long n, long long nwords, uint2 *pin,
-                               uint32_t *nin, unsigned long long *ncand) {
+                               const uint32_t *in_tgt, long long n, long long nwords, uint4 *hot,
+                               uint4 *cold, uint32_t *nin, unsigned long long *ncand) {
   long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if ((v >> 5) >= nwords) return;
   bool none = true;
   if (v < n) {
     const long long a = in_off[v], b = in_off[v + 1];
     const long long od = off[v + 1] - off[v];
-    none = a == b;
-    pin[v] = make_uint2(none ? INF : in_tgt[a], (uint32_t)min(od, 0xFFFFFFFFll));
+    const long long d = b - a;
+    none = d == 0;
+    uint32_t x[5];
+    for (int k = 0; k < 5; k++) x[k] = k < d ? in_tgt[a + k] : INF;
+    const unsigned long long tail =
+        d > 5 ? ((unsigned long long)(a + 5) << 24) | (unsigned long long)min(d - 5, 0xFFFFFFll) : 0ull;
+    hot[v] = make_uint4(x[0], x[1], x[2], (uint32_t)min(od, 0xFFFFFFFFll));
+    cold[v] = make_uint4(x[3], x[4], (uint32_t)(tail & 0xFFFFFFFFull), (uint32_t)(tail >> 32));
   }
   const unsigned bb = __ballot_sync(0xffffffffu, none);
   if ((threadIdx.x & 31) == 0) {
@@ -459,11 +477,11 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
   CU(cudaGetLastError());
   CU(cudaMalloc(&g->cnt, CNT_WORDS * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8], acq[4]
   CU(cudaMemset(g->cnt, 0, CNT_WORDS * 8));
-  CU(cudaMalloc(&g->pin, (size_t)n * 8));
+  CU(cudaMalloc(&g->phot, (size_t)n * 16));
+  CU(cudaMalloc(&g->pcold, (size_t)n * 16));
   CU(cudaMalloc(&g->nin, (size_t)g->nwords * 4));
-  k_pull_records<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->in_off, g->in_tgt, n,
-                                                                    g->nwords, g->pin, g->nin,
-                                                                    g->cnt + 6);
+  k_pull_records<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(
+      g->off, g->in_off, g->in_tgt, n, g->nwords, g->phot, g->pcold, g->nin, g->cnt + 6);
   CU(cudaGetLastError());
   CU(cudaMemcpy(&g->ncand, g->cnt + 6, 8, cudaMemcpyDeviceToHost));
   g->status = (int *)(g->cnt + 4);
@@ -816,7 +834,8 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   p.ebits = g->ebits;
   p.iso = g->iso;
   p.nin = g->nin;
-  p.pin = g->pin;
+  p.phot = g->phot;
+  p.pcold = g->pcold;
   p.ncand = g->ncand;
   p.rules = (int)o.rules;
   p.shadow = g->shadow;

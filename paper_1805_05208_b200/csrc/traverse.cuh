@@ -99,7 +99,10 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 
 // WP: widest path, (max, min) semiring; WBFS: integral-weight SSSP with buckets
 enum Algo { ALGO_BFS = 0, ALGO_BF = 1, ALGO_WP = 2, ALGO_WBFS = 3 };
-enum Emit { EMIT_LIST = 0, EMIT_COUNT = 1 };
+// EMIT_RED (Bellman-Ford, AUTO/SPARSE): no winners at all — the priority-write is
+// a fire-and-forget reduction and the next frontier is the bitmap of the vertices
+// it may have lowered (see apply_batch)
+enum Emit { EMIT_LIST = 0, EMIT_COUNT = 1, EMIT_RED = 2 };
 enum { LIST_HEAVY = 2 };
 
 struct RoundStat {           // mirrors gbbs_round_stat
@@ -126,7 +129,8 @@ struct Params {
   const uint32_t *in_tgt;
   const uint32_t *iso;       // [nwords] isolated-vertex (+padding) mask
   const uint32_t *nin;       // [nwords] no in-edges (+padding): never a pull candidate
-  const uint2 *pin;          // [n] pull record: (first in-neighbour or INF, out-degree)
+  const uint4 *phot;         // [n] pull records (in0, in1, in2, out-degree), gbbs.cu k_pull_records
+  const uint4 *pcold;        // [n]              (in3, in4, tail offset << 24 | tail count)
   long long ncand;           // vertices with at least one in-edge
   uint32_t *dist;            // [n]
   uint16_t *shadow;          // [n] BF/WP: 16-bit conservative copy of dist
@@ -281,6 +285,15 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *a) {
 #ifndef GBBS_PREFETCH
 #define GBBS_PREFETCH 1
 #endif
+// Bellman-Ford red rounds (EMIT_RED); 0 = the test-and-set list push of round 1
+#ifndef GBBS_BF_RED
+#define GBBS_BF_RED 1
+#endif
+// BFS push pre-check of the visited bit: 0 = L1-cached load (may see a stale word
+// and issue a redundant test-and-set), 1 = L2 load (__ldcg)
+#ifndef GBBS_PRECHECK_CG
+#define GBBS_PRECHECK_CG 0
+#endif
 __device__ __forceinline__ void prefetch_l2(const void *a) {
 #if GBBS_PREFETCH
   asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a));
@@ -289,6 +302,13 @@ __device__ __forceinline__ void prefetch_l2(const void *a) {
 
 __device__ __forceinline__ void st_stream(uint32_t *a, uint32_t v) {
   asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(ef_policy())
+               : "memory");
+}
+
+__device__ __forceinline__ void st_stream_v4(uint32_t *a, uint32_t x, uint32_t y, uint32_t z,
+                                             uint32_t w) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(x),
+               "r"(y), "r"(z), "r"(w), "l"(ef_policy())
                : "memory");
 }
 
@@ -313,6 +333,10 @@ __device__ __forceinline__ void diag_add(const unsigned long long *dbgc, int k,
   }
 }
 #endif
+__device__ __forceinline__ bool vbit(const uint32_t *vis, uint32_t u) {
+  return (vis[u >> 5] >> (u & 31)) & 1u;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -408,7 +432,7 @@ __device__ __forceinline__ void warp_append(const Params &p, int nb, unsigned lo
 // atomicAdd of (count, edge-sum) reserves positions AND their exclusive edge
 // prefix O, so the next round needs no degree scan.  Offsets are loaded FL
 // entries per lane at a time.  Warp-uniform call.
-template <int ALGO>
+template <int ALGO, bool CARRY = false>
 __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, int cnt, int nb,
                                            int r, uint32_t *bits_next,
                                            unsigned long long *tmark = nullptr,
@@ -482,10 +506,12 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
       if (keep) {
         GBBS_CHECK(pos < (unsigned long long)p.n);
         if (abp) *abp += 20;  // STATS: the entry (v, O, base)
-        fv[pos] = vv[u];
+        // CARRY (Bellman-Ford red rounds): the entry carries dist(v) as of the
+        // round's start instead of v, so tiles need no owner-distance loads
+        fv[pos] = CARRY ? ld_relaxed(p.dist + vv[u]) : vv[u];
         fo[pos] = o;
         fb[pos] = lo[u] - o;
-      } else if ((ALGO == ALGO_BF || ALGO == ALGO_WP) && i < cnt) {
+      } else if (!CARRY && (ALGO == ALGO_BF || ALGO == ALGO_WP) && i < cnt) {
         // out-degree-0 vertex: it never enters a frontier; release its TS bit.
         atomicAnd(bits_next + (vv[u] >> 5), ~(1u << (vv[u] & 31)));
       }
@@ -650,7 +676,9 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
 #endif
     uint32_t pre[NB];
 #pragma unroll
-    for (int j = 0; j < NB; j++) pre[j] = act[j] ? prebits[vv[j] >> 5] : FULL;
+    for (int j = 0; j < NB; j++)
+      pre[j] = act[j] ? (GBBS_PRECHECK_CG ? __ldcg(prebits + (vv[j] >> 5)) : prebits[vv[j] >> 5])
+                      : FULL;
 #ifdef GBBS_DIAG_TILE
 #pragma unroll
     for (int j = 0; j < NB; j++) GBBS_DEP(pre[j]);
@@ -663,6 +691,9 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       if (!(pre[j] & bit)) {
         const uint32_t old = atomicOr(bits + (vv[j] >> 5), bit);  // test-and-set
         win[j] = !(old & bit);
+#ifdef GBBS_DIAG_ATOMS  // diagnostic builds: executed test-and-sets in `swept`
+        if (STATS) ws.swept += 1;
+#endif
       }
     }
 #ifdef GBBS_DIAG_TILE
@@ -678,8 +709,10 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
 #pragma unroll
     for (int j = 0; j < NB; j++) {
       if (win[j]) {
+#ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
         st_stream(p.dist + vv[j], (uint32_t)(r + 1));
         if (p.parent) st_stream(p.parent + vv[j], uu[j]);
+#endif
       }
     }
   } else {
@@ -707,6 +740,39 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
         if (ovf && act[j]) atomicOr(p.status, 2);
       }
       cur[j] = act[j] ? (uint32_t)p.shadow[vv[j]] : (ALGO == ALGO_WP ? 0xFFFFu : 0u);
+    }
+    if constexpr (EMIT == EMIT_RED && ALGO == ALGO_BF) {
+      // Fire-and-forget priority-write: red.min on dist (its old value is not
+      // waited for), the shadow lowered to the candidate, and v marked in the
+      // next frontier bitmap with red.or.  The shadow stays an upper bound of the
+      // distance dist(v) reaches this round: it only receives candidates, and
+      // each candidate's red.min is issued before its shadow store.
+      // The shadow is only a pre-filter (racy stores can leave it above dist); a
+      // candidate it passes is confirmed against dist itself, which only falls: a
+      // candidate below the dist value read means dist(v) falls this round, so
+      // every mark is a vertex that improved (and the rounds end)
+      bool pass[NB];
+      uint32_t dv[NB];
+#pragma unroll
+      for (int j = 0; j < NB; j++) {
+        pass[j] = act[j] && nd[j] != INF && (nd[j] < cur[j] || cur[j] == 0xFFFFu);
+        dv[j] = pass[j] ? ld_relaxed(p.dist + vv[j]) : 0u;
+      }
+      bool mk = false;
+#pragma unroll
+      for (int j = 0; j < NB; j++) {
+        if (pass[j] && nd[j] < dv[j]) {
+          atomicMin(p.dist + vv[j], nd[j]);  // result unused: RED.MIN
+          p.shadow[vv[j]] = (uint16_t)min(nd[j], 0xFFFFu);
+          atomicOr(bits + (vv[j] >> 5), 1u << (vv[j] & 31));  // RED.OR
+          mk = true;
+#ifdef GBBS_DIAG_ATOMS
+          if (STATS) ws.swept += 1;
+#endif
+        }
+      }
+      ws.K |= mk;  // any mark: the frontier is not empty
+      return;
     }
     bool cand[NB];
     uint32_t oldv[NB];
@@ -791,6 +857,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
                                                long long E, int nb, int r, uint32_t *bits,
                                                const uint32_t *prebits, int TR) {
   constexpr long long BIG = 0x7FFFFFFFFFFFFFFFll;
+  constexpr bool W = ALGO != ALGO_BFS;  // weights, owner distances
   const int lane = threadIdx.x & 31;
   const long long ts = t * TR;
   const long long te = min(ts + (long long)TR, E);
@@ -799,7 +866,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
   const uint32_t *F = p.fv[lb];
   if (STATS && lane == 0) {
     ws.edges += (unsigned long long)(te - ts);
-    ws.ab += (unsigned long long)(te - ts) * ((ALGO != ALGO_BFS && p.wgt) ? 8 : 4);
+    ws.ab += (unsigned long long)(te - ts) * ((W && p.wgt) ? 8 : 4);
   }
 #ifdef GBBS_DIAG_TILE
   const unsigned long long tT0 = globaltimer_ns();
@@ -833,7 +900,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
     const bool valid = lane < n32;
     if (!valid) Ok = BIG;
     uint32_t Xk = Uk;
-    if (ALGO != ALGO_BFS) Xk = valid ? ld_relaxed(p.dist + Uk) : 0;
+    if (W && EMIT != EMIT_RED) Xk = valid ? ld_relaxed(p.dist + Uk) : 0;
     if (GBBS_PREFETCH && te - ts > 32 * NCH) {
       for (long long cst = ts + 32 * NCH; cst < te; cst += 32) {
         const int c0 = __popc(__ballot_sync(FULL, Ok <= cst)) - 1;
@@ -842,7 +909,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
         const long long bb = __shfl_sync(FULL, Bk, c0 + __popc(hm & lanemask_le()));
         if (cst + lane < te) {
           prefetch_l2(p.tgt + bb + cst + lane);
-          if (ALGO != ALGO_BFS && p.wgt) prefetch_l2(p.wgt + bb + cst + lane);
+          if (W && p.wgt) prefetch_l2(p.wgt + bb + cst + lane);
         }
       }
     }
@@ -868,7 +935,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
           if (act[j]) {
             GBBS_CHECK(bb + e >= 0 && bb + e < p.m);
             vv[j] = ld_stream(p.tgt + bb + e);
-            if (ALGO != ALGO_BFS) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
+            if (W) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
           }
         }
       }
@@ -911,7 +978,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
       cnt_h[h] = __popc(__ballot_sync(FULL, o2[h] < te));
       if (o2[h] < te) {
         w.base[kk] = b2[h];
-        w.own[kk] = (ALGO != ALGO_BFS) ? ld_relaxed(p.dist + u2[h]) : u2[h];
+        w.own[kk] = (W && EMIT != EMIT_RED) ? ld_relaxed(p.dist + u2[h]) : u2[h];
         const long long o = o2[h] - ts;
         w.head[o > 0 ? o : 0] = kk + 1;
       }
@@ -957,7 +1024,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
     for (long long e = ts + 32 * NCH + lane; e < te; e += 32) {
       const long long bb = w.base[w.head[e - ts] - 1];
       prefetch_l2(p.tgt + bb + e);
-      if (ALGO != ALGO_BFS && p.wgt) prefetch_l2(p.wgt + bb + e);
+      if (W && p.wgt) prefetch_l2(p.wgt + bb + e);
     }
   }
   for (long long cs = ts; cs < te; cs += 32 * NCH) {
@@ -976,7 +1043,7 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
         uu[j] = w.own[kk];
         GBBS_CHECK(bb + e >= 0 && bb + e < p.m);
         vv[j] = ld_stream(p.tgt + bb + e);
-        if (ALGO != ALGO_BFS) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
+        if (W) ww[j] = p.wgt ? ld_stream(p.wgt + bb + e) : 1u;
       }
     }
     apply_batch<ALGO, STATS, EMIT>(p, wsm.stage, ws, vv, uu, ww, act, nb, r, bits, prebits);
@@ -1122,7 +1189,7 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
   if (!__any_sync(FULL, fw != 0)) return;
   const int cnt = warp_gather(w, w0, fw);
   if (STATS && lane == 0) ws.swept += cnt;
-  if (ALGO == ALGO_BFS && convert) {
+  if ((ALGO == ALGO_BFS || EMIT == EMIT_RED) && convert) {
     // a10 bitmap -> list: stage the frontier vertices; flushes append them with
     // their edge prefixes to the heavy list, pushed in edge tiles after the barrier
     for (int c0 = 0; c0 < cnt; c0 += 32) {
@@ -1132,8 +1199,8 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
       if (valid) wsm.stage[ws.scnt + lane] = w.cand[c0 + lane];
       ws.scnt += __popc(bal);
       if (ws.scnt > WCAP - 32) {
-        warp_flush<ALGO>(p, wsm.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr,
-                         p.hcnt + (r & 1), STATS ? &ws.ab : nullptr);
+        warp_flush<ALGO, EMIT == EMIT_RED>(p, wsm.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr,
+                                           p.hcnt + (r & 1), STATS ? &ws.ab : nullptr);
         ws.scnt = 0;
       }
     }
@@ -1191,32 +1258,28 @@ static_assert(GBBS_PULL_SW <= SWEEP_WORDS, "pull units are gathered into SweepSm
 #ifndef GBBS_LONG_IN
 #define GBBS_LONG_IN 24
 #endif
+// L2 prefetch of the next candidate batch's hot pull records
+#ifndef GBBS_PULL_PF
+#define GBBS_PULL_PF 1
+#endif
 constexpr int PULL_STEPS = GBBS_PULL_STEPS;
 constexpr int LONG_IN = GBBS_LONG_IN;
 constexpr int PCH = GBBS_PCH;
 
 __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4(p); }
 
-__device__ __forceinline__ bool vbit(const uint32_t *vis, uint32_t u) {
-  return (vis[u >> 5] >> (u & 31)) & 1u;
-}
-
-// Pull record of a candidate: (first in-neighbour, out-degree) in one 8-byte load.
-__device__ __forceinline__ uint2 ld_stream_v2(const uint2 *a) {
-  uint2 v;
-  asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
-      : "=r"(v.x), "=r"(v.y)
-      : "l"(a), "l"(ef_policy()));
-  return v;
-}
 
 // Candidates = the unit's vertices that are unvisited and have in-edges (the
 // no-in-edge mask nin removes vertices no pull can ever acquire).  A candidate's
-// first in-edge comes from its 8-byte pull record, loaded beside its in-offsets:
-// rMAT in-lists are sorted by source, so the first in-neighbour is the lowest
-// id — the likeliest hub, visited early — and most acquisitions are decided
-// without touching the in-edge array.  The scan then continues from the second
-// in-edge in CSC order (same edges, same order, same early exit: P:1870-1874).
+// first five in-edges in CSC order come from its pull records (gbbs.cu
+// k_pull_records): the hot record (in0, in1, in2, out-degree) for every
+// candidate, the cold one (in3, in4, tail) only when in0..in2 miss.  rMAT
+// in-lists are sorted by source, so the first in-neighbours are the lowest ids —
+// the likeliest hubs, visited early — and most candidates are decided by one HBM
+// load and one or two probe steps, without the in-offset -> in-edge chain.  The
+// scan then continues at the tail (in-edge 5 onwards) in CSC order: same edges,
+// same order, same early exit as P:1870-1874 (the probes of in1/in2 and of in3/in4
+// are issued together; the first hit in CSC order is taken).
 // LISTOUT (light pulls, below): acquisitions with out-edges are also staged and
 // flushed into frontier list nb with their edge prefixes, so the next round can
 // push from a list instead of sweeping the bitmap.
@@ -1243,38 +1306,70 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
     uint32_t v[PCH], par[PCH], dgo[PCH];
     long long js[PCH];
     int rem[PCH];
-    uint2 rec[PCH];
-    long long o0[PCH], o1[PCH];
+    uint4 h[PCH];
+    if (GBBS_PULL_PF) {  // the next batch's hot records, into L2 while this one runs
 #pragma unroll
-    for (int q = 0; q < PCH; q++) {
-      const int i = c0 + 32 * q + lane;
-      v[q] = i < cnt ? w.cand[i] : 0;
-      rec[q] = make_uint2(INF, 0);
-      o0[q] = o1[q] = 0;
-      if (i < cnt) {
-        rec[q] = ld_stream_v2(p.pin + v[q]);
-        o0[q] = ld_stream64(p.in_off + v[q]);
-        o1[q] = ld_stream64(p.in_off + v[q] + 1);
+      for (int q = 0; q < PCH; q++) {
+        const int i = c0 + 32 * PCH + 32 * q + lane;
+        if (i < cnt) prefetch_l2(p.phot + w.cand[i]);
       }
     }
 #pragma unroll
     for (int q = 0; q < PCH; q++) {
       const int i = c0 + 32 * q + lane;
+      v[q] = i < cnt ? w.cand[i] : 0;
+      h[q] = make_uint4(INF, INF, INF, 0);
+      if (i < cnt) h[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.phot + v[q]));
+    }
+    bool any2 = false;
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
       par[q] = INF;
       js[q] = 0;
       rem[q] = 0;
-      dgo[q] = rec[q].y;  // out-degree an acquisition adds to the next round's edges
-      if (i < cnt) {
-        if (STATS) {
-          ws.ab += 24;  // pull record + in-offset pair
-          ws.edges += 1;
-        }
-        if (rec[q].x != INF && vbit(vis, rec[q].x)) {
-          par[q] = rec[q].x;
-          if (STATS) ws.hh += 1;
-        } else {
-          js[q] = o0[q] + 1;
-          rem[q] = (int)(o1[q] - js[q]);
+      dgo[q] = h[q].w;  // out-degree an acquisition adds to the next round's edges
+      if (STATS && c0 + 32 * q + lane < cnt) {
+        ws.ab += 16;  // hot record
+        ws.edges += 1;
+      }
+      if (h[q].x != INF && vbit(vis, h[q].x)) {
+        par[q] = h[q].x;
+        if (STATS) ws.hh += 1;
+      }
+      any2 |= par[q] == INF && h[q].y != INF;
+    }
+    if (__any_sync(FULL, any2)) {
+      // in1, in2 probed together with the cold record's load (in3, in4, tail)
+      uint4 cr[PCH];
+      bool m2[PCH];
+#pragma unroll
+      for (int q = 0; q < PCH; q++) {
+        m2[q] = par[q] == INF && h[q].y != INF;
+        cr[q] = make_uint4(INF, INF, 0, 0);
+        if (m2[q] && h[q].z != INF)
+          cr[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pcold + v[q]));
+      }
+#pragma unroll
+      for (int q = 0; q < PCH; q++) {
+        if (!m2[q]) continue;
+        const bool b1 = vbit(vis, h[q].y);
+        const bool b2 = h[q].z != INF && vbit(vis, h[q].z);
+        if (STATS) ws.edges += (b1 || h[q].z == INF) ? 1 : 2;
+        par[q] = b1 ? h[q].y : (b2 ? h[q].z : INF);
+      }
+#pragma unroll
+      for (int q = 0; q < PCH; q++) {
+        if (!m2[q] || par[q] != INF || h[q].z == INF) continue;
+        if (STATS) ws.ab += 16;  // cold record
+        const bool b3 = cr[q].x != INF && vbit(vis, cr[q].x);
+        const bool b4 = cr[q].y != INF && vbit(vis, cr[q].y);
+        if (STATS) ws.edges += (cr[q].x == INF) ? 0 : ((b3 || cr[q].y == INF) ? 1 : 2);
+        par[q] = b3 ? cr[q].x : (b4 ? cr[q].y : INF);
+        const unsigned long long tail = ((unsigned long long)cr[q].w << 32) | cr[q].z;
+        if (par[q] == INF && tail != 0) {
+          js[q] = (long long)(tail >> 24);
+          rem[q] = (int)(tail & 0xFFFFFFull);
+          if (rem[q] == 0xFFFFFF) rem[q] = (int)(ld_stream64(p.in_off + v[q] + 1) - js[q]);
         }
       }
     }
@@ -1686,9 +1781,9 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
     for (long long w0 = gw * sw; w0 < p.nwords; w0 += nw * sw)
       forward_words<ALGO, STATS, EMIT>(p, w, ws, w0, sw, fr, bits, precheck, nb, r, convert);
   }
-  if (ALGO == ALGO_BFS && convert && ws.scnt > 0) {
-    warp_flush<ALGO>(p, w.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr, p.hcnt + (r & 1),
-                     STATS ? &ws.ab : nullptr);
+  if ((ALGO == ALGO_BFS || EMIT == EMIT_RED) && convert && ws.scnt > 0) {
+    warp_flush<ALGO, EMIT == EMIT_RED>(p, w.stage, ws.scnt, LIST_HEAVY, r, nullptr, nullptr,
+                                       p.hcnt + (r & 1), STATS ? &ws.ab : nullptr);
     ws.scnt = 0;
   }
   team_sync<MG>(grid, p.bar, nblk);  // heavy list complete
@@ -1697,6 +1792,11 @@ __device__ __forceinline__ void forward_round(Smem &s, const Params &p, cg::grid
   const unsigned long long hc = s.hcnt;
   const long long hf = (long long)(hc >> p.ebits);
   const long long hE = (long long)(hc & ((1ull << p.ebits) - 1));
+  if (STATS && EMIT == EMIT_RED && threadIdx.x == 0 && blockIdx.x == 0 && p.stats &&
+      r < p.stats_cap) {  // the converted frontier (the round's counter only flags marks)
+    p.stats[r].frontier = hf;
+    p.stats[r].frontier_edges = hE;
+  }
   if (hf > 0)
     list_round<ALGO, STATS, EMIT>(p, w, ws, LIST_HEAVY, hf, hE, nb, r, bits,
                                   (ALGO == ALGO_BFS) ? precheck : bits, gw, nw,
@@ -1729,6 +1829,9 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
   WarpSmem &wsm = s.w[warp];
 
   // a1: per-run init
+#ifdef GBBS_DIAG_NOINIT  // diagnostic builds (results invalid): cost of the fill
+  if (ALGO != ALGO_BFS)
+#endif
   for (long long i = gtid; i < p.n; i += gstride) {
     // BFS/BF: 0 at src, INF elsewhere; widest path: INF (empty path) at src, 0 elsewhere
     if (ALGO == ALGO_WP) {
@@ -1813,6 +1916,9 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     if (ALGO == ALGO_BFS) kind = big ? 1 : (list_valid ? 0 : 2);
     else if (PM && big && p.mode == 3 && p.symmetric) kind = 3;
     else kind = (big || !list_valid) ? 2 : 0;
+    // Bellman-Ford, AUTO / SPARSE: red rounds (the frontier bitmap is converted to a
+    // list with its distances, then pushed with fire-and-forget priority-writes)
+    if (GBBS_BF_RED && ALGO == ALGO_BF && (p.mode == 0 || p.mode == 1)) kind = 5;
     if (GBBS_BID == 0 && tid == 0) {
       p.cnt[(r + 2) & 3] = 0;
       if (ALGO == ALGO_BFS) p.acq[(r + 2) & 3] = 0;
@@ -1862,6 +1968,12 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
         team_sync<MG>(grid, p.bar, GBBS_NBLK);  // every probe of bm[cb] is done: clear it for reuse as TS bits
         for (long long i = gtid; i < p.nwords; i += gstride) p.bm[cb][i] = 0;
       }
+      list_valid = false;
+      emit_count = true;
+    } else if (kind == 5) {  // Bellman-Ford red round
+      if constexpr (ALGO == ALGO_BF)
+        forward_round<ALGO, STATS, EMIT_RED, MG>(s, p, grid, wsm, ws, p.bm[cb], p.bm[nb], nullptr, nb,
+                                                 (int)r, gw, nw, true, GBBS_NBLK);
       list_valid = false;
       emit_count = true;
     } else if (kind == 2) {  // bitmap-forward

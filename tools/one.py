@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--src", type=int, default=0, help="index into the config's sources")
     ap.add_argument("--ctas", type=int, default=0, help="CTAs per SM (0 = max)")
     ap.add_argument("--delta", type=int, default=0, help="wbfs bucket width (0 = default)")
+    ap.add_argument("--noparent", action="store_true", help="BFS without the parent output")
     a = ap.parse_args()
     import torch
     from graphgen import device as gdev
@@ -33,7 +34,7 @@ def main():
     for _ in range(a.reps):
         st = gbbs.make_stats(0)
         if a.algo == "bfs":
-            g.bfs(s, d, p, opts=opts, stats=st)
+            g.bfs(s, d, None if a.noparent else p, opts=opts, stats=st)
         elif a.algo == "bf":
             g.bellman_ford(s, d, opts=opts, stats=st)
         elif a.algo == "wbfs":
