@@ -241,9 +241,15 @@ int gbbs_wbfs(const gbbs_graph *g, uint32_t src, uint32_t *dist,
  *         GBBS_DIST_NEGINF; with neg_scope = 1 exactly the vertices reachable
  *         from such a cycle are GBBS_DIST_NEGINF and the others keep their
  *         finite distance or GBBS_DIST_INF.
- * Cost: O(diam) rounds without a reachable negative cycle; with one, n rounds
- * (the cycle is proven by a frontier that is still non-empty after round
- * n - 1) plus, for neg_scope = 1, one edge pass and a reachability sweep.
+ * Cost: O(diam) rounds without a reachable negative cycle.  With one: from
+ * round 64 on, at every power-of-two round, the parent records of the
+ * relaxations (each a real edge) are checked for a cycle by pointer doubling
+ * (O(n log n) work); a parent cycle whose recorded weights sum below 0 proves
+ * a reachable negative cycle (reading N4) — neg_scope 0 then ends
+ * at once, neg_scope 1 fixes that cycle's forward closure at -infinity and
+ * continues with the other vertices.  Backstop: a frontier still non-empty
+ * after round n - 1 also proves one (then, for neg_scope = 1, one edge pass and
+ * a reachability sweep find every affected vertex).
  * Same stream/synchronization conventions as gbbs_bfs.
  * Errors: GBBS_EINVAL (g or dist NULL, src >= n, bad options), GBBS_ERANGE
  *         if (n - 1) * max|w| >= 2^62, GBBS_ENOMEM (8n bytes of staging for
@@ -270,8 +276,9 @@ int gbbs_wbfs_batch(const gbbs_graph *g, const uint32_t *srcs, int64_t k,
  * gbbs_betweenness_batch — k single-source betweenness computations (sources
  * srcs[0..k), host array) into device rows delta[i*n .. (i+1)*n) (double),
  * the same values as k gbbs_betweenness calls up to fp64 summation order.  The
- * traversals run concurrently, teams per cooperative launch (gbbs_opts.teams
- * in the _ex form; default 1: measured slower with teams, its levels are
+ * traversals are launched back to back on the stream with one synchronisation
+ * at the end (gbbs_opts.teams is accepted and ignored: several betweenness
+ * traversals per launch measured slower at every team count, their levels are
  * throughput-bound).
  * Errors as gbbs_betweenness, plus GBBS_EINVAL for host rows.
  */

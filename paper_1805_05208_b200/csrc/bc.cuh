@@ -511,14 +511,4 @@ __global__ void __launch_bounds__(BLOCK) bc_kernel(const __grid_constant__ BcPar
   bc_body<false>(p, 1);
 }
 
-// G betweenness traversals in one cooperative launch (teams, as traverse_mg_kernel).
-constexpr int BC_GMAX = 8;
-struct MultiBcParams {
-  BcParams ps[BC_GMAX];
-  int G;
-};
-__global__ void __launch_bounds__(BLOCK) bc_mg_kernel(const __grid_constant__ MultiBcParams mp) {
-  bc_body<true>(mp.ps[blockIdx.x % mp.G], mp.G);
-}
-
 }  // namespace gbbs_dev

@@ -91,7 +91,6 @@ struct gbbs_graph {
   unsigned *bar0 = nullptr;          // team 0's barrier words
   int mg_grid[3] = {0, 0, 0};        // co-resident CTAs of traverse_mg_kernel<ALGO>
   int wb_mg_grid = 0;                // co-resident CTAs of wbfs_mg_kernel
-  int bc_mg_grid = 0;                // co-resident CTAs of bc_mg_kernel
   RoundStat *dstats = nullptr;
   long long dstats_cap = 0;
   unsigned long long *dcount = nullptr;
@@ -742,10 +741,6 @@ struct TeamScratch {
   uint32_t *tag = nullptr;
   int nbq = 0;
   unsigned long long qcap = 0;
-  // betweenness state of this team
-  uint32_t *bc_dist = nullptr;
-  double *bc_sigma = nullptr;
-  long long *bc_lvl = nullptr;
 };
 
 static void free_teams(gbbs_graph *g) {
@@ -765,9 +760,6 @@ static void free_teams(gbbs_graph *g) {
     cudaFree(x->wctr);
     for (int i = 0; i < 3; i++) cudaFree(x->xq[i]);
     cudaFree(x->tag);
-    cudaFree(x->bc_dist);
-    cudaFree(x->bc_sigma);
-    cudaFree(x->bc_lvl);
     delete x;
     g->team[t] = nullptr;
   }
@@ -1321,6 +1313,7 @@ extern "C" int gbbs_bellman_ford_signed_ex(const gbbs_graph *cg_, uint32_t src, 
   p.stats_cap = cap;
   p.nwords = g->nwords;
   p.max_rounds = g->n;  // n rounds: a frontier left after them proves a negative cycle
+  p.wq = g->cnt + 10;    // scratch of the early negative-cycle check
   p.ebits = g->ebits;
   p.neg_scope = (int)o.neg_scope;
   p.src = src;
@@ -1513,13 +1506,6 @@ extern "C" int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *
 // ---------------------------------------------------------------------------
 #include "bc.cuh"
 
-// default teams for betweenness batches: 1 — measured (tools/teams_probe.py) c2
-// 23.8 / 24.7 / 28.0 / 32.1 ms and c4 105 / 118 / 134 / 134 ms for 1 / 2 / 4 / 8
-// teams (fp64 fetch-and-adds and random loads: throughput-bound levels)
-#ifndef BC_TEAMS_AUTO
-#define BC_TEAMS_AUTO 1
-#endif
-
 struct BcScratch {
   uint32_t *dist = nullptr;
   double *sigma = nullptr, *delta = nullptr;
@@ -1639,8 +1625,10 @@ extern "C" int gbbs_betweenness_ex(const gbbs_graph *cg_, uint32_t src, double *
   return GBBS_OK;
 }
 
-// Batch of betweenness traversals into device rows, G per launch (teams of
-// bc_mg_kernel, each with its own level, sigma, queue and counters).
+// Batch of betweenness traversals into device rows: the plain kernel per source,
+// launched back to back on the stream (the team form, several traversals per
+// launch, measured slower at every team count — DESIGN.md §6 — and was removed;
+// gbbs_opts.teams is accepted and ignored here).
 extern "C" int gbbs_betweenness_batch_ex(const gbbs_graph *cg_, const uint32_t *srcs, int64_t k,
                                          double *delta, void *cuda_stream,
                                          const gbbs_opts *opts) {
@@ -1655,9 +1643,6 @@ extern "C" int gbbs_betweenness_batch_ex(const gbbs_graph *cg_, const uint32_t *
   if (!is_device_ptr(delta)) return fail(GBBS_EINVAL, "gbbs_betweenness_batch writes device rows");
   gbbs_opts o;
   if (int rc0 = parse_opts(opts, OPTS_BATCH, o)) return rc0;
-  const int G = (int)(o.teams ? o.teams
-                              : ((g->n <= (1ll << 24) && g->m <= (1ll << 28)) ? BC_TEAMS_AUTO : 1));
-  if (G > BC_GMAX) return fail(GBBS_EINVAL, "teams %d > %d", G, BC_GMAX);
   DeviceGuard dguard(g->device);
   if (dguard.rc) return dguard.rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -1665,15 +1650,6 @@ extern "C" int gbbs_betweenness_batch_ex(const gbbs_graph *cg_, const uint32_t *
   int rc = GBBS_OK;
   BcScratch *b = bc_scratch(g, &rc);
   if (!b) return rc;
-  for (int t = 0; t < G; t++) {
-    if ((rc = team_scratch(g, t))) return rc;
-    TeamScratch *x = t ? g->team[t] : nullptr;
-    if (x && !x->bc_dist) {
-      CU(cudaMalloc(&x->bc_dist, n * 4));
-      CU(cudaMalloc(&x->bc_sigma, n * 8));
-      CU(cudaMalloc(&x->bc_lvl, (size_t)b->lvl_cap * 24));
-    }
-  }
   if (g->bstat_cap < k) {
     cudaFree(g->bstat);
     g->bstat = nullptr;
@@ -1681,52 +1657,32 @@ extern "C" int gbbs_betweenness_batch_ex(const gbbs_graph *cg_, const uint32_t *
     CU(cudaMalloc(&g->bstat, (size_t)k * 16));
     g->bstat_cap = k;
   }
-  if (!g->bc_mg_grid) {
-    int nsm = 0, per = 0;
-    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bc_mg_kernel, BLOCK, 0));
-    if (per < 1) return fail(GBBS_ECUDA, "multi-traversal betweenness kernel cannot be resident");
-    g->bc_mg_grid = per * nsm;
-  }
-  for (int64_t i0 = 0; i0 < k; i0 += G) {
-    MultiBcParams mp;
-    memset(&mp, 0, sizeof mp);
-    mp.G = (int)((k - i0) < G ? (k - i0) : G);
-    for (int t = 0; t < mp.G; t++) {
-      BcParams &p = mp.ps[t];
-      TeamScratch *x = t ? g->team[t] : nullptr;
-      p.n = g->n;
-      p.m = g->m;
-      p.off = g->off;
-      p.tgt = g->tgt;
-      p.dist = x ? x->bc_dist : b->dist;
-      p.sigma = x ? x->bc_sigma : b->sigma;
-      p.delta = delta + (i0 + t) * n;
-      p.qv = x ? x->fv[0] : g->fv[0];
-      p.qo = x ? x->fo[0] : g->fo[0];
-      p.qb = x ? x->fb[0] : g->fb[0];
-      p.lvl = x ? x->bc_lvl : b->lvl;
-      p.lvl_cap = b->lvl_cap;
-      p.cnt = x ? x->cnt : g->cnt;
-      p.wq = p.cnt + 10;
-      p.status = (int *)(p.cnt + 4);
-      p.rounds_out = (long long *)(p.cnt + 5);
-      p.bar = x ? x->bar : g->bar0;
-      p.ebits = g->ebits;
-      p.src = srcs[i0 + t];
-      bc_dense(g, o, p);
-    }
-    if (mp.G == 1) {  // the plain kernel (the team form costs ~15 % at G = 1)
-      void *a1[] = {&mp.ps[0]};
-      CU(cudaLaunchCooperativeKernel((const void *)bc_kernel, b->grid, BLOCK, a1, 0, st));
-    } else {
-      void *args[] = {&mp};
-      CU(cudaLaunchCooperativeKernel((const void *)bc_mg_kernel, g->bc_mg_grid, BLOCK, args, 0,
-                                     st));
-    }
-    for (int t = 0; t < mp.G; t++)
-      CU(cudaMemcpyAsync(g->bstat + 2 * (i0 + t), mp.ps[t].status, 16, cudaMemcpyDeviceToDevice,
-                         st));
+  for (int64_t i = 0; i < k; i++) {
+    BcParams p;
+    memset(&p, 0, sizeof p);
+    p.n = g->n;
+    p.m = g->m;
+    p.off = g->off;
+    p.tgt = g->tgt;
+    p.dist = b->dist;
+    p.sigma = b->sigma;
+    p.delta = delta + i * n;
+    p.qv = g->fv[0];
+    p.qo = g->fo[0];
+    p.qb = g->fb[0];
+    p.lvl = b->lvl;
+    p.lvl_cap = b->lvl_cap;
+    p.cnt = g->cnt;
+    p.wq = p.cnt + 10;
+    p.status = (int *)(p.cnt + 4);
+    p.rounds_out = (long long *)(p.cnt + 5);
+    p.bar = g->bar0;
+    p.ebits = g->ebits;
+    p.src = srcs[i];
+    bc_dense(g, o, p);
+    void *a1[] = {&p};
+    CU(cudaLaunchCooperativeKernel((const void *)bc_kernel, b->grid, BLOCK, a1, 0, st));
+    CU(cudaMemcpyAsync(g->bstat + 2 * i, p.status, 16, cudaMemcpyDeviceToDevice, st));
   }
   std::vector<long long> hs((size_t)k * 2);
   CU(cudaMemcpyAsync(hs.data(), g->bstat, (size_t)k * 16, cudaMemcpyDeviceToHost, st));

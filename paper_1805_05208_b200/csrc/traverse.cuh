@@ -242,6 +242,18 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
   return v;
 }
 
+// the 16-bit distance shadow (BF / widest path / wBFS) is read and written by many
+// threads at once: relaxed gpu-scope accesses, never plain ones
+__device__ __forceinline__ uint32_t ld_relaxed16(const uint16_t *p) {
+  unsigned short v;
+  asm volatile("ld.relaxed.gpu.global.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed16(uint16_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u16 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long *p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -288,11 +300,6 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *a) {
 // Bellman-Ford red rounds (EMIT_RED); 0 = the test-and-set list push of round 1
 #ifndef GBBS_BF_RED
 #define GBBS_BF_RED 1
-#endif
-// BFS push pre-check of the visited bit: 0 = L1-cached load (may see a stale word
-// and issue a redundant test-and-set), 1 = L2 load (__ldcg)
-#ifndef GBBS_PRECHECK_CG
-#define GBBS_PRECHECK_CG 0
 #endif
 __device__ __forceinline__ void prefetch_l2(const void *a) {
 #if GBBS_PREFETCH
@@ -677,8 +684,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     uint32_t pre[NB];
 #pragma unroll
     for (int j = 0; j < NB; j++)
-      pre[j] = act[j] ? (GBBS_PRECHECK_CG ? __ldcg(prebits + (vv[j] >> 5)) : prebits[vv[j] >> 5])
-                      : FULL;
+      pre[j] = act[j] ? ld_relaxed(prebits + (vv[j] >> 5)) : FULL;  // words others fetch-or
 #ifdef GBBS_DIAG_TILE
 #pragma unroll
     for (int j = 0; j < NB; j++) GBBS_DEP(pre[j]);
@@ -739,7 +745,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
         nd[j] = ovf ? INF : sum;
         if (ovf && act[j]) atomicOr(p.status, 2);
       }
-      cur[j] = act[j] ? (uint32_t)p.shadow[vv[j]] : (ALGO == ALGO_WP ? 0xFFFFu : 0u);
+      cur[j] = act[j] ? ld_relaxed16(p.shadow + vv[j]) : (ALGO == ALGO_WP ? 0xFFFFu : 0u);
     }
     if constexpr (EMIT == EMIT_RED && ALGO == ALGO_BF) {
       // Fire-and-forget priority-write: red.min on dist (its old value is not
@@ -763,7 +769,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       for (int j = 0; j < NB; j++) {
         if (pass[j] && nd[j] < dv[j]) {
           atomicMin(p.dist + vv[j], nd[j]);  // result unused: RED.MIN
-          p.shadow[vv[j]] = (uint16_t)min(nd[j], 0xFFFFu);
+          st_relaxed16(p.shadow + vv[j], min(nd[j], 0xFFFFu));
           atomicOr(bits + (vv[j] >> 5), 1u << (vv[j] & 31));  // RED.OR
           mk = true;
 #ifdef GBBS_DIAG_ATOMS
@@ -797,7 +803,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     }
 #pragma unroll
     for (int j = 0; j < NB; j++)
-      if (cand[j]) p.shadow[vv[j]] = (uint16_t)min(nd[j], 0xFFFFu);
+      if (cand[j]) st_relaxed16(p.shadow + vv[j], min(nd[j], 0xFFFFu));
     if constexpr (ALGO == ALGO_WBFS) {
       wbfs_stage<STATS, NB>(p, ws, st, cand, vv, nd, oldv, r);
       return;
@@ -1652,7 +1658,7 @@ __device__ __forceinline__ void pullmin_words(const Params &p, WarpSmem &wsm, lo
       const bool imp = (ALGO == ALGO_WP) ? best > cur : best < cur;
       if (imp) {  // only v's owner writes dist[v]
         p.dist[v] = best;
-        p.shadow[v] = (uint16_t)min(best, 0xFFFFu);
+        st_relaxed16(p.shadow + v, min(best, 0xFFFFu));
         atomicOr(&w.found[(v >> 5) - (uint32_t)w0], 1u << (v & 31));
         const long long dgo = je - js;  // symmetric: out-degree = in-degree
         if (dgo > 0) {

@@ -110,6 +110,56 @@ def test_c2_signed_johnson_full(G):
     g.close()
 
 
+def test_c2_planted_negative_cycle_early(G):
+    """NEXT-4 early negative-cycle check (reading N4) at c2 size: c2 plus a directed
+    appendage src -> a, a -> b -> c -> a (weights 1, 1, -5: a negative cycle) and a
+    chain of K vertices hanging off c.  Without the early check the proof takes n
+    rounds (~4.2 M); with it the call ends at the first power-of-two round >= 64.
+    Expected values (no oracle run at n rounds): scope 0 every entry -inf (N1);
+    scope 1 the appendage -inf (it is the cycle's forward closure) and every
+    original vertex its Dijkstra distance on c2 (no appendage edge leads back)."""
+    D, H = build("c2", True)
+    n0, s = D["n"], D["sources"][0]
+    off, tgt, w = H["off"], H["tgt"], H["w"]
+    K = 1000
+    a, b, c = n0, n0 + 1, n0 + 2
+    # insert s -> a at the end of s's list (a is the largest id), then the appendage
+    pos = int(off[s + 1])
+    tgt2 = np.concatenate([tgt[:pos], [a], tgt[pos:]]).astype(np.uint32)
+    w2 = np.concatenate([w[:pos], [3], w[pos:]]).astype(np.uint32)
+    off2 = off.copy()
+    off2[s + 1:] += 1
+    app = [(a, b, 1), (b, c, 1), (c, a, -5), (c, n0 + 3, 2)]
+    app += [(n0 + 3 + i, n0 + 4 + i, 2) for i in range(K - 4)]
+    n = n0 + K
+    deg = np.zeros(K, np.int64)
+    for x, _, _ in app:
+        deg[x - n0] += 1
+    app.sort()
+    off2 = np.concatenate([off2, off2[-1] + np.cumsum(deg)])
+    tgt2 = np.concatenate([tgt2, np.array([y for _, y, _ in app], np.uint32)])
+    w2 = np.concatenate([w2, np.array([x for _, _, x in app], np.int64).astype(np.int32).view(np.uint32)])
+    assert off2.shape[0] == n + 1 and off2[-1] == tgt2.shape[0]
+    g = G.Graph(off2, tgt2, w2)
+    ref = oracle.dijkstra64(off, tgt, w, s)[0]
+    fin = ref != np.uint64(0xFFFFFFFFFFFFFFFF)
+    exp1 = np.full(n, np.iinfo(np.int64).max, np.int64)
+    exp1[:n0][fin] = ref[fin].astype(np.int64)
+    exp1[n0:] = np.iinfo(np.int64).min
+    for scope in (0, 1):
+        st = G.make_stats(0)
+        d = torch.empty(n, dtype=torch.int64, device="cuda")
+        g.bellman_ford_signed(s, d, opts=G.make_opts(neg_scope=scope), stats=st)
+        got = d.cpu().numpy()
+        if scope == 0:
+            assert (got == np.iinfo(np.int64).min).all()
+        else:
+            assert (got == exp1).all()
+        assert st.rounds <= 256, st.rounds          # ended by the early check, not n rounds
+        assert st.kernel_ms < 1000.0, st.kernel_ms
+    g.close()
+
+
 def test_c3_full(G):
     D, H = build("c3", True)
     g = G.Graph(D["offsets"], D["targets"], D["weights"], symmetric=True)
