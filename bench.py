@@ -468,6 +468,10 @@ def run_ours(args, rank, world, local):
             # every relaxation probes the 16-bit distance shadow at a random address;
             # tools/gather_bench.cu measured 270 G random 2-byte L2 gathers/s on this B200
             "relax_vs_l2_gather_ceiling": round(bf_relax / (bf["kernel_ms"] * 1e-3) / 1e9 / 270.0, 4),
+            # ncu dram read+write per launch (mean over the config's sources, committed capture)
+            "traffic": ncu_traffic(bcfg.name, "bf"),
+            "traffic_vs_alg_bytes": (round(ncu_traffic(bcfg.name, "bf") / (bf["alg"] / len(bsrc)), 3)
+                                     if ncu_traffic(bcfg.name, "bf") else None),
             "clocks": bf["clocks"], "rounds": [v["rounds"] for v in bf["per"].values()]}
         for key, note in (("wbfs", "NEXT-2: integral-weight SSSP over distance buckets (bucket width "
                                    "1), same graph and weights as the Bellman-Ford leg"),

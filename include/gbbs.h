@@ -56,7 +56,11 @@ extern "C" {
 #define GBBS_SYMMETRIC 0x1u
 /* Use device arrays in place (zero copy).  The caller keeps offsets, targets
  * and weights alive and unmodified until gbbs_graph_destroy.  Host pointers
- * with this flag are an error (GBBS_EINVAL). */
+ * with this flag are an error (GBBS_EINVAL).  Dense rounds of symmetric graphs
+ * read targets in aligned 16-byte groups, so a borrowed targets array must be
+ * readable up to the next 16-byte boundary past targets[m - 1] (true of any
+ * cudaMalloc or PyTorch allocation, whose sizes are rounded up to 512 bytes);
+ * a targets pointer that is not 16-byte aligned is copied instead. */
 #define GBBS_BORROW 0x2u
 /* Skip the O(n+m) device validation of the CSR (offsets/targets). */
 #define GBBS_NO_VALIDATE 0x4u

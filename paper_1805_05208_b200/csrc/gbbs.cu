@@ -349,8 +349,9 @@ static int occupancy_grid(int *grid) {
   return GBBS_OK;
 }
 
-static int copy_in(void **dst, const void *src, size_t bytes) {
-  CU(cudaMalloc(dst, bytes ? bytes : 16));
+// pad: extra bytes allocated past the copy (the in-edge group loads of a8)
+static int copy_in(void **dst, const void *src, size_t bytes, size_t pad = 0) {
+  CU(cudaMalloc(dst, bytes + pad ? bytes + pad : 16));
   if (bytes) CU(cudaMemcpy(*dst, src, bytes, cudaMemcpyDefault));
   return GBBS_OK;
 }
@@ -375,15 +376,17 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
     g->off = (long long *)offsets;
     g->tgt = (uint32_t *)targets;
     g->wgt = (uint32_t *)weights;
-    // dense rounds read in-edges with 16-byte vector loads: copy a misaligned array
+    // dense rounds read in-edges with 16-byte vector loads of aligned groups of
+    // 4 (the last group may extend up to 12 bytes past targets[m - 1]: see
+    // GBBS_BORROW in gbbs.h): copy a misaligned array
     if (((uintptr_t)targets & 15) != 0) {
       g->tgt = nullptr;
       g->own_tgt = true;
-      if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4))) return rc;
+      if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4, 16))) return rc;
     }
   } else {
     if ((rc = copy_in((void **)&g->off, offsets, (size_t)(n + 1) * 8))) return rc;
-    if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4))) return rc;
+    if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4, 16))) return rc;
     if (weights && (rc = copy_in((void **)&g->wgt, weights, (size_t)m * 4))) return rc;
   }
   // endpoints
@@ -424,7 +427,7 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
     g->in_tgt = g->tgt;
   } else {
     CU(cudaMalloc(&g->in_off, (size_t)(n + 1) * 8));
-    CU(cudaMalloc(&g->in_tgt, (size_t)(m ? m : 1) * 4));
+    CU(cudaMalloc(&g->in_tgt, (size_t)(m ? m : 1) * 4 + 16));  // + the group loads' pad
     if (m == 0) {
       CU(cudaMemset(g->in_off, 0, (size_t)(n + 1) * 8));
     } else {

@@ -46,3 +46,26 @@ print("stall reasons:", ", ".join(f"{k[6:]} {100 * v / sum(allst.values()):.1f}%
 for ln, s in agg.most_common(top):
     t = ", ".join(f"{k[6:]} {v}" for k, v in st[ln].most_common(2))
     print(f"{100 * s / tot:5.1f}% {ln:8s} {src[ln]:88s} {t}")
+
+# --regions SRC: stall samples of file block 0 summed per enclosing function of SRC
+if "--regions" in sys.argv:
+    import re
+    srcf = sys.argv[sys.argv.index("--regions") + 1]
+    starts = []
+    for i, line in enumerate(open(srcf), 1):
+        mt = re.match(r"^(?:__device__|__global__)[^(]*?(\w+)\(", line)
+        if mt:
+            starts.append((i, mt.group(1)))
+    reg = collections.Counter()
+    for ln, sm in agg.items():
+        blk, num = ln.split(":")
+        if blk != "0":
+            reg["(other files)"] += sm
+            continue
+        name = "(top)"
+        for st0, nm in starts:
+            if st0 <= int(num):
+                name = nm
+        reg[name] += sm
+    for k, v in reg.most_common(20):
+        print(f"{100 * v / tot:5.1f}% {k}")
