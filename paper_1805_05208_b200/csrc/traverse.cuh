@@ -319,6 +319,27 @@ __device__ __forceinline__ void st_stream_v4(uint32_t *a, uint32_t x, uint32_t y
                : "memory");
 }
 
+// Stores of an acquired vertex's dist / parent (scattered 4-byte writes).
+// GBBS_STATE_ST: 0 = L2 evict-first, 1 = default policy, 2 = L2 evict-last
+#ifndef GBBS_STATE_ST
+#define GBBS_STATE_ST 0
+#endif
+__device__ __forceinline__ unsigned long long el_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_state(uint32_t *a, uint32_t v) {
+#if GBBS_STATE_ST == 0
+  st_stream(a, v);
+#elif GBBS_STATE_ST == 2
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(el_policy())
+               : "memory");
+#else
+  *a = v;
+#endif
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -716,8 +737,8 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     for (int j = 0; j < NB; j++) {
       if (win[j]) {
 #ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
-        st_stream(p.dist + vv[j], (uint32_t)(r + 1));
-        if (p.parent) st_stream(p.parent + vv[j], uu[j]);
+        st_state(p.dist + vv[j], (uint32_t)(r + 1));
+        if (p.parent) st_state(p.parent + vv[j], uu[j]);
 #endif
       }
     }
@@ -1490,8 +1511,8 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
         const uint32_t vq = v[q];
         if (STATS && (!LISTOUT || dgo[q] == 0)) ws.acquired += 1;  // LISTOUT: staged ones at flush
 #ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
-        st_stream(p.dist + vq, (uint32_t)(r + 1));
-        if (p.parent) st_stream(p.parent + vq, par[q]);
+        st_state(p.dist + vq, (uint32_t)(r + 1));
+        if (p.parent) st_state(p.parent + vq, par[q]);
 #endif
         atomicOr(&w.found[(vq >> 5) - (uint32_t)w0], 1u << (vq & 31));
         if (!LISTOUT && dgo[q] > 0) {
