@@ -360,7 +360,9 @@ typedef struct {
                              bucket list, 4 = wBFS near list (same bucket),
                              5 = Bellman-Ford red round (bitmap -> list with
                              distances, then a push whose priority-writes
-                             are reductions; frontier = the marked bitmap) */
+                             are reductions; frontier = the marked bitmap),
+                             6 = BFS list push run by one CTA alone (solo
+                             round: |U| + sum deg(U) <= 512) */
   int32_t bucket;         /* wBFS: the bucket the round processed; else 0 */
   int64_t frontier;       /* |U|: frontier vertices with out-degree > 0   */
   int64_t frontier_edges; /* sum of out-degrees of U                       */
@@ -436,6 +438,14 @@ int gbbs_widest_path_ex(const gbbs_graph *g, uint32_t src, uint32_t *width,
 /* Launch geometry of the persistent traversal kernel on this device:
  * *ctas = co-resident CTAs used, *threads = threads per CTA. */
 int gbbs_launch_info(const gbbs_graph *g, int32_t *ctas, int32_t *threads);
+
+/* gbbs_graph_in_edges — copy the handle's in-edge CSC (the transpose the dense
+ * pull reads, P:1870-1874 sec:prelims) into caller-owned buffers, host or
+ * device: in_offsets int64[n+1], in_sources uint32[m] (each in-list ascending
+ * by source id).  For a GBBS_SYMMETRIC graph this is the CSR itself.  Either
+ * pointer may be NULL (not copied).  Synchronous.
+ * Errors: GBBS_EINVAL (g NULL), GBBS_ECUDA. */
+int gbbs_graph_in_edges(const gbbs_graph *g, int64_t *in_offsets, uint32_t *in_sources);
 
 /* Thread-local message describing the last error on this thread ("" if none). */
 const char *gbbs_last_error(void);

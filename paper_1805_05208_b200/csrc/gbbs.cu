@@ -1,13 +1,12 @@
 // gbbs.cu — libgbbs: the C ABI declared in include/gbbs.h.
 //
 // Host side of the library: graph residency (copy/borrow, device validation,
-// in-edge CSC by device radix sort), per-handle scratch, and the launch of the
+// in-edge CSC by a hand-written counting transpose, csc.cuh), per-handle scratch, and the launch of the
 // persistent traversal kernel (traverse.cuh) for gbbs_bfs / gbbs_bellman_ford.
 // No torch types, no exceptions across the ABI, no CPU fallback: every step of
 // a traversal runs in the kernels of this file and traverse.cuh.
 #include <cuda_runtime.h>
 
-#include <cub/device/device_radix_sort.cuh>
 #include <cstdarg>
 #include <cstdio>
 #include <cstddef>
@@ -17,6 +16,7 @@
 
 #include "../../include/gbbs.h"
 #include "traverse.cuh"
+#include "csc.cuh"
 #include "sbf.cuh"
 
 using namespace gbbs_dev;
@@ -52,7 +52,7 @@ extern "C" const char *gbbs_last_error(void) { return g_last_error.c_str(); }
 // ---------------------------------------------------------------------------
 // control words per traversal scratch: packed counter ring [4], status, rounds,
 // count, -, heavy-list counters [2], work queues [8], acquisition ring [4]
-constexpr int CNT_WORDS = 22;
+constexpr int CNT_WORDS = 24;
 
 struct gbbs_graph {
   int device = 0;
@@ -222,37 +222,6 @@ __global__ void k_heavy_bits(const long long *off, long long n, long long nwords
   const bool h = v < n && off[v + 1] - off[v] > WBFS_HEAVY;
   const unsigned b = __ballot_sync(0xffffffffu, h);
   if ((threadIdx.x & 31) == 0) hv[v >> 5] = b;
-}
-
-// key = target << 32 | source for every edge; one warp per source vertex.
-__global__ void k_transpose_keys(const long long *off, const uint32_t *tgt, long long n,
-                                 unsigned long long *keys) {
-  long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  int lane = threadIdx.x & 31;
-  for (long long u = warp; u < n; u += nwarps) {
-    long long a = off[u], b = off[u + 1];
-    for (long long e = a + lane; e < b; e += 32)
-      keys[e] = ((unsigned long long)tgt[e] << 32) | (unsigned long long)u;
-  }
-}
-
-// From keys sorted by (target, source): in_tgt = source, in_off[v] = first index with target v.
-__global__ void k_csc_from_keys(const unsigned long long *keys, long long n, long long m,
-                                uint32_t *in_tgt, long long *in_off) {
-  long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long gs = (long long)gridDim.x * blockDim.x;
-  for (long long i = gt; i < m; i += gs) {
-    unsigned long long k = keys[i];
-    long long v = (long long)(k >> 32);
-    in_tgt[i] = (uint32_t)(k & 0xFFFFFFFFull);
-    long long pv = (i == 0) ? -1 : (long long)(keys[i - 1] >> 32);
-    for (long long x = pv + 1; x <= v; x++) in_off[x] = i;
-  }
-  if (gt == 0) {
-    long long last = (m == 0) ? -1 : (long long)(keys[m - 1] >> 32);
-    for (long long x = last + 1; x <= n; x++) in_off[x] = m;
-  }
 }
 
 // Bit v of word v/32 set iff v has no in- and no out-edges (or v >= n, padding):
@@ -431,31 +400,7 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
     if (m == 0) {
       CU(cudaMemset(g->in_off, 0, (size_t)(n + 1) * 8));
     } else {
-      unsigned long long *k0 = nullptr, *k1 = nullptr;
-      void *tmp = nullptr;
-      size_t tmp_bytes = 0;
-      CU(cudaMalloc(&k0, (size_t)m * 8));
-      cudaError_t e1 = cudaMalloc(&k1, (size_t)m * 8);
-      if (e1 != cudaSuccess) {
-        cudaFree(k0);
-        return fail(GBBS_ENOMEM, "CSC sort buffer: %s", cudaGetErrorString(e1));
-      }
-      k_transpose_keys<<<4736, 256>>>(g->off, g->tgt, n, k0);
-      cub::DoubleBuffer<unsigned long long> db(k0, k1);
-      int end_bit = 32 + bits_for((unsigned long long)(n - 1));
-      cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, m, 0, end_bit);
-      cudaError_t e2 = cudaMalloc(&tmp, tmp_bytes);
-      if (e2 == cudaSuccess) {
-        e2 = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, m, 0, end_bit);
-        if (e2 == cudaSuccess) {
-          k_csc_from_keys<<<4736, 256>>>(db.Current(), n, m, g->in_tgt, g->in_off);
-          e2 = cudaGetLastError();
-        }
-        if (e2 == cudaSuccess) e2 = cudaDeviceSynchronize();
-      }
-      cudaFree(tmp);
-      cudaFree(k0);
-      cudaFree(k1);
+      const cudaError_t e2 = gbbs_csc::build_csc(g->off, g->tgt, n, m, g->in_off, g->in_tgt);
       if (e2 != cudaSuccess)
         return fail(e2 == cudaErrorMemoryAllocation ? GBBS_ENOMEM : GBBS_ECUDA, "CSC build: %s",
                     cudaGetErrorString(e2));
@@ -477,7 +422,7 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
   CU(cudaMalloc(&g->iso, (size_t)g->nwords * 4));
   k_isolated<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->in_off, n, g->nwords, g->iso);
   CU(cudaGetLastError());
-  CU(cudaMalloc(&g->cnt, CNT_WORDS * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8], acq[4]
+  CU(cudaMalloc(&g->cnt, CNT_WORDS * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8], acq[4], solo[2]
   CU(cudaMemset(g->cnt, 0, CNT_WORDS * 8));
   CU(cudaMalloc(&g->phot, (size_t)n * 16));
   CU(cudaMalloc(&g->pcold, (size_t)n * 16));
@@ -540,6 +485,22 @@ extern "C" void gbbs_default_opts(gbbs_opts *o) {
   memset(o, 0, sizeof *o);
   o->threshold_den = 20;
   o->mode = GBBS_MODE_AUTO;
+}
+
+extern "C" int gbbs_graph_in_edges(const gbbs_graph *g, int64_t *in_offsets,
+                                   uint32_t *in_sources) {
+  if (!g) return fail(GBBS_EINVAL, "g is NULL");
+  int prev = 0;
+  CU(cudaGetDevice(&prev));
+  CU(cudaSetDevice(g->device));
+  cudaError_t e = cudaSuccess;
+  if (in_offsets)
+    e = cudaMemcpy(in_offsets, g->in_off, (size_t)(g->n + 1) * 8, cudaMemcpyDefault);
+  if (e == cudaSuccess && in_sources && g->m > 0)
+    e = cudaMemcpy(in_sources, g->in_tgt, (size_t)g->m * 4, cudaMemcpyDefault);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(GBBS_ECUDA, "in-edge copy: %s", cudaGetErrorString(e));
+  return GBBS_OK;
 }
 
 extern "C" int gbbs_launch_info(const gbbs_graph *g, int32_t *ctas, int32_t *threads) {
@@ -821,6 +782,7 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   p.hcnt = g->cnt + 8;
   p.wq = g->cnt + 10;
   p.acq = g->cnt + 18;
+  p.solo = g->cnt + 22;
   p.status = g->status;
   p.rounds_out = g->rounds;
   p.nwords = g->nwords;
@@ -860,6 +822,7 @@ static void fill_params_team(gbbs_graph *g, int algo, uint32_t src, uint32_t *dd
   p.hcnt = x->cnt + 8;
   p.wq = x->cnt + 10;
   p.acq = x->cnt + 18;
+  p.solo = x->cnt + 22;
   p.status = (int *)(x->cnt + 4);
   p.rounds_out = (long long *)(x->cnt + 5);
   p.shadow = x->shadow;

@@ -32,7 +32,7 @@ EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_b
            "gbbs_bfs_batch_ex", "gbbs_bellman_ford_batch_ex", "gbbs_wbfs_batch",
            "gbbs_wbfs_batch_ex", "gbbs_betweenness_batch", "gbbs_betweenness_batch_ex",
            "gbbs_betweenness", "gbbs_betweenness_ex", "gbbs_default_opts",
-           "gbbs_launch_info", "gbbs_last_error")
+           "gbbs_launch_info", "gbbs_graph_in_edges", "gbbs_last_error")
 
 
 class GbbsError(RuntimeError):
@@ -103,6 +103,9 @@ def _load():
     lib.gbbs_default_opts.argtypes = [ctypes.POINTER(gbbs_opts)]
     lib.gbbs_default_opts.restype = None
     lib.gbbs_launch_info.argtypes = [p, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    if hasattr(lib, "gbbs_graph_in_edges"):  # aux (test) call; absent in older dev builds
+        lib.gbbs_graph_in_edges.argtypes = [p, p, p]
+        lib.gbbs_graph_in_edges.restype = ctypes.c_int
     lib.gbbs_last_error.argtypes = []
     lib.gbbs_last_error.restype = ctypes.c_char_p
     for f in ("gbbs_graph_create", "gbbs_graph_info", "gbbs_bfs", "gbbs_bellman_ford", "gbbs_bfs_ex",
@@ -399,6 +402,15 @@ class Graph:
 
     def __exit__(self, *a):
         self.close()
+
+    def in_edges(self):
+        """The handle's in-edge CSC as host numpy arrays (in_offsets int64[n+1],
+        in_sources uint32[m]); gbbs_graph_in_edges."""
+        import numpy as np
+        off = np.empty(self.n + 1, dtype=np.int64)
+        src = np.empty(max(self.m, 1), dtype=np.uint32)
+        _check(lib.gbbs_graph_in_edges(self.handle, off.ctypes.data, src.ctypes.data))
+        return off, src[:self.m]
 
     def launch_info(self):
         c, t = ctypes.c_int32(), ctypes.c_int32()
