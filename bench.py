@@ -270,7 +270,7 @@ def run_ours(args, rank, world, local):
             out[s] = dict(m_reach=reach, rounds=st.rounds, dense_rounds=st.dense_rounds,
                           alg_bytes=alg, state_bytes=state,
                           relax=sum(r["edges_examined"] for r in recs),
-                          kinds="".join("SDFPBRs"[min(r["dense"], 6)] for r in recs))
+                          kinds="".join("SDFPBR"[min(r["dense"], 5)] for r in recs))
         return out
 
     def timed(G, algo, opts, steps, warmup, rows, prows):

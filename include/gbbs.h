@@ -360,9 +360,7 @@ typedef struct {
                              bucket list, 4 = wBFS near list (same bucket),
                              5 = Bellman-Ford red round (bitmap -> list with
                              distances, then a push whose priority-writes
-                             are reductions; frontier = the marked bitmap),
-                             6 = BFS list push run by one CTA alone (solo
-                             round: |U| + sum deg(U) <= 512) */
+                             are reductions; frontier = the marked bitmap) */
   int32_t bucket;         /* wBFS: the bucket the round processed; else 0 */
   int64_t frontier;       /* |U|: frontier vertices with out-degree > 0   */
   int64_t frontier_edges; /* sum of out-degrees of U                       */

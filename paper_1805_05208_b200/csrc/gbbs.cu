@@ -52,7 +52,7 @@ extern "C" const char *gbbs_last_error(void) { return g_last_error.c_str(); }
 // ---------------------------------------------------------------------------
 // control words per traversal scratch: packed counter ring [4], status, rounds,
 // count, -, heavy-list counters [2], work queues [8], acquisition ring [4]
-constexpr int CNT_WORDS = 24;
+constexpr int CNT_WORDS = 22;
 
 struct gbbs_graph {
   int device = 0;
@@ -422,7 +422,7 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
   CU(cudaMalloc(&g->iso, (size_t)g->nwords * 4));
   k_isolated<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(g->off, g->in_off, n, g->nwords, g->iso);
   CU(cudaGetLastError());
-  CU(cudaMalloc(&g->cnt, CNT_WORDS * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8], acq[4], solo[2]
+  CU(cudaMalloc(&g->cnt, CNT_WORDS * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8], acq[4]
   CU(cudaMemset(g->cnt, 0, CNT_WORDS * 8));
   CU(cudaMalloc(&g->phot, (size_t)n * 16));
   CU(cudaMalloc(&g->pcold, (size_t)n * 16));
@@ -782,7 +782,6 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   p.hcnt = g->cnt + 8;
   p.wq = g->cnt + 10;
   p.acq = g->cnt + 18;
-  p.solo = g->cnt + 22;
   p.status = g->status;
   p.rounds_out = g->rounds;
   p.nwords = g->nwords;
@@ -822,7 +821,6 @@ static void fill_params_team(gbbs_graph *g, int algo, uint32_t src, uint32_t *dd
   p.hcnt = x->cnt + 8;
   p.wq = x->cnt + 10;
   p.acq = x->cnt + 18;
-  p.solo = x->cnt + 22;
   p.status = (int *)(x->cnt + 4);
   p.rounds_out = (long long *)(x->cnt + 5);
   p.shadow = x->shadow;

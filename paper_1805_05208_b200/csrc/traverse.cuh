@@ -152,7 +152,6 @@ struct Params {
   long long dense_threshold; // dense iff |U| + sum deg(U) > dense_threshold
   long long max_rounds;
   unsigned long long *acq;   // BFS: ring [4] of per-round acquisition counts (reading A10b)
-  unsigned long long *solo;  // BFS solo rounds: [0] next round, [1] acquisitions so far
   int ebits;
   int mode;                  // 0 auto, 1 sparse, 2 dense, 3 pull
   int rules;                 // gbbs_opts.rules (GBBS_RULE_PAPER_ONLY = 1)
@@ -318,27 +317,6 @@ __device__ __forceinline__ void st_stream_v4(uint32_t *a, uint32_t x, uint32_t y
   asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(x),
                "r"(y), "r"(z), "r"(w), "l"(ef_policy())
                : "memory");
-}
-
-// Stores of an acquired vertex's dist / parent (scattered 4-byte writes).
-// GBBS_STATE_ST: 0 = L2 evict-first, 1 = default policy, 2 = L2 evict-last
-#ifndef GBBS_STATE_ST
-#define GBBS_STATE_ST 0
-#endif
-__device__ __forceinline__ unsigned long long el_policy() {
-  unsigned long long pol;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void st_state(uint32_t *a, uint32_t v) {
-#if GBBS_STATE_ST == 0
-  st_stream(a, v);
-#elif GBBS_STATE_ST == 2
-  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(el_policy())
-               : "memory");
-#else
-  *a = v;
-#endif
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -738,8 +716,8 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     for (int j = 0; j < NB; j++) {
       if (win[j]) {
 #ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
-        st_state(p.dist + vv[j], (uint32_t)(r + 1));
-        if (p.parent) st_state(p.parent + vv[j], uu[j]);
+        st_stream(p.dist + vv[j], (uint32_t)(r + 1));
+        if (p.parent) st_stream(p.parent + vv[j], uu[j]);
 #endif
       }
     }
@@ -879,16 +857,8 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
 // tile's owners are i0, i0+1, ... while O < te, discovered from the owner loads
 // the tile needs anyway.  Returns the first owner of the next tile.
 
-#ifndef GBBS_TILE_NOINLINE
-#define GBBS_TILE_NOINLINE 0
-#endif
-#if GBBS_TILE_NOINLINE
-#define GBBS_TILE_INL __noinline__
-#else
-#define GBBS_TILE_INL __forceinline__
-#endif
 template <int ALGO, bool STATS, int EMIT>
-__device__ GBBS_TILE_INL long long push_tile(const Params &p, WarpSmem &wsm, WarpState &ws,
+__device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, WarpState &ws,
                                                int lb, long long i0, long long t, long long f,
                                                long long E, int nb, int r, uint32_t *bits,
                                                const uint32_t *prebits, int TR) {
@@ -1319,19 +1289,8 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4
 // LISTOUT (light pulls, below): acquisitions with out-edges are also staged and
 // flushed into frontier list nb with their edge prefixes, so the next round can
 // push from a list instead of sweeping the bitmap.
-// GBBS_PULL_NOINLINE / GBBS_TILE_NOINLINE: compile the dense pull's unit and the
-// list push's tile as real calls, so their hot loops get the register file to
-// themselves instead of spilling around the persistent kernel's live state
-#ifndef GBBS_PULL_NOINLINE
-#define GBBS_PULL_NOINLINE 0
-#endif
-#if GBBS_PULL_NOINLINE
-#define GBBS_PULL_INL __noinline__
-#else
-#define GBBS_PULL_INL __forceinline__
-#endif
 template <bool STATS, bool LISTOUT = false>
-__device__ GBBS_PULL_INL void pull_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
+__device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
                                            const uint32_t *vis, uint32_t *vis_next, int r,
                                            WarpState &ws, int nb = 0) {
   const int lane = threadIdx.x & 31;
@@ -1531,8 +1490,8 @@ __device__ GBBS_PULL_INL void pull_words(const Params &p, WarpSmem &wsm, long lo
         const uint32_t vq = v[q];
         if (STATS && (!LISTOUT || dgo[q] == 0)) ws.acquired += 1;  // LISTOUT: staged ones at flush
 #ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
-        st_state(p.dist + vq, (uint32_t)(r + 1));
-        if (p.parent) st_state(p.parent + vq, par[q]);
+        st_stream(p.dist + vq, (uint32_t)(r + 1));
+        if (p.parent) st_stream(p.parent + vq, par[q]);
 #endif
         atomicOr(&w.found[(vq >> 5) - (uint32_t)w0], 1u << (vq & 31));
         if (!LISTOUT && dgo[q] > 0) {
@@ -1807,75 +1766,6 @@ __device__ __forceinline__ void round_stats(const Params &p, Smem &s, const Warp
   }
 }
 
-// ---- solo rounds (high-diameter / small-frontier latency path) ---------------------
-// A BFS round whose frontier is tiny (|U| + sum deg(U) <= GBBS_SOLO_MAX) is run by
-// the team's first CTA alone, and so are the following rounds while they stay
-// that small: the CTA's 8 warps push the list in edge tiles exactly as a full
-// round does (same test-and-set, same staging and packed-counter flush into the
-// next list), but rounds are separated by __syncthreads instead of the grid
-// barrier.  Every other CTA waits at one grid barrier for the whole stretch and
-// then resumes at the first round that is not small (or ends).  Published in
-// p.solo: the next round to run and the acquisition total so far (reading A10b).
-#ifndef GBBS_SOLO_MAX
-#define GBBS_SOLO_MAX 0
-#endif
-template <bool STATS>
-__device__ __noinline__ void solo_rounds(const Params &p, Smem &s, WarpSmem &wsm, long long r,
-                                         long long f, long long E, uint32_t *bits,
-                                         long long acq_total) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned long long emask = (1ull << p.ebits) - 1;
-  for (;;) {
-    if (tid == 0) {
-      p.cnt[(r + 2) & 3] = 0;
-      p.acq[(r + 2) & 3] = 0;
-      p.wq[(r + 2) & 3] = 0;
-      p.wq[4 + ((r + 2) & 3)] = 0;
-      p.hcnt[(r + 1) & 1] = 0;
-      if (STATS && p.stats && r < p.stats_cap) {
-        p.stats[r].dense = 6;  // list push, solo (kind 6)
-        p.stats[r].frontier = f;
-        p.stats[r].frontier_edges = E;
-      }
-    }
-    const int cb = (int)(r & 1), nb = cb ^ 1;
-    WarpState ws;
-    list_round<ALGO_BFS, STATS, EMIT_LIST>(p, wsm, ws, cb, f, E, nb, (int)r, bits, bits, warp,
-                                           NWARPS, p.wq + (r & 3));
-    unsigned long long t_work = 0, t_flush = 0;
-    if (STATS) t_work = globaltimer_ns();
-    if (ws.scnt > 0) {
-      if (STATS && lane == 0) ws.acquired += ws.scnt;
-      warp_flush<ALGO_BFS>(p, wsm.stage, ws.scnt, nb, (int)r, bits, &t_work, nullptr,
-                           STATS ? &ws.ab : nullptr);
-    }
-    if (lane == 0 && ws.A) atomicAdd(p.acq + ((r + 1) & 3), ws.A);
-    if (STATS) t_flush = globaltimer_ns();
-    if (STATS) round_stats<STATS>(p, s, ws, r, t_work, t_flush);
-    __syncthreads();  // the round's list entries, counters and TS bits are complete
-    if (tid == 0) {
-      s.cnt = ld_relaxed64(p.cnt + ((r + 1) & 3));
-      s.acq = ld_relaxed64(p.acq + ((r + 1) & 3));
-    }
-    __syncthreads();
-    const unsigned long long c = s.cnt;
-    const long long a = (long long)s.acq;
-    r++;
-    f = (long long)(c >> p.ebits);
-    E = (long long)(c & emask);
-    const bool over = f + E > p.dense_threshold;
-    const bool big = p.mode == 2 || ((p.mode == 0 || p.mode == 3) && over);
-    if (f == 0 || big || f + E > GBBS_SOLO_MAX || r >= p.max_rounds) break;
-    acq_total += a;  // the main loop adds the acquisitions of the round it resumes at
-    if (STATS && tid == 0 && p.stats && r < p.stats_cap)
-      p.stats[r].t_start_ns = (long long)globaltimer_ns();
-  }
-  if (tid == 0) {
-    p.solo[0] = (unsigned long long)r;
-    p.solo[1] = (unsigned long long)acq_total;
-  }
-}
-
 // ---- teams: several traversals in one cooperative launch --------------------------
 // A multi-traversal launch (MG) interleaves the CTAs into G teams, one traversal
 // each with its own scratch; a team synchronises with a sense-counting barrier on
@@ -2069,16 +1959,6 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     // Bellman-Ford, AUTO / SPARSE: red rounds (the frontier bitmap is converted to a
     // list with its distances, then pushed with fire-and-forget priority-writes)
     if (GBBS_BF_RED && ALGO == ALGO_BF && (p.mode == 0 || p.mode == 1)) kind = 5;
-#if GBBS_SOLO_MAX > 0
-    if (ALGO == ALGO_BFS && kind == 0 && f + E <= GBBS_SOLO_MAX) {
-      if (GBBS_BID == 0) solo_rounds<STATS>(p, s, wsm, r, f, E, p.bm[vc], acq_total);
-      team_sync<MG>(grid, p.bar, GBBS_NBLK);
-      const long long rs = (long long)ld_relaxed64(p.solo);
-      acq_total = (long long)ld_relaxed64(p.solo + 1);
-      r = rs - 1;  // the loop's r++ resumes at the first round not run solo
-      continue;
-    }
-#endif
     if (GBBS_BID == 0 && tid == 0) {
       p.cnt[(r + 2) & 3] = 0;
       if (ALGO == ALGO_BFS) p.acq[(r + 2) & 3] = 0;

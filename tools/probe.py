@@ -78,7 +78,7 @@ def main():
                       f"GTEPS={mreach / km / 1e6:.1f}", flush=True)
                 if a.rounds or st.rounds <= 40:
                     for i, r in enumerate(recs):
-                        print(f"   r{i:<4d} {'SDFPBRs'[r['dense']] if r['dense'] < 3 or a.algos.find('wbfs') < 0 else 'BN'[r['dense'] - 3]} k={r['bucket']:<6d} U={r['frontier']:>10d} "
+                        print(f"   r{i:<4d} {'SDFPBR'[r['dense']] if r['dense'] < 3 or a.algos.find('wbfs') < 0 else 'BN'[r['dense'] - 3]} k={r['bucket']:<6d} U={r['frontier']:>10d} "
                               f"E={r['frontier_edges']:>11d} acq={r['acquired']:>9d} "
                               f"ex={r['edges_examined']:>11d} sw={r['vertices_swept']:>9d} "
                               f"{(r['us'] or 0):9.1f}us  work<{r['work_us']:.1f} flush<{r['flush_us']:.1f} "
