@@ -226,7 +226,7 @@ struct WarpState {
   unsigned long long bk = 0;     // wBFS: bucket being processed
   unsigned long long pmask = 0;  // wBFS: bucket lists this lane appended to
   unsigned long long K = 0, D = 0;
-  unsigned long long A = 0;      // BFS: vertices acquired this round (warp-uniform)
+  unsigned long long A = 0;      // BFS dense rounds: vertices acquired (warp-uniform)
   unsigned long long edges = 0, swept = 0, acquired = 0;
   unsigned long long ab = 0, hh = 0;  // STATS: algorithmic bytes, pull head hits
 #ifdef GBBS_DIAG_LIST  // diagnostic builds: list-round phase timestamps
@@ -841,7 +841,6 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
       if (win[j]) st[ws.scnt + __popc(b & lanemask_lt())] = vv[j];
       ws.scnt += __popc(b);
-      if (ALGO == ALGO_BFS) ws.A += __popc(b);
     }
     if (ws.scnt > WCAP - 32 * NB) {
       if (STATS && lane == 0) ws.acquired += ws.scnt;
@@ -1916,6 +1915,7 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
 
   const unsigned long long emask = (1ull << p.ebits) - 1;
   int vc = 0;              // BFS: index of the current visited bitmap
+  bool prev_dense = false;  // BFS: was the previous round a dense pull (reading A10b count)
   bool list_valid = true;  // is this round's frontier materialised as a list?
   long long r = 0;
   for (;; r++) {
@@ -1927,7 +1927,10 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     const unsigned long long c = s.cnt;
     const long long f = (long long)(c >> p.ebits);
     const long long E = (long long)(c & emask);
-    if (ALGO == ALGO_BFS) acq_total += (long long)s.acq;
+    // dense rounds count their acquisitions (one atomic per warp); after a push round
+    // the frontier size f — its acquisitions with out-edges — stands in for them
+    // (per-warp counting on one word in every push round cost c3 ~1.3 us per round)
+    if (ALGO == ALGO_BFS && r > 0) acq_total += prev_dense ? (long long)s.acq : f;
     if (STATS && GBBS_BID == 0 && tid == 0 && p.stats && r < p.stats_cap)
       p.stats[r].t_start_ns = (long long)globaltimer_ns();
     if (f == 0) break;
@@ -1974,7 +1977,9 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
     const int cb = (int)(r & 1), nb = cb ^ 1;
     WarpState ws;
     bool emit_count = false;
-    if (kind == 1 && ALGO == ALGO_BFS && p.ncand - acq_total <= (long long)GBBS_LIGHT * nw) {
+    // light pulls sweep static 128-word blocks: only when every warp gets one
+    if (kind == 1 && ALGO == ALGO_BFS && p.ncand - acq_total <= (long long)GBBS_LIGHT * nw &&
+        p.nwords >= 128ll * nw) {
       light_pull<STATS>(p, wsm, ws, p.bm[vc], p.bm[vc ^ 1], (int)r, nb, gw, nw);
       vc ^= 1;
       list_valid = true;  // the acquisitions were also emitted as list nb
@@ -1985,7 +1990,10 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
         // dynamic assignment: a warp takes the next unit of psw words from a
         // per-round counter as soon as it is done, so no warp waits at the
         // barrier for another that drew two units
-        const int psw = GBBS_PULL_SW ? GBBS_PULL_SW : sw;
+        // 32-word units (c2/c4/c5: 2-5 % faster than 16 or 8), halved while there are
+        // fewer units than a quarter of the warps (a 2^14-vertex graph has 16)
+        int psw = GBBS_PULL_SW ? GBBS_PULL_SW : sw;
+        while (psw > 1 && (p.nwords + psw - 1) / psw < nw / 4) psw >>= 1;
         for (;;) {
           unsigned long long u = 0;
           if (lane == 0) u = atomicAdd(p.wq + (r & 3), 1ull);
@@ -2067,7 +2075,8 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
       const unsigned long long K = warp_sum64((long long)ws.K), D = warp_sum64((long long)ws.D);
       if (lane == 0 && K) atomicAdd(p.cnt + ((r + 1) & 3), (K << p.ebits) | D);
     }
-    if (ALGO == ALGO_BFS && lane == 0 && ws.A) atomicAdd(p.acq + ((r + 1) & 3), ws.A);
+    if (ALGO == ALGO_BFS && kind == 1 && lane == 0 && ws.A) atomicAdd(p.acq + ((r + 1) & 3), ws.A);
+    prev_dense = ALGO == ALGO_BFS && kind == 1;
     if (STATS) t_flush = globaltimer_ns();
 #ifdef GBBS_DIAG_LIST
     if (STATS) { t_work = ws.t1; t_flush = ws.t2; ws.t1 = ws.t2 = 0; }
