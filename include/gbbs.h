@@ -57,10 +57,11 @@ extern "C" {
 /* Use device arrays in place (zero copy).  The caller keeps offsets, targets
  * and weights alive and unmodified until gbbs_graph_destroy.  Host pointers
  * with this flag are an error (GBBS_EINVAL).  Dense rounds of symmetric graphs
- * read targets in aligned 16-byte groups, so a borrowed targets array must be
- * readable up to the next 16-byte boundary past targets[m - 1] (true of any
- * cudaMalloc or PyTorch allocation, whose sizes are rounded up to 512 bytes);
- * a targets pointer that is not 16-byte aligned is copied instead. */
+ * and list pushes of a hub's edges read targets (and weights) in aligned
+ * 16-byte groups, so borrowed targets and weights arrays must be readable up
+ * to the next 16-byte boundary past element m - 1 (true of any cudaMalloc or
+ * PyTorch allocation, whose sizes are rounded up to 512 bytes); a targets or
+ * weights pointer that is not 16-byte aligned is copied instead. */
 #define GBBS_BORROW 0x2u
 /* Skip the O(n+m) device validation of the CSR (offsets/targets). */
 #define GBBS_NO_VALIDATE 0x4u

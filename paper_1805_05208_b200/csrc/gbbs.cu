@@ -353,10 +353,15 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
       g->own_tgt = true;
       if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4, 16))) return rc;
     }
+    if (weights && ((uintptr_t)weights & 15) != 0) {  // same for the weights (list-push groups)
+      g->wgt = nullptr;
+      g->own_wgt = true;
+      if ((rc = copy_in((void **)&g->wgt, weights, (size_t)m * 4, 16))) return rc;
+    }
   } else {
     if ((rc = copy_in((void **)&g->off, offsets, (size_t)(n + 1) * 8))) return rc;
     if ((rc = copy_in((void **)&g->tgt, targets, (size_t)m * 4, 16))) return rc;
-    if (weights && (rc = copy_in((void **)&g->wgt, weights, (size_t)m * 4))) return rc;
+    if (weights && (rc = copy_in((void **)&g->wgt, weights, (size_t)m * 4, 16))) return rc;
   }
   // endpoints
   long long o0 = -1, on = -1;
