@@ -302,6 +302,9 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *a) {
 #ifndef GBBS_PREFETCH
 #define GBBS_PREFETCH 1
 #endif
+#ifndef GBBS_PREFETCH_W  // the weighted algorithms' list tiles too
+#define GBBS_PREFETCH_W 1
+#endif
 // Bellman-Ford red rounds (EMIT_RED); 0 = the test-and-set list push of round 1
 #ifndef GBBS_BF_RED
 #define GBBS_BF_RED 1
@@ -941,36 +944,41 @@ __device__ __forceinline__ long long push_tile(const Params &p, WarpSmem &wsm, W
     if (!valid) Ok = BIG;
     uint32_t Xk = Uk;
     if (W && EMIT != EMIT_RED) Xk = valid ? ld_relaxed(p.dist + Uk) : 0;
-    if (GBBS_PREFETCH && te - ts > 32 * NCH) {
-      for (long long cst = ts + 32 * NCH; cst < te; cst += 32) {
-        const int c0 = __popc(__ballot_sync(FULL, Ok <= cst)) - 1;
-        const long long rel = Ok - cst;
+    // owner starts relative to the tile, clamped to [-1, TR + 32] (32-bit compares;
+    // every owner starting at or before the tile behaves alike)
+    const int tn = (int)(te - ts);
+    const int ro = (int)max(-1ll, min(Ok - ts, (long long)TR + 32));
+    const long long Bt = Bk + ts;  // owner's target index of the tile's first slot
+    if (GBBS_PREFETCH && (!W || GBBS_PREFETCH_W) && tn > 32 * NCH) {
+      for (int cr = 32 * NCH; cr < tn; cr += 32) {
+        const int c0 = __popc(__ballot_sync(FULL, ro <= cr)) - 1;
+        const int rel = ro - cr;
         const unsigned hm = __reduce_or_sync(FULL, (rel > 0 && rel < 32) ? (1u << rel) : 0u);
-        const long long bb = __shfl_sync(FULL, Bk, c0 + __popc(hm & lanemask_le()));
-        if (cst + lane < te) {
-          prefetch_l2(p.tgt + bb + cst + lane);
-          if (W && p.wgt) prefetch_l2(p.wgt + bb + cst + lane);
+        const long long bb = __shfl_sync(FULL, Bt, c0 + __popc(hm & lanemask_le()));
+        if (cr + lane < tn) {
+          prefetch_l2(p.tgt + bb + cr + lane);
+          if (W && p.wgt) prefetch_l2(p.wgt + bb + cr + lane);
         }
       }
     }
-    for (long long cs = ts; cs < te; cs += 32 * NCH) {
+    for (int cs = 0; cs < tn; cs += 32 * NCH) {
       uint32_t vv[NCH], ww[NCH], uu[NCH];
       bool act[NCH];
 #pragma unroll
       for (int j = 0; j < NCH; j++) {
-        const long long cst = cs + 32 * j;
-        const long long e = cst + lane;
-        act[j] = e < te;
+        const int cr = cs + 32 * j;
+        const int e = cr + lane;
+        act[j] = e < tn;
         vv[j] = 0;
         ww[j] = 0;
         uu[j] = 0;
-        if (cst < te) {  // warp-uniform
-          const int c0 = __popc(__ballot_sync(FULL, Ok <= cst)) - 1;
-          const long long rel = Ok - cst;
+        if (cr < tn) {  // warp-uniform
+          const int c0 = __popc(__ballot_sync(FULL, ro <= cr)) - 1;
+          const int rel = ro - cr;
           const unsigned hb = (rel > 0 && rel < 32) ? (1u << rel) : 0u;
           const unsigned hm = __reduce_or_sync(FULL, hb);
           const int own = c0 + __popc(hm & lanemask_le());
-          const long long bb = __shfl_sync(FULL, Bk, own);
+          const long long bb = __shfl_sync(FULL, Bt, own);
           uu[j] = __shfl_sync(FULL, Xk, own);
           if (act[j]) {
             GBBS_CHECK(bb + e >= 0 && bb + e < p.m);
