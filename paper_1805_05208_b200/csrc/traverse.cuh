@@ -302,8 +302,8 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *a) {
 #ifndef GBBS_PREFETCH
 #define GBBS_PREFETCH 1
 #endif
-#ifndef GBBS_PREFETCH_W  // the weighted algorithms' list tiles too
-#define GBBS_PREFETCH_W 1
+#ifndef GBBS_PREFETCH_W  // the weighted algorithms' register-path tiles too: off, c4 BF -2.3 %
+#define GBBS_PREFETCH_W 0
 #endif
 // Bellman-Ford red rounds (EMIT_RED); 0 = the test-and-set list push of round 1
 #ifndef GBBS_BF_RED

@@ -1,3 +1,3 @@
 set -x
-AB_VARIANTS="pfw" AB_BF=1 bash tools/r02_ab.sh
+AB_VARIANTS="pch3" bash tools/r02_ab.sh
 echo DONE
