@@ -24,6 +24,7 @@ PRODUCT = dict(
     deps=[os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "traverse.cuh"),
           os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "bc.cuh"),
           os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "sbf.cuh"),
+          os.path.join(ROOT, "paper_1805_05208_b200", "csrc", "csc.cuh"),
           os.path.join(ROOT, "include", "gbbs.h")],
 )
 GEN = dict(
