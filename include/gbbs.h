@@ -347,11 +347,19 @@ typedef struct {
                              calls ignore it.                              */
   uint32_t rules;         /* direction-rule flags: GBBS_RULE_PAPER_ONLY
                              (BFS AUTO takes the paper's m/T test alone,
-                             without reading A10b's stay-dense test).
-                             Other bits must be zero.                      */
+                             without reading A10b's stay-dense test);
+                             GBBS_RULE_LEVEL_BYTES_ON / _OFF (BFS keeps
+                             the levels of a traversal as one byte per
+                             vertex and expands them into dist in a last
+                             coalesced pass, instead of one scattered
+                             4-byte store per acquisition — same dist,
+                             P:1475-1478; default: on above 2^24
+                             vertices).  Other bits must be zero.         */
 } gbbs_opts;
 
 #define GBBS_RULE_PAPER_ONLY 0x1
+#define GBBS_RULE_LEVEL_BYTES_ON 0x2
+#define GBBS_RULE_LEVEL_BYTES_OFF 0x4
 
 /* One record per round, filled only when gbbs_stats.rounds_out != NULL. */
 typedef struct {

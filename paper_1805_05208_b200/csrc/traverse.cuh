@@ -139,6 +139,7 @@ struct Params {
   long long ncand;           // vertices with at least one in-edge
   uint32_t *dist;            // [n]
   uint16_t *shadow;          // [n] BF/WP: 16-bit conservative copy of dist
+  uint8_t *lvl;              // [n] BFS: levels as bytes (bfs_set_dist), or nullptr: dist written directly
   uint32_t *parent;          // [n] or nullptr
   uint32_t *bm[2];           // BFS: visited (double-buffered); BF: frontier TS bits
   uint32_t *fv[3];           // lists 0/1 (rounds) and 2 (heavy): vertex
@@ -288,6 +289,14 @@ __device__ __forceinline__ long long ld_stream64(const long long *a) {
   return v;
 }
 
+__device__ __forceinline__ uint2 ld_stream_v2(const uint32_t *a) {
+  uint2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+      : "=r"(v.x), "=r"(v.y)
+      : "l"(a), "l"(ef_policy()));
+  return v;
+}
+
 __device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *a) {
   uint4 v;
   asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
@@ -348,6 +357,33 @@ __device__ __forceinline__ void diag_add(const unsigned long long *dbgc, int k,
   }
 }
 #endif
+// ---- BFS levels as bytes -------------------------------------------------------------
+// A BFS acquisition writes dist[v] = r + 1 exactly once (the test-and-set winner).  As
+// a scattered 4-byte store every such write is a partial-sector write that DRAM serves
+// as a 32-byte read-modify-write (measured on c5: 23 % of the traversal time goes to
+// the state stores).  The traversal therefore records levels below LVL_DIRECT in a
+// byte array (Params.lvl, n bytes: the 16-bit shadow's buffer, which BFS does not
+// use; 32 vertices per sector, mostly L2-resident) and one coalesced pass at the end expands
+// it into dist (4-byte stores, whole lines, no fill at the start).  Levels from
+// LVL_DIRECT on (graphs with more rounds than a byte holds) are stored in dist
+// directly and flagged LVL_DIRECT so the final pass leaves them alone.  The host
+// enables it for graphs above 2^24 vertices (gbbs.cu fill_params: on c2 / c3 the extra
+// pass costs more than the stores save) or on request (GBBS_RULE_LEVEL_BYTES_ON).
+constexpr uint32_t LVL_DIRECT = 254, LVL_INF = 255;
+
+__device__ __forceinline__ void bfs_set_dist(const Params &p, uint32_t v, uint32_t d) {
+  if (p.lvl) {
+    if (d < LVL_DIRECT) {
+      p.lvl[v] = (uint8_t)d;
+    } else {
+      p.lvl[v] = (uint8_t)LVL_DIRECT;
+      st_stream(p.dist + v, d);
+    }
+  } else {
+    st_stream(p.dist + v, d);
+  }
+}
+
 __device__ __forceinline__ bool vbit(const uint32_t *vis, uint32_t u) {
   return (vis[u >> 5] >> (u & 31)) & 1u;
 }
@@ -724,7 +760,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
     for (int j = 0; j < NB; j++) {
       if (win[j]) {
 #ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
-        st_stream(p.dist + vv[j], (uint32_t)(r + 1));
+        bfs_set_dist(p, vv[j], (uint32_t)(r + 1));
         if (p.parent) st_stream(p.parent + vv[j], uu[j]);
 #endif
       }
@@ -1332,7 +1368,7 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4
 // flushed into frontier list nb with their edge prefixes, so the next round can
 // push from a list instead of sweeping the bitmap.
 template <bool STATS, bool LISTOUT = false>
-__device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
+__device__ __forceinline__ void pull_words_lockstep(const Params &p, WarpSmem &wsm, long long w0, int sw,
                                            const uint32_t *vis, uint32_t *vis_next, int r,
                                            WarpState &ws, int nb = 0) {
   const int lane = threadIdx.x & 31;
@@ -1532,7 +1568,7 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
         const uint32_t vq = v[q];
         if (STATS && (!LISTOUT || dgo[q] == 0)) ws.acquired += 1;  // LISTOUT: staged ones at flush
 #ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
-        st_stream(p.dist + vq, (uint32_t)(r + 1));
+        bfs_set_dist(p, vq, (uint32_t)(r + 1));
         if (p.parent) st_stream(p.parent + vq, par[q]);
 #endif
         atomicOr(&w.found[(vq >> 5) - (uint32_t)w0], 1u << (vq & 31));
@@ -1562,6 +1598,320 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
   __syncwarp();
   if (mine) vis_next[word] = vw | w.found[lane];
   __syncwarp();
+}
+
+// ---- phased pull ---------------------------------------------------------------------
+// The same scan, run as three passes over the unit's candidates with the survivors
+// of each pass compacted in place in w.cand, so that every pass runs with full
+// warps instead of the whole batch waiting for its longest in-list:
+//   pass 1  hot record, probe in0                      (every candidate)
+//   pass 2  probes in1, in2 + cold record, in3, in4    (candidates in0 did not decide)
+//   pass 3  the tail from in-edge 5 on, 16-byte groups (candidates in0..in4 did not decide)
+// Per candidate the in-edges are examined in the same CSC order with the same
+// early exit; a pass re-reads its record from L2 instead of carrying
+// it in shared memory (not counted as algorithmic bytes: the scan needs it once).
+#ifndef GBBS_PULL_PHASED
+#define GBBS_PULL_PHASED 1
+#endif
+#ifndef GBBS_PULL_P1
+#define GBBS_PULL_P1 4
+#endif
+constexpr int P1CH = GBBS_PULL_P1;
+
+// One 32-candidate chunk's outcome: state writes, found bits, next-frontier counts
+// (or, LISTOUT, staging for the next round's list).  Warp-convergent.
+template <bool STATS, bool LISTOUT>
+__device__ __forceinline__ void pull_commit(const Params &p, WarpSmem &wsm, long long w0, int r,
+                                            WarpState &ws, int nb, uint32_t vq, uint32_t par,
+                                            uint32_t dgo) {
+  SweepSmem &w = wsm.u.s;
+  const bool acq = par != INF;
+  ws.A += __popc(__ballot_sync(FULL, acq));
+  if (acq) {
+    if (STATS && (!LISTOUT || dgo == 0)) ws.acquired += 1;  // LISTOUT: staged ones at flush
+#ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
+    bfs_set_dist(p, vq, (uint32_t)(r + 1));
+    if (p.parent) st_stream(p.parent + vq, par);
+#endif
+    atomicOr(&w.found[(vq >> 5) - (uint32_t)w0], 1u << (vq & 31));
+    if (!LISTOUT && dgo > 0) {
+      ws.K += 1;
+      ws.D += dgo;
+    }
+  }
+  if (LISTOUT) {
+    const bool stg = acq && dgo > 0;
+    const unsigned b = __ballot_sync(FULL, stg);
+    GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
+    if (stg) wsm.stage[ws.scnt + __popc(b & lanemask_lt())] = vq;
+    ws.scnt += __popc(b);
+    if (ws.scnt > WCAP - 32) {
+      if (STATS && (threadIdx.x & 31) == 0) ws.acquired += ws.scnt;
+      warp_flush<ALGO_BFS>(p, wsm.stage, ws.scnt, nb, r, nullptr, nullptr, nullptr,
+                           STATS ? &ws.ab : nullptr);
+      ws.scnt = 0;
+    }
+  }
+}
+
+template <bool STATS, bool LISTOUT = false>
+__device__ __forceinline__ void pull_words_phased(const Params &p, WarpSmem &wsm, long long w0,
+                                                  int sw, const uint32_t *vis, uint32_t *vis_next,
+                                                  int r, WarpState &ws, int nb = 0) {
+  const int lane = threadIdx.x & 31;
+  SweepSmem &w = wsm.u.s;
+  const long long word = w0 + lane;
+  const bool mine = lane < sw && word < p.nwords;
+  const uint32_t vw = mine ? vis[word] : FULL;
+  const uint32_t skip = mine ? (vw | __ldg(p.nin + word)) : FULL;
+  if (STATS && mine) ws.ab += 12;  // visited + no-in words read, next visited word written
+  if (!__any_sync(FULL, skip != FULL)) {  // nothing to pull: carry the words over
+    if (mine) vis_next[word] = vw;
+    return;
+  }
+  const int cnt = warp_gather(w, w0, ~skip);
+  w.found[lane] = 0;
+  __syncwarp();
+  if (STATS && lane == 0) ws.swept += cnt;
+
+  // pass 1: hot record + in0, P1CH * 32 candidates in flight
+  int ns = 0;
+  for (int c0 = 0; c0 < cnt; c0 += 32 * P1CH) {
+    uint32_t v[P1CH];
+    uint4 h[P1CH];
+    if (GBBS_PULL_PF) {  // the next batch's hot records, into L2 while this one runs
+#pragma unroll
+      for (int q = 0; q < P1CH; q++) {
+        const int i = c0 + 32 * P1CH + 32 * q + lane;
+        if (i < cnt) prefetch_l2(p.phot + w.cand[i]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < P1CH; q++) {
+      const int i = c0 + 32 * q + lane;
+      v[q] = i < cnt ? w.cand[i] : 0;
+      h[q] = make_uint4(INF, INF, INF, 0);
+      if (i < cnt) h[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.phot + v[q]));
+    }
+    __syncwarp();  // the batch's candidates are in registers: survivors may overwrite them
+#pragma unroll
+    for (int q = 0; q < P1CH; q++) {
+      if (c0 + 32 * q >= cnt) break;
+      if (STATS && c0 + 32 * q + lane < cnt) {
+        ws.ab += 16;  // hot record
+        ws.edges += 1;
+      }
+      const bool hit = h[q].x != INF && vbit(vis, h[q].x);
+      if (STATS && hit) ws.hh += 1;
+      pull_commit<STATS, LISTOUT>(p, wsm, w0, r, ws, nb, v[q], hit ? h[q].x : INF, h[q].w);
+      const bool surv = !hit && h[q].y != INF;
+      const unsigned b = __ballot_sync(FULL, surv);
+      if (surv) w.cand[ns + __popc(b & lanemask_lt())] = v[q];
+      ns += __popc(b);
+    }
+  }
+  __syncwarp();
+
+  // pass 2: in1, in2 probed together with the cold record's load (in3, in4, tail)
+  int nt = 0;
+  for (int c0 = 0; c0 < ns; c0 += 32 * PCH) {
+    uint32_t v[PCH], par[PCH];
+    uint4 h[PCH], cr[PCH];
+    bool need[PCH];
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      const int i = c0 + 32 * q + lane;
+      v[q] = i < ns ? w.cand[i] : 0;
+      h[q] = make_uint4(INF, INF, INF, 0);
+      if (i < ns) h[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.phot + v[q]));
+    }
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      cr[q] = make_uint4(INF, INF, 0, 0);
+      if (h[q].z != INF) cr[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pcold + v[q]));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      par[q] = INF;
+      if (h[q].y == INF) continue;  // idle lane
+      const bool b1 = vbit(vis, h[q].y);
+      const bool b2 = h[q].z != INF && vbit(vis, h[q].z);
+      if (STATS) ws.edges += (b1 || h[q].z == INF) ? 1 : 2;
+      par[q] = b1 ? h[q].y : (b2 ? h[q].z : INF);
+    }
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      need[q] = false;
+      if (h[q].y == INF || par[q] != INF || h[q].z == INF) continue;
+      if (STATS) ws.ab += 16;  // cold record
+      const bool b3 = cr[q].x != INF && vbit(vis, cr[q].x);
+      const bool b4 = cr[q].y != INF && vbit(vis, cr[q].y);
+      if (STATS) ws.edges += (cr[q].x == INF) ? 0 : ((b3 || cr[q].y == INF) ? 1 : 2);
+      par[q] = b3 ? cr[q].x : (b4 ? cr[q].y : INF);
+      const unsigned long long tail = ((unsigned long long)cr[q].w << 32) | cr[q].z;
+      if (par[q] == INF && tail != 0) {
+        need[q] = true;
+        prefetch_l2(p.in_tgt + ((long long)(tail >> 24) & ~3ll));  // pass 3 starts here
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      if (c0 + 32 * q >= ns) break;
+      pull_commit<STATS, LISTOUT>(p, wsm, w0, r, ws, nb, v[q], par[q], h[q].w);
+      const unsigned b = __ballot_sync(FULL, need[q]);
+      if (need[q]) w.cand[nt + __popc(b & lanemask_lt())] = v[q];
+      nt += __popc(b);
+    }
+  }
+  __syncwarp();
+
+  // pass 3: the tail, 16-byte groups of in-edges
+  for (int c0 = 0; c0 < nt; c0 += 32 * PCH) {
+    uint32_t v[PCH], par[PCH], dgo[PCH];
+    long long js[PCH];
+    int rem[PCH];
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      const int i = c0 + 32 * q + lane;
+      v[q] = i < nt ? w.cand[i] : 0;
+      par[q] = INF;
+      js[q] = 0;
+      rem[q] = 0;
+      dgo[q] = 0;
+      if (i < nt) {
+        const uint2 t = ld_stream_v2(reinterpret_cast<const uint32_t *>(p.pcold + v[q]) + 2);
+        dgo[q] = ld_stream(reinterpret_cast<const uint32_t *>(p.phot + v[q]) + 3);
+        const unsigned long long tail = ((unsigned long long)t.y << 32) | t.x;
+        js[q] = (long long)(tail >> 24);
+        rem[q] = (int)(tail & 0xFFFFFFull);
+        if (rem[q] == 0xFFFFFF) rem[q] = (int)(ld_stream64(p.in_off + v[q] + 1) - js[q]);
+      }
+    }
+    __syncwarp();
+    bool anyrem = false;
+#pragma unroll
+    for (int q = 0; q < PCH; q++) anyrem |= rem[q] > 0;
+    if (__any_sync(FULL, anyrem)) {
+      for (int step = 0; step < PULL_STEPS; step++) {
+        uint4 g[PCH];
+#pragma unroll
+        for (int q = 0; q < PCH; q++)
+          if (rem[q] > 0) {
+            GBBS_CHECK(js[q] >= 0 && js[q] < p.m);
+            g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+          }
+        bool live = false;
+#pragma unroll
+        for (int q = 0; q < PCH; q++) {
+          if (rem[q] <= 0) continue;
+          const int lo = (int)(js[q] & 3);
+          const int hi = min(4, lo + rem[q]);
+          const uint32_t e[4] = {g[q].x, g[q].y, g[q].z, g[q].w};
+          bool b[4];
+#pragma unroll
+          for (int k = 0; k < 4; k++) b[k] = (k >= lo && k < hi) ? vbit(vis, e[k]) : false;
+          uint32_t hit = INF;
+#pragma unroll
+          for (int k = 3; k >= 0; k--)
+            if (b[k]) hit = e[k];
+          if (STATS) {
+            ws.edges += hi - lo;
+            ws.ab += 16;
+          }
+          js[q] += hi - lo;
+          rem[q] -= hi - lo;
+          if (hit != INF) {
+            par[q] = hit;
+            rem[q] = 0;
+          }
+          live |= rem[q] > 0;
+        }
+        if (!__any_sync(FULL, live)) break;
+      }
+    }
+    // short remainders: per lane; long remainders: the whole warp, one vertex at a time
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      for (;;) {
+        const bool go = rem[q] > 0 && rem[q] <= LONG_IN;
+        if (!__any_sync(FULL, go)) break;
+        if (go) {
+          GBBS_CHECK(js[q] >= 0 && js[q] < p.m);
+          const uint4 g = ldg_v4(p.in_tgt + (js[q] & ~3ll));
+          const int lo = (int)(js[q] & 3);
+          const int hi = min(4, lo + rem[q]);
+          const uint32_t e[4] = {g.x, g.y, g.z, g.w};
+          uint32_t hit = INF;
+#pragma unroll
+          for (int k = 3; k >= 0; k--)
+            if (k >= lo && k < hi && vbit(vis, e[k])) hit = e[k];
+          if (STATS) {
+            ws.edges += hi - lo;
+            ws.ab += 16;
+          }
+          js[q] += hi - lo;
+          rem[q] -= hi - lo;
+          if (hit != INF) {
+            par[q] = hit;
+            rem[q] = 0;
+          }
+        }
+      }
+      unsigned longs = __ballot_sync(FULL, rem[q] > LONG_IN);
+      while (longs) {
+        const int l = __ffs(longs) - 1;
+        longs &= longs - 1;
+        long long a = __shfl_sync(FULL, js[q], l);
+        const long long e_end = a + __shfl_sync(FULL, rem[q], l);
+        uint32_t found = INF;
+        // groups of 128 in-edges per step: a 16-byte load per lane, then the probes
+        while (a < e_end) {
+          const long long a0 = a & ~3ll;
+          const long long gk = a0 + 4 * lane;
+          uint32_t hit = INF;
+          if (gk < e_end) {
+            GBBS_CHECK(gk >= 0 && gk < p.m);
+            const uint4 g = ldg_v4(p.in_tgt + gk);
+            const uint32_t e[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int k = 3; k >= 0; k--)
+              if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit = e[k];
+            if (STATS) ws.ab += 16;
+          }
+          if (STATS && lane == 0) ws.edges += min(a0 + 128, e_end) - a;
+          const unsigned hb = __ballot_sync(FULL, hit != INF);  // first hit in CSC order
+          if (hb) {
+            found = __shfl_sync(FULL, hit, __ffs(hb) - 1);
+            break;
+          }
+          a = a0 + 128;
+        }
+        if (lane == l) {
+          rem[q] = 0;
+          par[q] = found;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PCH; q++) {
+      if (c0 + 32 * q >= nt) break;
+      pull_commit<STATS, LISTOUT>(p, wsm, w0, r, ws, nb, v[q], par[q], dgo[q]);
+    }
+  }
+  __syncwarp();
+  if (mine) vis_next[word] = vw | w.found[lane];
+  __syncwarp();
+}
+
+template <bool STATS, bool LISTOUT = false>
+__device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
+                                           const uint32_t *vis, uint32_t *vis_next, int r,
+                                           WarpState &ws, int nb = 0) {
+  if (GBBS_PULL_PHASED)
+    pull_words_phased<STATS, LISTOUT>(p, wsm, w0, sw, vis, vis_next, r, ws, nb);
+  else
+    pull_words_lockstep<STATS, LISTOUT>(p, wsm, w0, sw, vis, vis_next, r, ws, nb);
 }
 
 // ---- light pull: a dense round with few candidates left -----------------------------
@@ -1911,9 +2261,26 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
   WarpSmem &wsm = s.w[warp];
 
   // a1: per-run init
-#ifdef GBBS_DIAG_NOINIT  // diagnostic builds (results invalid): cost of the fill
-  if (ALGO != ALGO_BFS)
+  if (ALGO == ALGO_BFS && p.lvl) {
+    // levels: LVL_INF everywhere, 0 at src (16 bytes per thread and step; the buffer
+    // holds 2n bytes; the tail group is written byte by byte); parent as before
+    uint8_t *lvl = p.lvl;
+    for (long long i = gtid * 16; i < p.n; i += gstride * 16) {
+      if (i + 16 <= p.n) {
+        uint32_t x[4] = {FULL, FULL, FULL, FULL};
+        if ((long long)src >= i && (long long)src < i + 16)
+          x[(src - i) >> 2] &= ~(0xFFu << (8 * ((src - i) & 3)));
+        *reinterpret_cast<uint4 *>(lvl + i) = make_uint4(x[0], x[1], x[2], x[3]);
+      } else {
+        for (long long k = i; k < p.n; k++) lvl[k] = (k == (long long)src) ? 0 : (uint8_t)LVL_INF;
+      }
+    }
+#ifndef GBBS_DIAG_NOINIT  // diagnostic builds (results invalid): cost of the fill
+    if (p.parent)
+      for (long long i = gtid; i < p.n; i += gstride)
+        st_stream(p.parent + i, (i == src) ? src : INF);
 #endif
+  } else
   for (long long i = gtid; i < p.n; i += gstride) {
     // BFS/BF: 0 at src, INF elsewhere; widest path: INF (empty path) at src, 0 elsewhere
     if (ALGO == ALGO_WP) {
@@ -2126,6 +2493,51 @@ __device__ __forceinline__ void traverse_body(const Params &p, Smem &s, int G) {
 #endif
     if (STATS) round_stats<STATS>(p, s, ws, r, t_work, t_flush);
     team_sync<MG>(grid, p.bar, GBBS_NBLK);
+  }
+  if (ALGO == ALGO_BFS && p.lvl) {
+    // a12: expand the levels into dist (every write of the last round is visible: the
+    // loop is left after a team barrier).  A warp takes 1024 levels per step: each lane
+    // loads two 16-byte groups (coalesced), the groups are transposed through the
+    // warp's shared memory, and dist is written as whole 512-byte rows (16 bytes per
+    // lane) — partial-sector stores cost the L2 several requests per sector.
+    const uint8_t *lvl = p.lvl;
+    const bool al = (reinterpret_cast<unsigned long long>(p.dist) & 15ull) == 0;
+    uint32_t *tw = wsm.u.s.cand;  // 256 words of scratch
+    for (long long b0 = gw * 1024; b0 < p.n; b0 += nw * 1024) {
+      if (b0 + 1024 <= p.n) {
+        const uint4 q0 = __ldcg(reinterpret_cast<const uint4 *>(lvl + b0) + lane);
+        const uint4 q1 = __ldcg(reinterpret_cast<const uint4 *>(lvl + b0 + 512) + lane);
+        reinterpret_cast<uint4 *>(tw)[lane] = q0;
+        reinterpret_cast<uint4 *>(tw)[32 + lane] = q1;
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const uint32_t wd = tw[k * 32 + lane];  // levels of b0 + 128 k + 4 lane .. + 3
+          const long long v0 = b0 + 128 * k + 4 * lane;
+          const uint32_t x = wd ^ 0xFEFEFEFEu;  // a zero byte <=> LVL_DIRECT: dist already final
+          const bool direct = ((x - 0x01010101u) & ~x & 0x80808080u) != 0;
+          uint32_t d[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const uint32_t l = (wd >> (8 * e)) & 0xFFu;
+            d[e] = l == LVL_INF ? INF : l;
+          }
+          if (al && !direct) {
+            st_stream_v4(p.dist + v0, d[0], d[1], d[2], d[3]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+              if (d[e] != LVL_DIRECT) st_stream(p.dist + v0 + e, d[e]);
+          }
+        }
+        __syncwarp();
+      } else {  // the last, partial block
+        for (long long j = b0 + lane; j < p.n; j += 32) {
+          const uint32_t l = __ldcg(lvl + j);
+          if (l != LVL_DIRECT) st_stream(p.dist + j, l == LVL_INF ? INF : l);
+        }
+      }
+    }
   }
   if (GBBS_BID == 0 && tid == 0) *p.rounds_out = r;
 }

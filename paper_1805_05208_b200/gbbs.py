@@ -24,6 +24,8 @@ GBBS_DIST_NEGINF = np.iinfo(np.int64).min
 GBBS_SYMMETRIC, GBBS_BORROW, GBBS_NO_VALIDATE = 0x1, 0x2, 0x4
 GBBS_MODE_AUTO, GBBS_MODE_SPARSE, GBBS_MODE_DENSE, GBBS_MODE_PULL = 0, 1, 2, 3
 GBBS_RULE_PAPER_ONLY = 0x1
+GBBS_RULE_LEVEL_BYTES_ON = 0x2
+GBBS_RULE_LEVEL_BYTES_OFF = 0x4
 
 EXPORTS = ("gbbs_graph_create", "gbbs_graph_destroy", "gbbs_graph_info", "gbbs_bfs",
            "gbbs_bellman_ford", "gbbs_widest_path", "gbbs_bfs_ex", "gbbs_bellman_ford_ex",
