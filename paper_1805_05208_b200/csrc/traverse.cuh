@@ -1367,252 +1367,17 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4
 // LISTOUT (light pulls, below): acquisitions with out-edges are also staged and
 // flushed into frontier list nb with their edge prefixes, so the next round can
 // push from a list instead of sweeping the bitmap.
-template <bool STATS, bool LISTOUT = false>
-__device__ __forceinline__ void pull_words_lockstep(const Params &p, WarpSmem &wsm, long long w0, int sw,
-                                           const uint32_t *vis, uint32_t *vis_next, int r,
-                                           WarpState &ws, int nb = 0) {
-  const int lane = threadIdx.x & 31;
-  SweepSmem &w = wsm.u.s;
-  const long long word = w0 + lane;
-  const bool mine = lane < sw && word < p.nwords;
-  const uint32_t vw = mine ? vis[word] : FULL;
-  const uint32_t skip = mine ? (vw | __ldg(p.nin + word)) : FULL;
-  if (STATS && mine) ws.ab += 12;  // visited + no-in words read, next visited word written
-  if (!__any_sync(FULL, skip != FULL)) {  // nothing to pull: carry the words over
-    if (mine) vis_next[word] = vw;
-    return;
-  }
-  const int cnt = warp_gather(w, w0, ~skip);
-  w.found[lane] = 0;
-  __syncwarp();
-  if (STATS && lane == 0) ws.swept += cnt;
-  for (int c0 = 0; c0 < cnt; c0 += 32 * PCH) {
-    uint32_t v[PCH], par[PCH], dgo[PCH];
-    long long js[PCH];
-    int rem[PCH];
-    uint4 h[PCH];
-    if (GBBS_PULL_PF) {  // the next batch's hot records, into L2 while this one runs
-#pragma unroll
-      for (int q = 0; q < PCH; q++) {
-        const int i = c0 + 32 * PCH + 32 * q + lane;
-        if (i < cnt) prefetch_l2(p.phot + w.cand[i]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < PCH; q++) {
-      const int i = c0 + 32 * q + lane;
-      v[q] = i < cnt ? w.cand[i] : 0;
-      h[q] = make_uint4(INF, INF, INF, 0);
-      if (i < cnt) h[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.phot + v[q]));
-    }
-    bool any2 = false;
-#pragma unroll
-    for (int q = 0; q < PCH; q++) {
-      par[q] = INF;
-      js[q] = 0;
-      rem[q] = 0;
-      dgo[q] = h[q].w;  // out-degree an acquisition adds to the next round's edges
-      if (STATS && c0 + 32 * q + lane < cnt) {
-        ws.ab += 16;  // hot record
-        ws.edges += 1;
-      }
-      if (h[q].x != INF && vbit(vis, h[q].x)) {
-        par[q] = h[q].x;
-        if (STATS) ws.hh += 1;
-      }
-      any2 |= par[q] == INF && h[q].y != INF;
-    }
-    if (__any_sync(FULL, any2)) {
-      // in1, in2 probed together with the cold record's load (in3, in4, tail)
-      uint4 cr[PCH];
-      bool m2[PCH];
-#pragma unroll
-      for (int q = 0; q < PCH; q++) {
-        m2[q] = par[q] == INF && h[q].y != INF;
-        cr[q] = make_uint4(INF, INF, 0, 0);
-        if (m2[q] && h[q].z != INF)
-          cr[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pcold + v[q]));
-      }
-#pragma unroll
-      for (int q = 0; q < PCH; q++) {
-        if (!m2[q]) continue;
-        const bool b1 = vbit(vis, h[q].y);
-        const bool b2 = h[q].z != INF && vbit(vis, h[q].z);
-        if (STATS) ws.edges += (b1 || h[q].z == INF) ? 1 : 2;
-        par[q] = b1 ? h[q].y : (b2 ? h[q].z : INF);
-      }
-#pragma unroll
-      for (int q = 0; q < PCH; q++) {
-        if (!m2[q] || par[q] != INF || h[q].z == INF) continue;
-        if (STATS) ws.ab += 16;  // cold record
-        const bool b3 = cr[q].x != INF && vbit(vis, cr[q].x);
-        const bool b4 = cr[q].y != INF && vbit(vis, cr[q].y);
-        if (STATS) ws.edges += (cr[q].x == INF) ? 0 : ((b3 || cr[q].y == INF) ? 1 : 2);
-        par[q] = b3 ? cr[q].x : (b4 ? cr[q].y : INF);
-        const unsigned long long tail = ((unsigned long long)cr[q].w << 32) | cr[q].z;
-        if (par[q] == INF && tail != 0) {
-          js[q] = (long long)(tail >> 24);
-          rem[q] = (int)(tail & 0xFFFFFFull);
-          if (rem[q] == 0xFFFFFF) rem[q] = (int)(ld_stream64(p.in_off + v[q] + 1) - js[q]);
-        }
-      }
-    }
-    bool anyrem = false;
-#pragma unroll
-    for (int q = 0; q < PCH; q++) anyrem |= rem[q] > 0;
-    if (__any_sync(FULL, anyrem)) {
-      for (int step = 0; step < PULL_STEPS; step++) {
-        uint4 g[PCH];
-#pragma unroll
-        for (int q = 0; q < PCH; q++)
-          if (rem[q] > 0) {
-            GBBS_CHECK(js[q] >= 0 && js[q] < p.m);
-            g[q] = ldg_v4(p.in_tgt + (js[q] & ~3ll));
-          }
-        bool live = false;
-#pragma unroll
-        for (int q = 0; q < PCH; q++) {
-          if (rem[q] <= 0) continue;
-          const int lo = (int)(js[q] & 3);
-          const int hi = min(4, lo + rem[q]);
-          const uint32_t e[4] = {g[q].x, g[q].y, g[q].z, g[q].w};
-          bool b[4];
-#pragma unroll
-          for (int k = 0; k < 4; k++) b[k] = (k >= lo && k < hi) ? vbit(vis, e[k]) : false;
-          uint32_t hit = INF;
-#pragma unroll
-          for (int k = 3; k >= 0; k--)
-            if (b[k]) hit = e[k];
-          if (STATS) {
-            ws.edges += hi - lo;
-            ws.ab += 16;
-          }
-          js[q] += hi - lo;
-          rem[q] -= hi - lo;
-          if (hit != INF) {
-            par[q] = hit;
-            rem[q] = 0;
-          }
-          live |= rem[q] > 0;
-        }
-        if (!__any_sync(FULL, live)) break;
-      }
-    }
-    // short remainders: per lane; long remainders: the whole warp, one vertex at a time
-#pragma unroll
-    for (int q = 0; q < PCH; q++) {
-      for (;;) {
-        const bool go = rem[q] > 0 && rem[q] <= LONG_IN;
-        if (!__any_sync(FULL, go)) break;
-        if (go) {
-          GBBS_CHECK(js[q] >= 0 && js[q] < p.m);
-          const uint4 g = ldg_v4(p.in_tgt + (js[q] & ~3ll));
-          const int lo = (int)(js[q] & 3);
-          const int hi = min(4, lo + rem[q]);
-          const uint32_t e[4] = {g.x, g.y, g.z, g.w};
-          uint32_t hit = INF;
-#pragma unroll
-          for (int k = 3; k >= 0; k--)
-            if (k >= lo && k < hi && vbit(vis, e[k])) hit = e[k];
-          if (STATS) {
-            ws.edges += hi - lo;
-            ws.ab += 16;
-          }
-          js[q] += hi - lo;
-          rem[q] -= hi - lo;
-          if (hit != INF) {
-            par[q] = hit;
-            rem[q] = 0;
-          }
-        }
-      }
-      unsigned longs = __ballot_sync(FULL, rem[q] > LONG_IN);
-      while (longs) {
-        const int l = __ffs(longs) - 1;
-        longs &= longs - 1;
-        long long a = __shfl_sync(FULL, js[q], l);
-        const long long e_end = a + __shfl_sync(FULL, rem[q], l);
-        uint32_t found = INF;
-        // groups of 128 in-edges per step: a 16-byte load per lane, then the probes
-        while (a < e_end) {
-          const long long a0 = a & ~3ll;
-          const long long gk = a0 + 4 * lane;
-          uint32_t hit = INF;
-          if (gk < e_end) {
-            GBBS_CHECK(gk >= 0 && gk < p.m);
-            const uint4 g = ldg_v4(p.in_tgt + gk);
-            const uint32_t e[4] = {g.x, g.y, g.z, g.w};
-#pragma unroll
-            for (int k = 3; k >= 0; k--)
-              if (gk + k >= a && gk + k < e_end && vbit(vis, e[k])) hit = e[k];
-            if (STATS) ws.ab += 16;
-          }
-          if (STATS && lane == 0) ws.edges += min(a0 + 128, e_end) - a;
-          const unsigned hb = __ballot_sync(FULL, hit != INF);  // first hit in CSC order
-          if (hb) {
-            found = __shfl_sync(FULL, hit, __ffs(hb) - 1);
-            break;
-          }
-          a = a0 + 128;
-        }
-        if (lane == l) {
-          rem[q] = 0;
-          par[q] = found;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < PCH; q++) {
-      ws.A += __popc(__ballot_sync(FULL, par[q] != INF));
-      if (par[q] != INF) {
-        const uint32_t vq = v[q];
-        if (STATS && (!LISTOUT || dgo[q] == 0)) ws.acquired += 1;  // LISTOUT: staged ones at flush
-#ifndef GBBS_DIAG_NOSTATE  // diagnostic builds (results invalid): cost of the state writes
-        bfs_set_dist(p, vq, (uint32_t)(r + 1));
-        if (p.parent) st_stream(p.parent + vq, par[q]);
-#endif
-        atomicOr(&w.found[(vq >> 5) - (uint32_t)w0], 1u << (vq & 31));
-        if (!LISTOUT && dgo[q] > 0) {
-          ws.K += 1;
-          ws.D += dgo[q];
-        }
-      }
-    }
-    if (LISTOUT) {
-#pragma unroll
-      for (int q = 0; q < PCH; q++) {
-        const bool stg = par[q] != INF && dgo[q] > 0;
-        const unsigned b = __ballot_sync(FULL, stg);
-        GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
-        if (stg) wsm.stage[ws.scnt + __popc(b & lanemask_lt())] = v[q];
-        ws.scnt += __popc(b);
-      }
-      if (ws.scnt > WCAP - 32 * PCH) {
-        if (STATS && (threadIdx.x & 31) == 0) ws.acquired += ws.scnt;
-        warp_flush<ALGO_BFS>(p, wsm.stage, ws.scnt, nb, r, nullptr, nullptr, nullptr,
-                             STATS ? &ws.ab : nullptr);
-        ws.scnt = 0;
-      }
-    }
-  }
-  __syncwarp();
-  if (mine) vis_next[word] = vw | w.found[lane];
-  __syncwarp();
-}
-
-// ---- phased pull ---------------------------------------------------------------------
-// The same scan, run as three passes over the unit's candidates with the survivors
-// of each pass compacted in place in w.cand, so that every pass runs with full
-// warps instead of the whole batch waiting for its longest in-list:
+//
+// The scan runs as three passes over the unit's candidates with the survivors of
+// each pass compacted in place in w.cand, so that every pass runs with full warps
+// instead of a whole batch waiting for its longest in-list (the lock-step batch it
+// replaced: c5 +0.7 %, c2 +8 %):
 //   pass 1  hot record, probe in0                      (every candidate)
 //   pass 2  probes in1, in2 + cold record, in3, in4    (candidates in0 did not decide)
 //   pass 3  the tail from in-edge 5 on, 16-byte groups (candidates in0..in4 did not decide)
 // Per candidate the in-edges are examined in the same CSC order with the same
 // early exit; a pass re-reads its record from L2 instead of carrying
 // it in shared memory (not counted as algorithmic bytes: the scan needs it once).
-#ifndef GBBS_PULL_PHASED
-#define GBBS_PULL_PHASED 1
-#endif
 #ifndef GBBS_PULL_P1
 #define GBBS_PULL_P1 4
 #endif
@@ -1655,9 +1420,9 @@ __device__ __forceinline__ void pull_commit(const Params &p, WarpSmem &wsm, long
 }
 
 template <bool STATS, bool LISTOUT = false>
-__device__ __forceinline__ void pull_words_phased(const Params &p, WarpSmem &wsm, long long w0,
-                                                  int sw, const uint32_t *vis, uint32_t *vis_next,
-                                                  int r, WarpState &ws, int nb = 0) {
+__device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
+                                           const uint32_t *vis, uint32_t *vis_next, int r,
+                                           WarpState &ws, int nb = 0) {
   const int lane = threadIdx.x & 31;
   SweepSmem &w = wsm.u.s;
   const long long word = w0 + lane;
@@ -1902,16 +1667,6 @@ __device__ __forceinline__ void pull_words_phased(const Params &p, WarpSmem &wsm
   __syncwarp();
   if (mine) vis_next[word] = vw | w.found[lane];
   __syncwarp();
-}
-
-template <bool STATS, bool LISTOUT = false>
-__device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long long w0, int sw,
-                                           const uint32_t *vis, uint32_t *vis_next, int r,
-                                           WarpState &ws, int nb = 0) {
-  if (GBBS_PULL_PHASED)
-    pull_words_phased<STATS, LISTOUT>(p, wsm, w0, sw, vis, vis_next, r, ws, nb);
-  else
-    pull_words_lockstep<STATS, LISTOUT>(p, wsm, w0, sw, vis, vis_next, r, ws, nb);
 }
 
 // ---- light pull: a dense round with few candidates left -----------------------------

@@ -27,6 +27,7 @@ ARRAYS = [  # (name, regex on the source line) — first match wins, order matte
     ("in-offsets (in_off)", r"\bin_off\b"),
     ("no-in-edge mask (nin)", r"\bnin\b"),
     ("isolated mask (iso)", r"\biso\b"),
+    ("level bytes (lvl)", r"\blvl\b|\bbfs_set_dist\("),
     ("dist", r"\bp\.dist\b|\bdist \+"),
     ("parent", r"\bp\.parent\b"),
     ("shadow", r"\bshadow\b"),
