@@ -562,6 +562,7 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
         fv[pos] = CARRY ? ld_relaxed(p.dist + vv[u]) : vv[u];
         fo[pos] = o;
         fb[pos] = lo[u] - o;
+        if (GBBS_PF_TGT && ALGO == ALGO_BFS && cnt <= 64) prefetch_l2(p.tgt + lo[u]);
       } else if (!CARRY && (ALGO == ALGO_BF || ALGO == ALGO_WP) && i < cnt) {
         // out-degree-0 vertex: it never enters a frontier; release its TS bit.
         atomicAnd(bits_next + (vv[u] >> 5), ~(1u << (vv[u] & 31)));
@@ -884,6 +885,7 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       const unsigned b = __ballot_sync(FULL, win[j]);
       GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
       if (win[j]) st[ws.scnt + __popc(b & lanemask_lt())] = vv[j];
+      if (GBBS_PF_OFF && ALGO == ALGO_BFS && win[j]) prefetch_l2(p.off + vv[j]);
       ws.scnt += __popc(b);
     }
     if (ws.scnt > WCAP - 32 * NB) {
@@ -1326,6 +1328,15 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #endif
 #ifndef GBBS_LIST_DYNQ_BFS
 #define GBBS_LIST_DYNQ_BFS 0
+#endif
+// latency knobs of small rounds: L2 prefetch of a winner's offset pair when it is
+// staged (the flush loads it), and of an entry's first target line when it is written
+// (the next round's tile loads it)
+#ifndef GBBS_PF_OFF
+#define GBBS_PF_OFF 0
+#endif
+#ifndef GBBS_PF_TGT
+#define GBBS_PF_TGT 0
 #endif
 // words per dynamically assigned sweep unit (0 = sweep_unit's); measured (c2/c4/c5
 // BFS): 32 beats 16 and 8 by 2-5 % and 4 by 20 %; the queue itself -17 % on c4/c5
