@@ -66,6 +66,8 @@ struct gbbs_graph {
   bool own_off = true, own_tgt = true, own_wgt = true;
   uint4 *phot = nullptr;     // pull records: (in0, in1, in2, out-degree)
   uint4 *pcold = nullptr;    //               (in3, in4, tail)
+  uint2 *phot8 = nullptr;    // GBBS_REC8 layout (traverse.cuh Params)
+  uint4 *pc32 = nullptr;
   uint32_t *nin = nullptr;   // no-in-edge mask (+ padding)
   long long ncand = 0;       // vertices with at least one in-edge
   uint16_t *shadow = nullptr;  // 16-bit distance shadow (BF / widest path)
@@ -138,6 +140,8 @@ static void free_graph(gbbs_graph *g) {
   if (g->own_wgt) cudaFree(g->wgt);
   cudaFree(g->phot);
   cudaFree(g->pcold);
+  cudaFree(g->phot8);
+  cudaFree(g->pc32);
   cudaFree(g->nin);
   cudaFree(g->shadow);
   if (g->in_off && g->in_off != g->off) cudaFree(g->in_off);
@@ -254,7 +258,8 @@ __global__ void k_isolated(const long long *off, const long long *in_off, long l
 // act as the frontier, reading R2).  *ncand counts the others.
 __global__ void k_pull_records(const long long *off, const long long *in_off,
                                const uint32_t *in_tgt, long long n, long long nwords, uint4 *hot,
-                               uint4 *cold, uint32_t *nin, unsigned long long *ncand) {
+                               uint4 *cold, uint32_t *nin, unsigned long long *ncand,
+                               uint2 *hot8, uint4 *c32) {
   long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if ((v >> 5) >= nwords) return;
   bool none = true;
@@ -267,8 +272,15 @@ __global__ void k_pull_records(const long long *off, const long long *in_off,
     for (int k = 0; k < 5; k++) x[k] = k < d ? in_tgt[a + k] : INF;
     const unsigned long long tail =
         d > 5 ? ((unsigned long long)(a + 5) << 24) | (unsigned long long)min(d - 5, 0xFFFFFFll) : 0ull;
-    hot[v] = make_uint4(x[0], x[1], x[2], (uint32_t)min(od, 0xFFFFFFFFll));
-    cold[v] = make_uint4(x[3], x[4], (uint32_t)(tail & 0xFFFFFFFFull), (uint32_t)(tail >> 32));
+    if (hot8) {
+      const uint32_t od31 = (uint32_t)min(od, 0x7FFFFFFFll);
+      hot8[v] = make_uint2(x[0], od31 | (d > 1 ? 0x80000000u : 0u));
+      c32[2 * v] = make_uint4(x[1], x[2], x[3], x[4]);
+      c32[2 * v + 1] = make_uint4((uint32_t)(tail & 0xFFFFFFFFull), (uint32_t)(tail >> 32), od31, 0u);
+    } else {
+      hot[v] = make_uint4(x[0], x[1], x[2], (uint32_t)min(od, 0xFFFFFFFFll));
+      cold[v] = make_uint4(x[3], x[4], (uint32_t)(tail & 0xFFFFFFFFull), (uint32_t)(tail >> 32));
+    }
   }
   const unsigned bb = __ballot_sync(0xffffffffu, none);
   if ((threadIdx.x & 31) == 0) {
@@ -429,11 +441,17 @@ static int create_impl(long long n, long long m, const int64_t *offsets, const u
   CU(cudaGetLastError());
   CU(cudaMalloc(&g->cnt, CNT_WORDS * 8));  // ring[4], status, rounds, count, -, heavy[2], wq[8], acq[4]
   CU(cudaMemset(g->cnt, 0, CNT_WORDS * 8));
-  CU(cudaMalloc(&g->phot, (size_t)n * 16));
-  CU(cudaMalloc(&g->pcold, (size_t)n * 16));
+  if (GBBS_REC8) {
+    CU(cudaMalloc(&g->phot8, (size_t)n * 8));
+    CU(cudaMalloc(&g->pc32, (size_t)n * 32));
+  } else {
+    CU(cudaMalloc(&g->phot, (size_t)n * 16));
+    CU(cudaMalloc(&g->pcold, (size_t)n * 16));
+  }
   CU(cudaMalloc(&g->nin, (size_t)g->nwords * 4));
   k_pull_records<<<(unsigned)((g->nwords * 32 + 255) / 256), 256>>>(
-      g->off, g->in_off, g->in_tgt, n, g->nwords, g->phot, g->pcold, g->nin, g->cnt + 6);
+      g->off, g->in_off, g->in_tgt, n, g->nwords, g->phot, g->pcold, g->nin, g->cnt + 6, g->phot8,
+      g->pc32);
   CU(cudaGetLastError());
   CU(cudaMemcpy(&g->ncand, g->cnt + 6, 8, cudaMemcpyDeviceToHost));
   g->status = (int *)(g->cnt + 4);
@@ -799,6 +817,8 @@ static void fill_params(gbbs_graph *g, int algo, uint32_t src, uint32_t *ddist, 
   p.nin = g->nin;
   p.phot = g->phot;
   p.pcold = g->pcold;
+  p.phot8 = g->phot8;
+  p.pc32 = g->pc32;
   p.ncand = g->ncand;
   p.rules = (int)o.rules;
   p.shadow = g->shadow;

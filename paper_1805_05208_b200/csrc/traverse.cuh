@@ -76,6 +76,15 @@ constexpr int TE = GBBS_TE;           // edges per warp tile (edgeMapBlocked bsi
 #define GBBS_NCH 4
 #endif
 constexpr int NCH = GBBS_NCH;         // 32-edge chunks in flight per batch
+// latency knobs of small rounds: L2 prefetch of a winner's offset pair when it is
+// staged (the flush loads it), and of an entry's first target line when it is written
+// (the next round's tile loads it)
+#ifndef GBBS_PF_OFF
+#define GBBS_PF_OFF 0
+#endif
+#ifndef GBBS_PF_TGT
+#define GBBS_PF_TGT 0
+#endif
 // single-owner list-push tiles of the weighted algorithms read targets and weights
 // as 16-byte groups (push_tile): c4 Bellman-Ford -8 %; for BFS it measured +0.4..1.5 %
 #ifndef GBBS_VEC_TILE
@@ -136,6 +145,11 @@ struct Params {
   const uint32_t *nin;       // [nwords] no in-edges (+padding): never a pull candidate
   const uint4 *phot;         // [n] pull records (in0, in1, in2, out-degree), gbbs.cu k_pull_records
   const uint4 *pcold;        // [n]              (in3, in4, tail offset << 24 | tail count)
+  // GBBS_REC8 layout: 8-byte hot records (in0, out-degree saturated to 31 bits | bit 31:
+  // more in-edges), four per sector, and one 32-byte cold record per vertex:
+  // (in1, in2, in3, in4) (tail lo, tail hi, out-degree, 0)
+  const uint2 *phot8;        // [n]
+  const uint4 *pc32;         // [2n]
   long long ncand;           // vertices with at least one in-edge
   uint32_t *dist;            // [n]
   uint16_t *shadow;          // [n] BF/WP: 16-bit conservative copy of dist
@@ -1329,15 +1343,6 @@ __device__ __forceinline__ void forward_words(const Params &p, WarpSmem &wsm, Wa
 #ifndef GBBS_LIST_DYNQ_BFS
 #define GBBS_LIST_DYNQ_BFS 0
 #endif
-// latency knobs of small rounds: L2 prefetch of a winner's offset pair when it is
-// staged (the flush loads it), and of an entry's first target line when it is written
-// (the next round's tile loads it)
-#ifndef GBBS_PF_OFF
-#define GBBS_PF_OFF 0
-#endif
-#ifndef GBBS_PF_TGT
-#define GBBS_PF_TGT 0
-#endif
 // words per dynamically assigned sweep unit (0 = sweep_unit's); measured (c2/c4/c5
 // BFS): 32 beats 16 and 8 by 2-5 % and 4 by 20 %; the queue itself -17 % on c4/c5
 #ifndef GBBS_PULL_SW
@@ -1391,6 +1396,9 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4
 // it in shared memory (not counted as algorithmic bytes: the scan needs it once).
 #ifndef GBBS_PULL_P1
 #define GBBS_PULL_P1 4
+#endif
+#ifndef GBBS_REC8
+#define GBBS_REC8 0
 #endif
 constexpr int P1CH = GBBS_PULL_P1;
 
@@ -1459,7 +1467,10 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
 #pragma unroll
       for (int q = 0; q < P1CH; q++) {
         const int i = c0 + 32 * P1CH + 32 * q + lane;
-        if (i < cnt) prefetch_l2(p.phot + w.cand[i]);
+        if (i < cnt) {
+          if (GBBS_REC8) prefetch_l2(p.phot8 + w.cand[i]);
+          else prefetch_l2(p.phot + w.cand[i]);
+        }
       }
     }
 #pragma unroll
@@ -1467,14 +1478,21 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
       const int i = c0 + 32 * q + lane;
       v[q] = i < cnt ? w.cand[i] : 0;
       h[q] = make_uint4(INF, INF, INF, 0);
-      if (i < cnt) h[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.phot + v[q]));
+      if (GBBS_REC8) {
+        if (i < cnt) {
+          const uint2 t = ld_stream_v2(reinterpret_cast<const uint32_t *>(p.phot8 + v[q]));
+          h[q] = make_uint4(t.x, (t.y >> 31) ? 0u : INF, INF, t.y & 0x7FFFFFFFu);  // y: "has in1" flag
+        }
+      } else if (i < cnt) {
+        h[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.phot + v[q]));
+      }
     }
     __syncwarp();  // the batch's candidates are in registers: survivors may overwrite them
 #pragma unroll
     for (int q = 0; q < P1CH; q++) {
       if (c0 + 32 * q >= cnt) break;
       if (STATS && c0 + 32 * q + lane < cnt) {
-        ws.ab += 16;  // hot record
+        ws.ab += GBBS_REC8 ? 8 : 16;  // hot record
         ws.edges += 1;
       }
       const bool hit = h[q].x != INF && vbit(vis, h[q].x);
@@ -1499,12 +1517,25 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
       const int i = c0 + 32 * q + lane;
       v[q] = i < ns ? w.cand[i] : 0;
       h[q] = make_uint4(INF, INF, INF, 0);
-      if (i < ns) h[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.phot + v[q]));
+      if (GBBS_REC8) {
+        cr[q] = make_uint4(INF, INF, 0, 0);
+        if (i < ns) {  // one sector: (in1, in2, in3, in4) (tail, out-degree)
+          const uint4 c0r = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pc32 + 2 * (size_t)v[q]));
+          const uint4 c1r = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pc32 + 2 * (size_t)v[q] + 1));
+          h[q] = make_uint4(0u, c0r.x, c0r.y, c1r.z);
+          cr[q] = make_uint4(c0r.z, c0r.w, c1r.x, c1r.y);
+          if (STATS) ws.ab += 32;
+        }
+      } else if (i < ns) {
+        h[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.phot + v[q]));
+      }
     }
+    if (!GBBS_REC8) {
 #pragma unroll
-    for (int q = 0; q < PCH; q++) {
-      cr[q] = make_uint4(INF, INF, 0, 0);
-      if (h[q].z != INF) cr[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pcold + v[q]));
+      for (int q = 0; q < PCH; q++) {
+        cr[q] = make_uint4(INF, INF, 0, 0);
+        if (h[q].z != INF) cr[q] = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pcold + v[q]));
+      }
     }
     __syncwarp();
 #pragma unroll
@@ -1520,7 +1551,7 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
     for (int q = 0; q < PCH; q++) {
       need[q] = false;
       if (h[q].y == INF || par[q] != INF || h[q].z == INF) continue;
-      if (STATS) ws.ab += 16;  // cold record
+      if (STATS && !GBBS_REC8) ws.ab += 16;  // cold record
       const bool b3 = cr[q].x != INF && vbit(vis, cr[q].x);
       const bool b4 = cr[q].y != INF && vbit(vis, cr[q].y);
       if (STATS) ws.edges += (cr[q].x == INF) ? 0 : ((b3 || cr[q].y == INF) ? 1 : 2);
@@ -1556,8 +1587,15 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
       rem[q] = 0;
       dgo[q] = 0;
       if (i < nt) {
-        const uint2 t = ld_stream_v2(reinterpret_cast<const uint32_t *>(p.pcold + v[q]) + 2);
-        dgo[q] = ld_stream(reinterpret_cast<const uint32_t *>(p.phot + v[q]) + 3);
+        uint2 t;
+        if (GBBS_REC8) {
+          const uint4 c1r = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pc32 + 2 * (size_t)v[q] + 1));
+          t = make_uint2(c1r.x, c1r.y);
+          dgo[q] = c1r.z;
+        } else {
+          t = ld_stream_v2(reinterpret_cast<const uint32_t *>(p.pcold + v[q]) + 2);
+          dgo[q] = ld_stream(reinterpret_cast<const uint32_t *>(p.phot + v[q]) + 3);
+        }
         const unsigned long long tail = ((unsigned long long)t.y << 32) | t.x;
         js[q] = (long long)(tail >> 24);
         rem[q] = (int)(tail & 0xFFFFFFull);
