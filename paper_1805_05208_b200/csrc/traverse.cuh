@@ -76,15 +76,6 @@ constexpr int TE = GBBS_TE;           // edges per warp tile (edgeMapBlocked bsi
 #define GBBS_NCH 4
 #endif
 constexpr int NCH = GBBS_NCH;         // 32-edge chunks in flight per batch
-// latency knobs of small rounds: L2 prefetch of a winner's offset pair when it is
-// staged (the flush loads it), and of an entry's first target line when it is written
-// (the next round's tile loads it)
-#ifndef GBBS_PF_OFF
-#define GBBS_PF_OFF 0
-#endif
-#ifndef GBBS_PF_TGT
-#define GBBS_PF_TGT 0
-#endif
 // single-owner list-push tiles of the weighted algorithms read targets and weights
 // as 16-byte groups (push_tile): c4 Bellman-Ford -8 %; for BFS it measured +0.4..1.5 %
 #ifndef GBBS_VEC_TILE
@@ -576,7 +567,6 @@ __device__ __forceinline__ void warp_flush(const Params &p, const uint32_t *st, 
         fv[pos] = CARRY ? ld_relaxed(p.dist + vv[u]) : vv[u];
         fo[pos] = o;
         fb[pos] = lo[u] - o;
-        if (GBBS_PF_TGT && ALGO == ALGO_BFS && cnt <= 64) prefetch_l2(p.tgt + lo[u]);
       } else if (!CARRY && (ALGO == ALGO_BF || ALGO == ALGO_WP) && i < cnt) {
         // out-degree-0 vertex: it never enters a frontier; release its TS bit.
         atomicAnd(bits_next + (vv[u] >> 5), ~(1u << (vv[u] & 31)));
@@ -899,7 +889,6 @@ __device__ __forceinline__ void apply_batch(const Params &p, uint32_t *st, WarpS
       const unsigned b = __ballot_sync(FULL, win[j]);
       GBBS_CHECK(ws.scnt + __popc(b) <= WCAP);
       if (win[j]) st[ws.scnt + __popc(b & lanemask_lt())] = vv[j];
-      if (GBBS_PF_OFF && ALGO == ALGO_BFS && win[j]) prefetch_l2(p.off + vv[j]);
       ws.scnt += __popc(b);
     }
     if (ws.scnt > WCAP - 32 * NB) {
@@ -1369,6 +1358,13 @@ constexpr int PCH = GBBS_PCH;
 __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4(p); }
 
 
+// Pull records (gbbs.cu k_pull_records), GBBS_REC8 layout: the hot record is 8 bytes —
+// (in0, out-degree | "has more in-edges" in bit 31), four per 32-byte sector — and is
+// all that pass 1 reads; the cold record is one sector per vertex — (in1, in2, in3,
+// in4) (tail, out-degree) — read by pass 2 in two 16-byte loads, so a candidate in0
+// does not decide costs one more sector instead of a re-read of the hot record plus
+// the cold one.  The text below describes the older 16 + 16-byte pair (GBBS_REC8 = 0).
+//
 // Candidates = the unit's vertices that are unvisited and have in-edges (the
 // no-in-edge mask nin removes vertices no pull can ever acquire).  A candidate's
 // first five in-edges in CSC order come from its pull records (gbbs.cu
@@ -1397,8 +1393,10 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4
 #ifndef GBBS_PULL_P1
 #define GBBS_PULL_P1 4
 #endif
+// pull-record layout: 1 = 8-byte hot + 32-byte cold records (c5 -4 %, c4 -6 % against
+// the 16-byte hot / 16-byte cold pair, 0, kept for A/B)
 #ifndef GBBS_REC8
-#define GBBS_REC8 0
+#define GBBS_REC8 1
 #endif
 constexpr int P1CH = GBBS_PULL_P1;
 
