@@ -134,3 +134,29 @@ def test_rules_on_and_off_together_rejected(G):
     with pytest.raises(Exception):
         g.bfs(0, d, None, opts=G.make_opts(rules=G.GBBS_RULE_LEVEL_BYTES_ON | G.GBBS_RULE_LEVEL_BYTES_OFF))
     g.close()
+
+
+def test_pull_record_boundaries(G):
+    """In-degrees 1..14 with the only reachable in-neighbour LAST in CSC order: the pull
+    must walk the hot record (in0), the cold record (in1..in4) and the tail (in5..)
+    in order and take that neighbour as the parent; dead in-neighbours
+    have lower ids, so they come first in every in-list."""
+    ndead, K = 20, 14
+    A = ndead + 1
+    n = A + 1 + K
+    edges = [(0, A)]
+    for k in range(1, K + 1):
+        t = A + k
+        edges += [(d, t) for d in range(1, k)]  # k - 1 unreachable in-neighbours
+        edges.append((A, t))
+    off, tgt = graphgen.from_edge_list(n, edges, symmetric=False)
+    ref, _ = oracle.bfs(off, tgt, 0)
+    assert ref[A] == 1 and (ref[A + 1:] == 2).all() and (ref[1:A] == 0xFFFFFFFF).all()
+    g = G.Graph(off, tgt, symmetric=False)
+    for on in (True, False):
+        for mode in MODES:
+            d, p = _bfs(G, g, 0, _opts(G, mode, on))
+            assert (d == ref).all(), (on, mode)
+            assert (p[A + 1:] == A).all() and p[A] == 0, (on, mode, p)
+            assert oracle.check_bfs(off, tgt, 0, d, p)[0]
+    g.close()

@@ -21,8 +21,8 @@ import sys
 import tempfile
 
 ARRAYS = [  # (name, regex on the source line) — first match wins, order matters
-    ("pull hot records (phot)", r"\bphot\b"),
-    ("pull cold records (pcold)", r"\bpcold\b"),
+    ("pull hot records (phot)", r"\bphot8?\b"),
+    ("pull cold records (pcold)", r"\bpcold\b|\bpc32\b"),
     ("in-edges (in_tgt)", r"\bin_tgt\b"),
     ("in-offsets (in_off)", r"\bin_off\b"),
     ("no-in-edge mask (nin)", r"\bnin\b"),
