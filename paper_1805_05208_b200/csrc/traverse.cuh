@@ -294,6 +294,13 @@ __device__ __forceinline__ long long ld_stream64(const long long *a) {
   return v;
 }
 
+// one 32-byte (256-bit) load: sm_100's LDG.256 — a whole sector in one L2 request
+__device__ __forceinline__ void ld_stream_v8(const uint32_t *a, uint4 &lo, uint4 &hi) {
+  asm("ld.global.nc.L2::cache_hint.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+      : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+      : "l"(a), "l"(ef_policy()));
+}
+
 __device__ __forceinline__ uint2 ld_stream_v2(const uint32_t *a) {
   uint2 v;
   asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
@@ -1361,7 +1368,7 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4
 // Pull records (gbbs.cu k_pull_records), GBBS_REC8 layout: the hot record is 8 bytes —
 // (in0, out-degree | "has more in-edges" in bit 31), four per 32-byte sector — and is
 // all that pass 1 reads; the cold record is one sector per vertex — (in1, in2, in3,
-// in4) (tail, out-degree) — read by pass 2 in two 16-byte loads, so a candidate in0
+// in4) (tail, out-degree) — read by pass 2 in one 256-bit load, so a candidate in0
 // does not decide costs one more sector instead of a re-read of the hot record plus
 // the cold one.  The text below describes the older 16 + 16-byte pair (GBBS_REC8 = 0).
 //
@@ -1397,6 +1404,11 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t *p) { return ld_stream_v4
 // the 16-byte hot / 16-byte cold pair, 0, kept for A/B)
 #ifndef GBBS_REC8
 #define GBBS_REC8 1
+#endif
+// the cold sector as ONE 256-bit load (LDG.256) instead of two 16-byte loads: c5 -1.0 %,
+// c4 -0.8 %, c2 -2.1 % (0 kept for A/B)
+#ifndef GBBS_LD256
+#define GBBS_LD256 1
 #endif
 constexpr int P1CH = GBBS_PULL_P1;
 
@@ -1518,8 +1530,13 @@ __device__ __forceinline__ void pull_words(const Params &p, WarpSmem &wsm, long 
       if (GBBS_REC8) {
         cr[q] = make_uint4(INF, INF, 0, 0);
         if (i < ns) {  // one sector: (in1, in2, in3, in4) (tail, out-degree)
-          const uint4 c0r = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pc32 + 2 * (size_t)v[q]));
-          const uint4 c1r = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pc32 + 2 * (size_t)v[q] + 1));
+          uint4 c0r, c1r;
+          if (GBBS_LD256) {
+            ld_stream_v8(reinterpret_cast<const uint32_t *>(p.pc32 + 2 * (size_t)v[q]), c0r, c1r);
+          } else {
+            c0r = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pc32 + 2 * (size_t)v[q]));
+            c1r = ld_stream_v4(reinterpret_cast<const uint32_t *>(p.pc32 + 2 * (size_t)v[q] + 1));
+          }
           h[q] = make_uint4(0u, c0r.x, c0r.y, c1r.z);
           cr[q] = make_uint4(c0r.z, c0r.w, c1r.x, c1r.y);
           if (STATS) ws.ab += 32;
